@@ -1,0 +1,377 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU oracle for the SpGEMM path.
+
+Two checkers, both used only by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs (never by the product):
+
+* ``liboracle.so`` — oracle.c, a plain-C restatement of the reference
+  algorithms (each function cites reference file:line);
+* ``_ref/libcspgemm_ref.so`` — the UNMODIFIED reference headers from
+  /root/reference/proj/include compiled by oracle/Makefile (present wherever
+  it was built; it travels to the GPU box with the snapshot).
+
+The restatement is pinned against the reference build and against the
+golden vectors in tests/golden/ (see tests/test_oracle.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from collections import namedtuple
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libcspgemm_ref.so"
+REF_INCLUDE = Path("/root/reference/proj/include")
+
+Csr = namedtuple("Csr", "nrows ncols row_ptr col_idx values")
+
+i32, i64, u64, dbl = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+vp = C.c_void_p
+P = C.POINTER
+
+
+class orc_candidate(C.Structure):
+    _fields_ = [("i", i32), ("j", i32), ("score", dbl)]
+
+
+class orc_access_stats(C.Structure):
+    _fields_ = [("b_row_loads", u64), ("a_inner_iters", u64), ("placeholder_skips", u64)]
+
+
+class orc_cluster(C.Structure):
+    _fields_ = [("nclusters", i64), ("nrows", i64), ("ncols", i64), ("ncolslots", i64),
+                ("nslots", i64), ("cluster_sizes", P(i32)), ("cluster_col_ptr", P(i64)),
+                ("col_idx", P(i32)), ("value_ptr", P(i64)), ("values", P(dbl)),
+                ("valid", P(u64)), ("row_map", P(i32))]
+
+
+CAND = np.dtype([("i", np.int32), ("j", np.int32), ("score", np.float64)])
+
+_orc = None
+_ref = None
+
+
+def build(with_ref: bool = True) -> None:
+    """Build liboracle.so (and oracle/_ref when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", str(HERE), "all"], check=True)
+    if with_ref and REF_INCLUDE.exists():
+        subprocess.run(["make", "-s", "-C", str(HERE), "ref"], check=True)
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+def lib() -> C.CDLL:
+    global _orc
+    if _orc is None:
+        if not ORACLE_SO.exists():
+            build(with_ref=False)
+        l = C.CDLL(str(ORACLE_SO))
+        l.orc_spgemm_symbolic.argtypes = [i64, i64, vp, vp, vp, vp, vp]
+        l.orc_spgemm_rowwise.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp, vp, P(P(i32)), P(P(dbl))]
+        l.orc_spgemm_rowwise.restype = i64
+        l.orc_jaccard.argtypes = [vp, vp, i64, i64]
+        l.orc_jaccard.restype = dbl
+        l.orc_spgemm_topk.argtypes = [i64, vp, vp, vp, vp, i32, dbl, P(P(orc_candidate))]
+        l.orc_spgemm_topk.restype = i64
+        l.orc_build_csr_cluster.argtypes = [i64, i64, vp, vp, vp, i64, vp, vp, P(orc_cluster)]
+        l.orc_cluster_to_csr.argtypes = [P(orc_cluster), vp, P(P(i32)), P(P(dbl))]
+        l.orc_cluster_to_csr.restype = i64
+        l.orc_spgemm_clusterwise.argtypes = [P(orc_cluster), i64, vp, vp, vp, P(orc_cluster),
+                                             P(orc_access_stats)]
+        l.orc_cluster_free.argtypes = [P(orc_cluster)]
+        l.orc_merge_candidates.argtypes = [i64, vp, vp, vp, i64, dbl, i32, vp]
+        l.orc_merge_candidates.restype = i64
+        l.orc_free.argtypes = [vp]
+        _orc = l
+    return _orc
+
+
+def have_ref() -> bool:
+    return REF_SO.exists()
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not REF_SO.exists():
+            raise RuntimeError("oracle/_ref not built (needs /root/reference; run make -C oracle ref)")
+        l = C.CDLL(str(REF_SO))
+        l.ref_last_error.restype = C.c_char_p
+        l.ref_spgemm_rowwise.argtypes = [i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, i64, i64, C.c_int,
+                                         P(i64), P(P(i64)), P(P(i32)), P(P(dbl))]
+        l.ref_spgemm_symbolic.argtypes = [i64, i64, vp, vp, i64, i64, vp, vp, C.c_int, vp]
+        l.ref_spgemm_topk.argtypes = [i64, i64, vp, vp, i32, dbl, C.c_int, P(i64),
+                                      P(P(orc_candidate))]
+        l.ref_hierarchical_clusters.argtypes = [i64, i64, vp, vp, dbl, i32, C.c_int, P(i64),
+                                                P(P(i64)), P(P(i32))]
+        l.ref_variable_length_clusters.argtypes = [i64, i64, vp, vp, dbl, i32, P(i64), P(P(i64)),
+                                                   P(P(i32))]
+        l.ref_spgemm_clusterwise.argtypes = [i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, i64, vp, vp,
+                                             C.c_int, P(i64), P(P(i64)), P(P(i32)), P(P(dbl)),
+                                             vp, P(i64), P(i64)]
+        l.ref_time_clusterwise.argtypes = [i64, i64, vp, vp, vp, i64, vp, vp, C.c_int, C.c_int,
+                                           P(dbl)]
+        l.ref_reorder_rcm.argtypes = [i64, i64, vp, vp, vp]
+        l.ref_reorder_random.argtypes = [i64, u64, vp]
+        l.ref_reorder_degree.argtypes = [i64, i64, vp, vp, vp]
+        l.ref_permute_symmetric.argtypes = [i64, i64, vp, vp, vp, vp, P(P(i64)), P(P(i32)),
+                                            P(P(dbl))]
+        l.ref_jaccard.argtypes = [i64, i64, vp, vp, i64, i64, P(dbl)]
+        l.ref_free.argtypes = [vp]
+        _ref = l
+    return _ref
+
+
+def _arr(ptr, n, dtype, free):
+    out = np.ctypeslib.as_array(ptr, shape=(n,)).copy() if n else np.zeros(0, dtype)
+    free(C.cast(ptr, vp))
+    return out.astype(dtype, copy=False)
+
+
+def _csr_args(a):
+    return (np.ascontiguousarray(a.row_ptr, np.int64), np.ascontiguousarray(a.col_idx, np.int32),
+            np.ascontiguousarray(a.values, np.float64))
+
+
+# ---------------------------------------------------------------- restatement
+def spgemm_symbolic(a, b) -> np.ndarray:
+    arp, aci, _ = _csr_args(a)
+    brp, bci, _ = _csr_args(b)
+    out = np.zeros(a.nrows, np.int64)
+    lib().orc_spgemm_symbolic(a.nrows, b.ncols, _p(arp), _p(aci), _p(brp), _p(bci), _p(out))
+    return out
+
+
+def spgemm_rowwise(a, b) -> Csr:
+    arp, aci, av = _csr_args(a)
+    brp, bci, bv = _csr_args(b)
+    crp = np.zeros(a.nrows + 1, np.int64)
+    cc, cv = P(i32)(), P(dbl)()
+    nnz = lib().orc_spgemm_rowwise(a.nrows, b.ncols, _p(arp), _p(aci), _p(av), _p(brp), _p(bci),
+                                   _p(bv), _p(crp), C.byref(cc), C.byref(cv))
+    return Csr(a.nrows, b.ncols, crp, _arr(cc, nnz, np.int32, lib().orc_free),
+               _arr(cv, nnz, np.float64, lib().orc_free))
+
+
+def transpose_pattern(a):
+    """Pattern transpose (stable; rows sorted) in numpy."""
+    rows = np.repeat(np.arange(a.nrows, dtype=np.int64), np.diff(a.row_ptr))
+    order = np.lexsort((rows, a.col_idx))
+    cols_t = rows[order].astype(np.int32)
+    cnt = np.bincount(a.col_idx, minlength=a.ncols)
+    rp = np.zeros(a.ncols + 1, np.int64)
+    rp[1:] = np.cumsum(cnt)
+    return Csr(a.ncols, a.nrows, rp, cols_t, np.ones(cols_t.size))
+
+
+def spgemm_topk(a, topk: int, jacc_th: float) -> np.ndarray:
+    arp, aci, _ = _csr_args(a)
+    at = transpose_pattern(a)
+    out = P(orc_candidate)()
+    n = lib().orc_spgemm_topk(a.nrows, _p(arp), _p(aci), _p(at.row_ptr), _p(at.col_idx), topk,
+                              jacc_th, C.byref(out))
+    res = np.zeros(n, CAND)
+    if n:
+        raw = C.cast(out, P(C.c_char * (n * CAND.itemsize))).contents
+        res = np.frombuffer(bytes(raw), dtype=CAND).copy()
+    lib().orc_free(C.cast(out, vp))
+    return res
+
+
+def jaccard(a, i: int, j: int) -> float:
+    arp, aci, _ = _csr_args(a)
+    return float(lib().orc_jaccard(_p(arp), _p(aci), i, j))
+
+
+def _cluster_to_dict(c: orc_cluster) -> dict:
+    nc, ncs, ns, n = c.nclusters, c.ncolslots, c.nslots, c.nrows
+    arr = lambda p, k: np.ctypeslib.as_array(p, shape=(max(k, 1),))[:k].copy()
+    d = {"nclusters": nc, "nrows": n, "ncols": c.ncols,
+         "cluster_sizes": arr(c.cluster_sizes, nc), "cluster_col_ptr": arr(c.cluster_col_ptr, nc + 1),
+         "col_idx": arr(c.col_idx, ncs), "value_ptr": arr(c.value_ptr, nc + 1),
+         "values": arr(c.values, ns), "valid": arr(c.valid, (ns + 63) // 64),
+         "row_map": arr(c.row_map, n)}
+    return d
+
+
+def build_csr_cluster(a, cluster_ptr: np.ndarray, rows: np.ndarray) -> dict:
+    arp, aci, av = _csr_args(a)
+    cp = np.ascontiguousarray(cluster_ptr, np.int64)
+    rr = np.ascontiguousarray(rows, np.int32)
+    c = orc_cluster()
+    lib().orc_build_csr_cluster(a.nrows, a.ncols, _p(arp), _p(aci), _p(av), cp.size - 1, _p(cp),
+                                _p(rr), C.byref(c))
+    d = _cluster_to_dict(c)
+    lib().orc_cluster_free(C.byref(c))
+    return d
+
+
+def spgemm_clusterwise(a, cluster_ptr, rows, b):
+    """Returns (cluster_to_csr(C) as Csr, C-format dict, access stats tuple)."""
+    arp, aci, av = _csr_args(a)
+    brp, bci, bv = _csr_args(b)
+    cp = np.ascontiguousarray(cluster_ptr, np.int64)
+    rr = np.ascontiguousarray(rows, np.int32)
+    ac = orc_cluster()
+    lib().orc_build_csr_cluster(a.nrows, a.ncols, _p(arp), _p(aci), _p(av), cp.size - 1, _p(cp),
+                                _p(rr), C.byref(ac))
+    cc = orc_cluster()
+    st = orc_access_stats()
+    lib().orc_spgemm_clusterwise(C.byref(ac), b.ncols, _p(brp), _p(bci), _p(bv), C.byref(cc),
+                                 C.byref(st))
+    crp = np.zeros(a.nrows + 1, np.int64)
+    ci, cv = P(i32)(), P(dbl)()
+    nnz = lib().orc_cluster_to_csr(C.byref(cc), _p(crp), C.byref(ci), C.byref(cv))
+    csr = Csr(a.nrows, b.ncols, crp, _arr(ci, nnz, np.int32, lib().orc_free),
+              _arr(cv, nnz, np.float64, lib().orc_free))
+    d = _cluster_to_dict(cc)
+    lib().orc_cluster_free(C.byref(ac))
+    lib().orc_cluster_free(C.byref(cc))
+    return csr, d, (st.b_row_loads, st.a_inner_iters, st.placeholder_skips)
+
+
+def merge_candidates(a, pairs: np.ndarray, jacc_th: float, max_cluster: int):
+    """Returns (cluster_ptr, rows) of the merge (reference clustering.hpp:122-183)."""
+    arp, aci, _ = _csr_args(a)
+    pr = np.ascontiguousarray(pairs, CAND)
+    cl = np.zeros(a.nrows, np.int32)
+    nc = lib().orc_merge_candidates(a.nrows, _p(arp), _p(aci), _p(pr), pr.size, jacc_th,
+                                    max_cluster, _p(cl))
+    order = np.argsort(cl, kind="stable")
+    ptr = np.zeros(nc + 1, np.int64)
+    ptr[1:] = np.cumsum(np.bincount(cl, minlength=nc))
+    return ptr, order.astype(np.int32)
+
+
+# ------------------------------------------------------------ reference build
+def _ref_check(rc):
+    if rc != 0:
+        msg = ref().ref_last_error().decode()
+        if rc == 1:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+
+def ref_spgemm_rowwise(a, b, r0: int = 0, r1: int | None = None, threads: int = 0) -> Csr:
+    r1 = a.nrows if r1 is None else r1
+    arp, aci, av = _csr_args(a)
+    brp, bci, bv = _csr_args(b)
+    nnz = i64()
+    crp, cci, cv = P(i64)(), P(i32)(), P(dbl)()
+    _ref_check(ref().ref_spgemm_rowwise(a.nrows, a.ncols, _p(arp), _p(aci), _p(av), b.nrows, b.ncols,
+                                        _p(brp), _p(bci), _p(bv), r0, r1, threads, C.byref(nnz),
+                                        C.byref(crp), C.byref(cci), C.byref(cv)))
+    f = ref().ref_free
+    n = nnz.value
+    return Csr(r1 - r0, b.ncols, _arr(crp, r1 - r0 + 1, np.int64, f), _arr(cci, n, np.int32, f),
+               _arr(cv, n, np.float64, f))
+
+
+def ref_spgemm_symbolic(a, b, threads: int = 0) -> np.ndarray:
+    arp, aci, _ = _csr_args(a)
+    brp, bci, _ = _csr_args(b)
+    out = np.zeros(a.nrows, np.int64)
+    _ref_check(ref().ref_spgemm_symbolic(a.nrows, a.ncols, _p(arp), _p(aci), b.nrows, b.ncols,
+                                         _p(brp), _p(bci), threads, _p(out)))
+    return out
+
+
+def ref_spgemm_topk(a, topk: int, jacc_th: float, threads: int = 0) -> np.ndarray:
+    arp, aci, _ = _csr_args(a)
+    n = i64()
+    out = P(orc_candidate)()
+    _ref_check(ref().ref_spgemm_topk(a.nrows, a.ncols, _p(arp), _p(aci), topk, jacc_th, threads,
+                                     C.byref(n), C.byref(out)))
+    cnt = n.value
+    res = np.zeros(cnt, CAND)
+    if cnt:
+        raw = C.cast(out, P(C.c_char * (cnt * CAND.itemsize))).contents
+        res = np.frombuffer(bytes(raw), dtype=CAND).copy()
+    ref().ref_free(C.cast(out, vp))
+    return res
+
+
+def _ref_asg(fn, *args):
+    nc = i64()
+    ptr, rows = P(i64)(), P(i32)()
+    _ref_check(fn(*args, C.byref(nc), C.byref(ptr), C.byref(rows)))
+    p = _arr(ptr, nc.value + 1, np.int64, ref().ref_free)
+    r = _arr(rows, int(p[-1]), np.int32, ref().ref_free)
+    return p, r
+
+
+def ref_hierarchical_clusters(a, jacc_th=0.3, max_cluster=8, threads: int = 0):
+    arp, aci, _ = _csr_args(a)
+    return _ref_asg(ref().ref_hierarchical_clusters, a.nrows, a.ncols, _p(arp), _p(aci), jacc_th,
+                    max_cluster, threads)
+
+
+def ref_variable_length_clusters(a, jacc_th=0.3, max_cluster=8):
+    arp, aci, _ = _csr_args(a)
+    return _ref_asg(ref().ref_variable_length_clusters, a.nrows, a.ncols, _p(arp), _p(aci),
+                    jacc_th, max_cluster)
+
+
+def ref_spgemm_clusterwise(a, cluster_ptr, rows, b, threads: int = 0):
+    arp, aci, av = _csr_args(a)
+    brp, bci, bv = _csr_args(b)
+    cp = np.ascontiguousarray(cluster_ptr, np.int64)
+    rr = np.ascontiguousarray(rows, np.int32)
+    nnz = i64()
+    crp, cci, cv = P(i64)(), P(i32)(), P(dbl)()
+    st = np.zeros(3, np.uint64)
+    slots, colslots = i64(), i64()
+    _ref_check(ref().ref_spgemm_clusterwise(a.nrows, a.ncols, _p(arp), _p(aci), _p(av), b.nrows,
+                                            b.ncols, _p(brp), _p(bci), _p(bv), cp.size - 1, _p(cp),
+                                            _p(rr), threads, C.byref(nnz), C.byref(crp),
+                                            C.byref(cci), C.byref(cv), _p(st), C.byref(slots),
+                                            C.byref(colslots)))
+    f = ref().ref_free
+    n = nnz.value
+    csr = Csr(a.nrows, b.ncols, _arr(crp, a.nrows + 1, np.int64, f), _arr(cci, n, np.int32, f),
+              _arr(cv, n, np.float64, f))
+    return csr, tuple(int(x) for x in st), int(slots.value), int(colslots.value)
+
+
+def ref_reorder_rcm(a) -> np.ndarray:
+    arp, aci, _ = _csr_args(a)
+    out = np.zeros(a.nrows, np.int32)
+    _ref_check(ref().ref_reorder_rcm(a.nrows, a.ncols, _p(arp), _p(aci), _p(out)))
+    return out
+
+
+def ref_reorder_random(n: int, seed: int) -> np.ndarray:
+    out = np.zeros(n, np.int32)
+    _ref_check(ref().ref_reorder_random(n, seed, _p(out)))
+    return out
+
+
+def ref_reorder_degree(a) -> np.ndarray:
+    arp, aci, _ = _csr_args(a)
+    out = np.zeros(a.nrows, np.int32)
+    _ref_check(ref().ref_reorder_degree(a.nrows, a.ncols, _p(arp), _p(aci), _p(out)))
+    return out
+
+
+def ref_permute_symmetric(a, perm) -> Csr:
+    arp, aci, av = _csr_args(a)
+    pp = np.ascontiguousarray(perm, np.int32)
+    rp, ci, v = P(i64)(), P(i32)(), P(dbl)()
+    _ref_check(ref().ref_permute_symmetric(a.nrows, a.ncols, _p(arp), _p(aci), _p(av), _p(pp),
+                                           C.byref(rp), C.byref(ci), C.byref(v)))
+    f = ref().ref_free
+    rpa = _arr(rp, a.nrows + 1, np.int64, f)
+    nnz = int(rpa[-1])
+    return Csr(a.nrows, a.ncols, rpa, _arr(ci, nnz, np.int32, f), _arr(v, nnz, np.float64, f))
+
+
+def ref_jaccard(a, i, j) -> float:
+    arp, aci, _ = _csr_args(a)
+    out = dbl()
+    _ref_check(ref().ref_jaccard(a.nrows, a.ncols, _p(arp), _p(aci), i, j, C.byref(out)))
+    return float(out.value)

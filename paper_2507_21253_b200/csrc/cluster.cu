@@ -1,0 +1,771 @@
+// Cluster-wise SpGEMM on sm_100a and the device CSR_Cluster format.
+//
+// Replaces reference build_csr_cluster (cluster_format.hpp:130-186),
+// cluster_to_csr (:190-233), spgemm_clusterwise (cluster_spgemm.hpp:55-189)
+// and the AccessStats counters (cluster_spgemm.hpp:26-45).
+//
+// Cluster kernel (Algorithm 1 of the paper, B200 form): one CTA owns one
+// cluster of K rows.  For every merged column k of the cluster the B row is
+// loaded from global memory ONCE (coalesced), and each product is scattered
+// to every live member (member_mask bit) as a composite key (member, j) in
+// shared memory.  A stable radix sort by (member, j) followed by ordered run
+// reduction gives, for every member row, exactly the values of the row-wise
+// kernel (contributions still summed in ascending k from 0.0), so C is
+// written directly as CSR over the original row indices and is bit-identical
+// to spgemm_rowwise(cluster_to_csr(A), B).  Singleton clusters and clusters
+// with more than CAP products are routed to the row-wise bins.
+#include "esc.cuh"
+
+#include <algorithm>
+#include <numeric>
+
+namespace bsp {
+
+namespace {
+
+constexpr int MAXK = 32;  // cluster size limit of the device format (member_mask is 32-bit)
+
+struct ClusterMats {
+    const int32_t* __restrict__ sizes;
+    const int64_t* __restrict__ member_ptr;
+    const int64_t* __restrict__ ccp;  // cluster_col_ptr
+    const int32_t* __restrict__ ccol;
+    const int64_t* __restrict__ vptr;
+    const double* __restrict__ aval;
+    const uint32_t* __restrict__ mask;
+    const int32_t* __restrict__ row_map;
+    const int64_t* __restrict__ brp;
+    const int32_t* __restrict__ bcol;
+    const double* __restrict__ bval;
+    int32_t ncols;
+};
+
+// ---------------------------------------------------------------------------
+// format construction: one warp per cluster, K-way merge of member rows
+// ---------------------------------------------------------------------------
+// MODE 0: union size per cluster; MODE 1: write merged columns, values,
+// valid bits and member masks.
+template <int MODE>
+__global__ void build_cluster_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                     const double* __restrict__ val, int64_t ncl,
+                                     const int64_t* __restrict__ mptr,
+                                     const int32_t* __restrict__ rows, int64_t* __restrict__ ucount,
+                                     const int64_t* __restrict__ ccp, const int64_t* __restrict__ vptr,
+                                     int32_t* __restrict__ ocol, double* __restrict__ oval,
+                                     unsigned long long* __restrict__ valid,
+                                     uint32_t* __restrict__ omask) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t{blockDim.x} + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t{gridDim.x} * blockDim.x) >> 5;
+    for (int64_t c = warp; c < ncl; c += nwarps) {
+        const int K = static_cast<int>(mptr[c + 1] - mptr[c]);
+        int64_t cur = 0, end = 0;
+        if (lane < K) {
+            const int32_t r = rows[mptr[c] + lane];
+            cur = rp[r];
+            end = rp[r + 1];
+        }
+        int64_t u = 0;
+        const int64_t cbase = MODE ? ccp[c] : 0;
+        const int64_t vbase = MODE ? vptr[c] : 0;
+        for (;;) {
+            const int32_t mine = (lane < K && cur < end) ? col[cur] : INT32_MAX;
+            const int32_t mn = __reduce_min_sync(0xffffffffu, mine);
+            if (mn == INT32_MAX) break;
+            const bool hit = (mine == mn);
+            const uint32_t who = __ballot_sync(0xffffffffu, hit);
+            if (MODE) {
+                if (lane == 0) {
+                    ocol[cbase + u] = mn;
+                    omask[cbase + u] = who;
+                }
+                if (hit) {
+                    const int64_t slot = vbase + u * K + lane;
+                    oval[slot] = val[cur];
+                    atomicOr(&valid[slot >> 6], 1ull << (slot & 63));
+                }
+            }
+            if (hit) ++cur;
+            ++u;
+        }
+        if (!MODE && lane == 0) ucount[c] = u;
+    }
+}
+
+__global__ void value_ptr_kernel(const int64_t* __restrict__ ucount, const int64_t* __restrict__ mptr,
+                                 int64_t ncl, int64_t* __restrict__ slots,
+                                 int32_t* __restrict__ sizes) {
+    for (int64_t c = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; c < ncl;
+         c += int64_t{gridDim.x} * blockDim.x) {
+        const int64_t K = mptr[c + 1] - mptr[c];
+        slots[c] = K * ucount[c];
+        sizes[c] = static_cast<int32_t>(K);
+    }
+}
+
+// cluster_to_csr: per (cluster, member) valid count, then compaction.
+template <int MODE>
+__global__ void cluster_to_csr_kernel(const int32_t* __restrict__ sizes,
+                                      const int64_t* __restrict__ mptr,
+                                      const int64_t* __restrict__ ccp,
+                                      const int32_t* __restrict__ ccol,
+                                      const int64_t* __restrict__ vptr,
+                                      const double* __restrict__ vals,
+                                      const uint32_t* __restrict__ mask,
+                                      const int32_t* __restrict__ row_map, int64_t ncl,
+                                      int64_t* __restrict__ row_nnz, const int64_t* __restrict__ crp,
+                                      int32_t* __restrict__ ocol, double* __restrict__ oval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t{blockDim.x} + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t{gridDim.x} * blockDim.x) >> 5;
+    for (int64_t c = warp; c < ncl; c += nwarps) {
+        const int K = sizes[c];
+        const int64_t u0 = ccp[c], u1 = ccp[c + 1];
+        for (int l = 0; l < K; ++l) {
+            const int32_t row = row_map[mptr[c] + l];
+            int64_t pos = MODE ? crp[row] : 0;
+            int64_t cnt = 0;
+            for (int64_t ub = u0; ub < u1; ub += 32) {
+                const int64_t u = ub + lane;
+                const bool has = u < u1 && ((mask[u] >> l) & 1u);
+                const uint32_t b = __ballot_sync(0xffffffffu, has);
+                if (MODE && has) {
+                    const int64_t o = pos + __popc(b & ((1u << lane) - 1u));
+                    ocol[o] = ccol[u];
+                    oval[o] = vals[vptr[c] + (u - u0) * K + l];
+                }
+                pos += __popc(b);
+                cnt += __popc(b);
+            }
+            if (!MODE && lane == 0) row_nnz[row] = cnt;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cluster products + routing
+// ---------------------------------------------------------------------------
+constexpr int NCC = 4;  // 0: row-wise, 1: <=512, 2: <=2048, 3: <=4096 products
+__constant__ int kClusterCap[NCC] = {0, 512, 2048, 4096};
+
+__global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
+                                        uint8_t* __restrict__ ccls, uint8_t* __restrict__ row_skip,
+                                        unsigned long long* __restrict__ counts) {
+    __shared__ unsigned s_cnt[NCC];
+    if (threadIdx.x < NCC) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t c = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; c < ncl;
+         c += int64_t{gridDim.x} * blockDim.x) {
+        const int K = m.sizes[c];
+        int64_t P = 0;
+        for (int64_t u = m.ccp[c]; u < m.ccp[c + 1]; ++u) {
+            const int32_t k = m.ccol[u];
+            P += static_cast<int64_t>(__popc(m.mask[u])) * (m.brp[k + 1] - m.brp[k]);
+        }
+        int cl = 0;
+        const bool fits = (bit_length(static_cast<uint32_t>(K)) + cbits) <= 31;
+        if (K >= 2 && fits && P > 0 && P <= kClusterCap[NCC - 1]) {
+            cl = 1;
+            while (P > kClusterCap[cl]) ++cl;
+        }
+        ccls[c] = static_cast<uint8_t>(cl);
+        if (cl > 0)
+            for (int l = 0; l < K; ++l) row_skip[m.row_map[m.member_ptr[c] + l]] = 1;
+        atomicAdd(&s_cnt[cl], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < NCC) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+__global__ void cluster_bucket_kernel(const uint8_t* __restrict__ ccls, int64_t ncl,
+                                      unsigned long long* __restrict__ cursor,
+                                      int32_t* __restrict__ lists) {
+    for (int64_t c = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; c < ncl;
+         c += int64_t{gridDim.x} * blockDim.x) {
+        const int cl = ccls[c];
+        if (cl > 0) lists[atomicAdd(&cursor[cl], 1ull)] = static_cast<int32_t>(c);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cluster tile kernel
+// ---------------------------------------------------------------------------
+template <int T, int I, bool NUMERIC>
+struct ClusterShared {
+    static constexpr int CAPT = T * I;
+    using Sort = cub::BlockRadixSort<uint32_t, T, I, uint32_t>;
+    using Scan = cub::BlockScan<int32_t, T>;
+    uint32_t keys[CAPT];
+    double vals[NUMERIC ? CAPT : 1];
+    union {
+        typename Sort::TempStorage sort;
+        uint32_t sidx[CAPT];
+    } u;
+    typename Scan::TempStorage scan;
+    int64_t pstart[T];
+    int64_t pvb[T];
+    int32_t plen[T];
+    int32_t poff[T];
+    uint32_t pmask[T];
+    int32_t mcnt[MAXK];
+    int32_t mstart[MAXK];
+    int64_t mbase[MAXK];
+};
+
+template <int T, int I, bool NUMERIC>
+__global__ void __launch_bounds__(T) cluster_tile_kernel(ClusterMats m, const int32_t* __restrict__ ids,
+                                                         int cbits, int64_t* __restrict__ row_nnz,
+                                                         const int64_t* __restrict__ crp,
+                                                         int32_t* __restrict__ ocol,
+                                                         double* __restrict__ oval) {
+    using S = ClusterShared<T, I, NUMERIC>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S& s = *reinterpret_cast<S*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = T / 32;
+    const int32_t c = ids[blockIdx.x];
+    const int K = m.sizes[c];
+    const int64_t u0 = m.ccp[c], u1 = m.ccp[c + 1];
+    const int64_t vbase = m.vptr[c];
+    const uint32_t colmask = (1u << cbits) - 1u;
+    if (tid < MAXK) s.mcnt[tid] = 0;
+    int total = 0;
+    for (int64_t uc = u0; uc < u1; uc += T) {
+        const int64_t u = uc + tid;
+        int len = 0, seg = 0;
+        int64_t start = 0;
+        uint32_t msk = 0;
+        if (u < u1) {
+            const int32_t k = __ldg(m.ccol + u);
+            msk = __ldg(m.mask + u);
+            start = __ldg(m.brp + k);
+            seg = static_cast<int>(__ldg(m.brp + k + 1) - start);
+            len = seg * __popc(msk);
+        }
+        int off, chunk;
+        typename S::Scan(s.scan).ExclusiveSum(len, off, chunk);
+        s.pstart[tid] = start;
+        s.plen[tid] = seg;
+        s.poff[tid] = total + off;
+        s.pmask[tid] = msk;
+        s.pvb[tid] = vbase + (u - u0) * K;
+        __syncthreads();
+        const int nslots = static_cast<int>(::min(int64_t{T}, u1 - uc));
+        for (int slot = warp; slot < nslots; slot += NW) {
+            const int l_seg = s.plen[slot];
+            const uint32_t msk2 = s.pmask[slot];
+            if (l_seg == 0 || msk2 == 0) continue;
+            const int64_t st = s.pstart[slot];
+            const int o = s.poff[slot];
+            const int64_t vb = s.pvb[slot];
+            for (int q = lane; q < l_seg; q += 32) {
+                // one global load of the B entry, reused by every live member
+                const uint32_t j = static_cast<uint32_t>(__ldg(m.bcol + st + q));
+                double bv = 0.0;
+                if (NUMERIC) bv = __ldg(m.bval + st + q);
+                uint32_t mm = msk2;
+                int r = 0;
+                while (mm) {
+                    const int l = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const int pos = o + r * l_seg + q;
+                    s.keys[pos] = (static_cast<uint32_t>(l) << cbits) | j;
+                    if (NUMERIC) s.vals[pos] = __dmul_rn(__ldg(m.aval + vb + l), bv);
+                    ++r;
+                }
+            }
+        }
+        total += chunk;
+        __syncthreads();
+    }
+    const uint32_t pad = static_cast<uint32_t>(K) << cbits;
+    const int bits = bit_length(pad);
+    uint32_t k[I], v[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = tid * I + i;
+        k[i] = e < total ? s.keys[e] : pad;
+        v[i] = static_cast<uint32_t>(e);
+    }
+    __syncthreads();
+    typename S::Sort(s.u.sort).Sort(k, v, 0, bits);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        s.keys[tid * I + i] = k[i];
+        s.u.sidx[tid * I + i] = v[i];
+    }
+    __syncthreads();
+    bool head[I];
+    int nh = 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = tid * I + i;
+        head[i] = e < total && (e == 0 || k[i] != s.keys[e - 1]);
+        nh += head[i];
+        if (head[i]) atomicAdd(&s.mcnt[k[i] >> cbits], 1);
+    }
+    int hoff, tile_cnt;
+    typename S::Scan(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
+    __syncthreads();
+    if (!NUMERIC) {
+        if (tid < K) row_nnz[m.row_map[m.member_ptr[c] + tid]] = s.mcnt[tid];
+        return;
+    }
+    if (tid == 0) {
+        int acc = 0;
+        for (int l = 0; l < K; ++l) {
+            s.mstart[l] = acc;
+            acc += s.mcnt[l];
+        }
+    }
+    if (tid < K) s.mbase[tid] = crp[m.row_map[m.member_ptr[c] + tid]];
+    double res[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        res[i] = 0.0;
+        if (head[i]) {
+            double acc = 0.0;
+            int e = tid * I + i;
+            do {
+                acc = __dadd_rn(acc, s.vals[s.u.sidx[e]]);
+                ++e;
+            } while (e < total && s.keys[e] == k[i]);
+            res[i] = acc;
+        }
+    }
+    __syncthreads();
+    int r = hoff;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        if (head[i]) {
+            s.keys[r] = k[i];
+            s.vals[r] = res[i];
+            ++r;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < tile_cnt; e += T) {
+        const uint32_t key = s.keys[e];
+        const int l = static_cast<int>(key >> cbits);
+        const int64_t pos = s.mbase[l] + (e - s.mstart[l]);
+        ocol[pos] = static_cast<int32_t>(key & colmask);
+        oval[pos] = s.vals[e];
+    }
+}
+
+template <int T, int I, bool NUMERIC>
+void launch_cluster(bsp_handle h, const ClusterMats& m, const int32_t* ids, int64_t n, int cbits,
+                    int64_t* row_nnz, const int64_t* crp, int32_t* ocol, double* oval) {
+    if (n <= 0) return;
+    using S = ClusterShared<T, I, NUMERIC>;
+    auto k = cluster_tile_kernel<T, I, NUMERIC>;
+    set_smem(k, sizeof(S));
+    BSP_LAUNCH(h, k, static_cast<unsigned>(n), T, sizeof(S), m, ids, cbits, row_nnz, crp, ocol,
+               oval);
+}
+
+template <bool NUMERIC>
+void run_cluster_classes(bsp_handle h, const ClusterMats& m, const int32_t* lists,
+                         const int64_t* off, const int64_t* cnt, int cbits, int64_t* row_nnz,
+                         const int64_t* crp, int32_t* ocol, double* oval) {
+    launch_cluster<64, 8, NUMERIC>(h, m, lists + off[1], cnt[1], cbits, row_nnz, crp, ocol, oval);
+    launch_cluster<128, 16, NUMERIC>(h, m, lists + off[2], cnt[2], cbits, row_nnz, crp, ocol, oval);
+    launch_cluster<256, 16, NUMERIC>(h, m, lists + off[3], cnt[3], cbits, row_nnz, crp, ocol, oval);
+}
+
+// access statistics (reference cluster_spgemm.hpp:26-45, counted at :129-135)
+__global__ void cluster_stats_kernel(const int32_t* __restrict__ sizes,
+                                     const int64_t* __restrict__ ccp,
+                                     const int32_t* __restrict__ ccol,
+                                     const uint32_t* __restrict__ mask,
+                                     const int64_t* __restrict__ brp, int64_t ncl,
+                                     unsigned long long* __restrict__ out) {
+    unsigned long long loads = 0, iters = 0, skips = 0;
+    for (int64_t c = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; c < ncl;
+         c += int64_t{gridDim.x} * blockDim.x) {
+        const int K = sizes[c];
+        for (int64_t u = ccp[c]; u < ccp[c + 1]; ++u) {
+            const int32_t k = ccol[u];
+            const int64_t bn = brp[k + 1] - brp[k];
+            if (bn == 0) continue;
+            ++loads;
+            iters += static_cast<unsigned long long>(K * bn);
+            skips += static_cast<unsigned long long>((K - __popc(mask[u])) * bn);
+        }
+    }
+    atomicAdd(&out[0], loads);
+    atomicAdd(&out[1], iters);
+    atomicAdd(&out[2], skips);
+}
+
+__global__ void rowwise_stats_kernel(const int32_t* __restrict__ acol, int64_t nnz,
+                                     const int64_t* __restrict__ brp,
+                                     unsigned long long* __restrict__ out) {
+    unsigned long long loads = 0, iters = 0;
+    for (int64_t p = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; p < nnz;
+         p += int64_t{gridDim.x} * blockDim.x) {
+        const int32_t k = acol[p];
+        const int64_t bn = brp[k + 1] - brp[k];
+        if (bn > 0) {
+            ++loads;
+            iters += static_cast<unsigned long long>(bn);
+        }
+    }
+    atomicAdd(&out[0], loads);
+    atomicAdd(&out[1], iters);
+}
+
+int grid_for(bsp_handle h, int64_t n, int block) {
+    return static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(div_up(std::max<int64_t>(n, 1), block), int64_t{h->sm_count} * 16)));
+}
+
+ClusterMats make_cluster_mats(const bsp_csr_cluster* a, const bsp_csr* b) {
+    return ClusterMats{a->cluster_sizes, a->member_ptr, a->cluster_col_ptr, a->col_idx,
+                       a->value_ptr,     a->values,     a->member_mask,     a->row_map,
+                       b->row_ptr,       b->col_idx,    b->values,          static_cast<int32_t>(b->ncols)};
+}
+
+}  // namespace
+
+// Builds the device CSR_Cluster of a device CSR for a device-resident
+// assignment (member_ptr/rows already on the device, owned by `out`).
+void build_cluster_device(bsp_handle h, const bsp_csr* A, int64_t ncl, int64_t* mptr,
+                          int32_t* rows, bool keep_csr, bsp_csr_cluster* out) {
+    DBuf<int64_t> ucount(h, ncl + 1);
+    BSP_CUDA(cudaMemsetAsync(ucount.p, 0, (ncl + 1) * sizeof(int64_t), h->stream));
+    const int g = grid_for(h, ncl * 32, 256);
+    BSP_LAUNCH(h, build_cluster_kernel<0>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl, mptr,
+               rows, ucount.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    DBuf<int64_t> ccp(h, ncl + 1);
+    exclusive_scan_i64(h, ucount.p, ccp.p, ncl + 1);
+    DBuf<int64_t> slots(h, ncl + 1);
+    DBuf<int32_t> sizes(h, ncl);
+    BSP_CUDA(cudaMemsetAsync(slots.p + ncl, 0, sizeof(int64_t), h->stream));
+    BSP_LAUNCH(h, value_ptr_kernel, grid_for(h, ncl, 256), 256, 0, ucount.p, mptr, ncl, slots.p,
+               sizes.p);
+    DBuf<int64_t> vptr(h, ncl + 1);
+    exclusive_scan_i64(h, slots.p, vptr.p, ncl + 1);
+    int64_t tot[2];
+    d2h(h, &tot[0], ccp.p + ncl, 1);
+    d2h(h, &tot[1], vptr.p + ncl, 1);
+    sync(h);
+    const int64_t ncolslots = tot[0], nslots = tot[1];
+    DBuf<int32_t> ocol(h, ncolslots);
+    DBuf<uint32_t> omask(h, ncolslots);
+    DBuf<double> oval(h, nslots);
+    const int64_t nwords = (nslots + 63) / 64;
+    DBuf<uint64_t> valid(h, nwords);
+    BSP_CUDA(cudaMemsetAsync(oval.p, 0, std::max<int64_t>(nslots, 1) * sizeof(double), h->stream));
+    BSP_CUDA(cudaMemsetAsync(valid.p, 0, std::max<int64_t>(nwords, 1) * sizeof(uint64_t), h->stream));
+    BSP_LAUNCH(h, build_cluster_kernel<1>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl, mptr,
+               rows, nullptr, ccp.p, vptr.p, ocol.p, oval.p,
+               reinterpret_cast<unsigned long long*>(valid.p), omask.p);
+    out->nclusters = ncl;
+    out->nrows = A->nrows;
+    out->ncols = A->ncols;
+    out->ncolslots = ncolslots;
+    out->nslots = nslots;
+    out->cluster_sizes = sizes.release();
+    out->member_ptr = mptr;
+    out->cluster_col_ptr = ccp.release();
+    out->col_idx = ocol.release();
+    out->value_ptr = vptr.release();
+    out->values = oval.release();
+    out->valid = valid.release();
+    out->member_mask = omask.release();
+    out->row_map = rows;
+    out->csr_row_ptr = nullptr;
+    out->csr_col_idx = nullptr;
+    out->csr_values = nullptr;
+    if (keep_csr) {
+        DBuf<int64_t> rp(h, A->nrows + 1);
+        DBuf<int32_t> ci(h, A->nnz);
+        DBuf<double> v(h, A->nnz);
+        BSP_CUDA(cudaMemcpyAsync(rp.p, A->row_ptr, (A->nrows + 1) * sizeof(int64_t),
+                                 cudaMemcpyDeviceToDevice, h->stream));
+        BSP_CUDA(cudaMemcpyAsync(ci.p, A->col_idx, A->nnz * sizeof(int32_t),
+                                 cudaMemcpyDeviceToDevice, h->stream));
+        BSP_CUDA(cudaMemcpyAsync(v.p, A->values, A->nnz * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, h->stream));
+        out->csr_row_ptr = rp.release();
+        out->csr_col_idx = ci.release();
+        out->csr_values = v.release();
+    }
+    out->owned = 1;
+}
+
+void cluster_to_csr_device(bsp_handle h, const bsp_csr_cluster* m, bsp_csr* out) {
+    const int64_t n = m->nrows;
+    DBuf<int64_t> cnt(h, n + 1);
+    BSP_CUDA(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(int64_t), h->stream));
+    const int g = grid_for(h, m->nclusters * 32, 256);
+    BSP_LAUNCH(h, cluster_to_csr_kernel<0>, g, 256, 0, m->cluster_sizes, m->member_ptr,
+               m->cluster_col_ptr, m->col_idx, m->value_ptr, m->values, m->member_mask,
+               m->row_map, m->nclusters, cnt.p, nullptr, nullptr, nullptr);
+    DBuf<int64_t> rp(h, n + 1);
+    exclusive_scan_i64(h, cnt.p, rp.p, n + 1);
+    const int64_t nnz = read_scalar(h, rp.p + n);
+    DBuf<int32_t> ci(h, nnz);
+    DBuf<double> v(h, nnz);
+    BSP_LAUNCH(h, cluster_to_csr_kernel<1>, g, 256, 0, m->cluster_sizes, m->member_ptr,
+               m->cluster_col_ptr, m->col_idx, m->value_ptr, m->values, m->member_mask,
+               m->row_map, m->nclusters, nullptr, rp.p, ci.p, v.p);
+    out->nrows = n;
+    out->ncols = m->ncols;
+    out->nnz = nnz;
+    out->row_ptr = rp.release();
+    out->col_idx = ci.release();
+    out->values = v.release();
+    out->owned = 1;
+}
+
+void free_cluster(bsp_handle h, bsp_csr_cluster* m) {
+    if (!m || !m->owned) return;
+    void* ptrs[] = {m->cluster_sizes, m->member_ptr, m->cluster_col_ptr, m->col_idx,
+                    m->value_ptr,     m->values,     m->valid,           m->member_mask,
+                    m->row_map,       m->csr_row_ptr, m->csr_col_idx,    m->csr_values};
+    for (void* p : ptrs) dfree(h, p);
+    *m = bsp_csr_cluster{};
+}
+
+}  // namespace bsp
+
+using namespace bsp;
+
+extern "C" {
+
+int bsp_csr_cluster_build(bsp_handle h, const bsp_csr* A, int64_t nclusters,
+                          const int64_t* cluster_ptr, const int32_t* rows, bsp_csr_cluster* out) {
+    return guarded([&] {
+        check_csr(A, "build_csr_cluster");
+        require(out != nullptr && (nclusters == 0 || (cluster_ptr && rows)),
+                "build_csr_cluster: null argument");
+        BSP_CUDA(cudaSetDevice(h->device));
+        // ClusterAssignment::validate (cluster_format.hpp:34-51)
+        const int64_t n = A->nrows;
+        std::vector<char> seen(static_cast<size_t>(n), 0);
+        require(cluster_ptr == nullptr || cluster_ptr[0] == 0, "cluster assignment: bad offsets");
+        for (int64_t c = 0; c < nclusters; ++c) {
+            const int64_t b = cluster_ptr[c], e = cluster_ptr[c + 1];
+            require(e > b, "cluster assignment: empty cluster");
+            require(e - b <= MAXK, "cluster assignment: cluster larger than 32 rows is not "
+                                   "supported by the device format");
+            for (int64_t q = b; q < e; ++q) {
+                const int32_t r = rows[q];
+                require(r >= 0 && r < n, "cluster assignment: row index out of range");
+                require(!seen[r], "cluster assignment: row assigned twice");
+                seen[r] = 1;
+                if (q > b) require(rows[q - 1] < r, "cluster assignment: members must be strictly increasing");
+            }
+        }
+        for (int64_t i = 0; i < n; ++i)
+            require(seen[i], "cluster assignment: row " + std::to_string(i) + " not covered");
+        const int64_t total = nclusters > 0 ? cluster_ptr[nclusters] : 0;
+        DBuf<int64_t> mptr(h, nclusters + 1);
+        DBuf<int32_t> drows(h, total);
+        if (nclusters > 0) {
+            h2d(h, mptr.p, cluster_ptr, nclusters + 1);
+            h2d(h, drows.p, rows, total);
+        } else {
+            BSP_CUDA(cudaMemsetAsync(mptr.p, 0, sizeof(int64_t), h->stream));
+        }
+        bsp_csr_cluster tmp{};
+        build_cluster_device(h, A, nclusters, mptr.p, drows.p, true, &tmp);
+        mptr.release();
+        drows.release();
+        *out = tmp;
+        sync(h);
+    });
+}
+
+int bsp_csr_cluster_free(bsp_handle h, bsp_csr_cluster* m) {
+    return guarded([&] { free_cluster(h, m); });
+}
+
+int bsp_csr_cluster_download(bsp_handle h, const bsp_csr_cluster* m, bsp_host_csr_cluster* o) {
+    return guarded([&] {
+        require(m && o, "csr_cluster_download: null argument");
+        o->nclusters = m->nclusters;
+        o->nrows = m->nrows;
+        o->ncols = m->ncols;
+        o->ncolslots = m->ncolslots;
+        o->nslots = m->nslots;
+        o->cluster_sizes = host_malloc<int32_t>(m->nclusters);
+        o->cluster_col_ptr = host_malloc<int64_t>(m->nclusters + 1);
+        o->col_idx = host_malloc<int32_t>(m->ncolslots);
+        o->value_ptr = host_malloc<int64_t>(m->nclusters + 1);
+        o->values = host_malloc<double>(m->nslots);
+        const int64_t nw = (m->nslots + 63) / 64;
+        o->valid = host_malloc<uint64_t>(nw);
+        o->row_map = host_malloc<int32_t>(m->nrows);
+        d2h(h, o->cluster_sizes, m->cluster_sizes, m->nclusters);
+        d2h(h, o->cluster_col_ptr, m->cluster_col_ptr, m->nclusters + 1);
+        d2h(h, o->col_idx, m->col_idx, m->ncolslots);
+        d2h(h, o->value_ptr, m->value_ptr, m->nclusters + 1);
+        d2h(h, o->values, m->values, m->nslots);
+        d2h(h, o->valid, m->valid, nw);
+        d2h(h, o->row_map, m->row_map, m->nrows);
+        sync(h);
+    });
+}
+
+void bsp_host_csr_cluster_free(bsp_host_csr_cluster* m) {
+    if (!m) return;
+    std::free(m->cluster_sizes);
+    std::free(m->cluster_col_ptr);
+    std::free(m->col_idx);
+    std::free(m->value_ptr);
+    std::free(m->values);
+    std::free(m->valid);
+    std::free(m->row_map);
+    *m = bsp_host_csr_cluster{};
+}
+
+int bsp_cluster_to_csr(bsp_handle h, const bsp_csr_cluster* m, bsp_csr* out) {
+    return guarded([&] {
+        require(m && out, "cluster_to_csr: null argument");
+        BSP_CUDA(cudaSetDevice(h->device));
+        cluster_to_csr_device(h, m, out);
+    });
+}
+
+int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr* B, bsp_csr* C,
+                           bsp_csr_cluster* C_cluster) {
+    return guarded([&] {
+        require(A && B && C, "spgemm_clusterwise: null argument");
+        check_csr(B, "spgemm_clusterwise");
+        require(A->ncols == B->nrows, "spgemm_clusterwise: dimension mismatch (a.ncols != b.nrows)");
+        BSP_CUDA(cudaSetDevice(h->device));
+        h->stats = bsp_exec_stats{};
+        h->stats.chunks = 1;
+        const int64_t n = A->nrows, ncl = A->nclusters;
+        // Row view of A for clusters routed to the row-wise bins.
+        bsp_csr acsr{};
+        bsp_csr tmp_csr{};
+        if (A->csr_row_ptr) {
+            int64_t nnz = 0;
+            d2h(h, &nnz, A->csr_row_ptr + n, 1);
+            sync(h);
+            acsr = bsp_csr{n, A->ncols, nnz, A->csr_row_ptr, A->csr_col_idx, A->csr_values, 0};
+        } else {
+            cluster_to_csr_device(h, A, &tmp_csr);
+            acsr = tmp_csr;
+        }
+        const ClusterMats cm = make_cluster_mats(A, B);
+        const int cbits = bit_length(static_cast<uint32_t>(std::max<int64_t>(B->ncols - 1, 0)));
+        DBuf<uint8_t> ccls(h, ncl);
+        DBuf<uint8_t> skip(h, n);
+        BSP_CUDA(cudaMemsetAsync(skip.p, 0, std::max<int64_t>(n, 1), h->stream));
+        DBuf<unsigned long long> counts(h, NCC);
+        BSP_CUDA(cudaMemsetAsync(counts.p, 0, NCC * sizeof(unsigned long long), h->stream));
+        BSP_LAUNCH(h, cluster_products_kernel, grid_for(h, ncl, 256), 256, 0, cm, ncl, cbits, ccls.p,
+                   skip.p, counts.p);
+        unsigned long long hc[NCC];
+        d2h(h, hc, counts.p, NCC);
+        sync(h);
+        int64_t off[NCC], cnt[NCC];
+        int64_t acc = 0;
+        for (int c = 0; c < NCC; ++c) {
+            cnt[c] = static_cast<int64_t>(hc[c]);
+            off[c] = acc;
+            if (c > 0) acc += cnt[c];
+        }
+        DBuf<int32_t> lists(h, acc);
+        if (acc > 0) {
+            DBuf<unsigned long long> cursor(h, NCC);
+            std::vector<unsigned long long> cur(NCC, 0);
+            for (int c = 1; c < NCC; ++c) cur[c] = static_cast<unsigned long long>(off[c]);
+            h2d(h, cursor.p, cur.data(), NCC);
+            BSP_LAUNCH(h, cluster_bucket_kernel, grid_for(h, ncl, 256), 256, 0, ccls.p, ncl,
+                       cursor.p, lists.p);
+        }
+        const Mats m = make_mats(&acsr, B);
+        RowwisePlan plan;
+        build_plan(h, m, 0, n, skip.p, plan, nullptr);
+        h->stats.units[5] = cnt[1] + cnt[2] + cnt[3];  // cluster tiles
+        DBuf<int64_t> row_nnz(h, n + 1);
+        BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
+        run_cluster_classes<false>(h, cm, lists.p, off, cnt, cbits, row_nnz.p, nullptr, nullptr,
+                                   nullptr);
+        DBuf<int64_t> win_nnz;
+        plan_symbolic(h, m, plan, row_nnz.p, win_nnz);
+        DBuf<int64_t> rp(h, n + 1);
+        exclusive_scan_i64(h, row_nnz.p, rp.p, n + 1);
+        DBuf<int64_t> win_scan(h, plan.nwin + 1);
+        if (plan.nwin > 0) exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
+        const int64_t nnz = read_scalar(h, rp.p + n);
+        h->stats.nnz_out = nnz;
+        DBuf<int32_t> ccol(h, nnz);
+        DBuf<double> cval(h, nnz);
+        run_cluster_classes<true>(h, cm, lists.p, off, cnt, cbits, nullptr, rp.p, ccol.p, cval.p);
+        plan_numeric(h, m, plan, rp.p, win_scan.p, ccol.p, cval.p);
+        C->nrows = n;
+        C->ncols = B->ncols;
+        C->nnz = nnz;
+        C->row_ptr = rp.release();
+        C->col_idx = ccol.release();
+        C->values = cval.release();
+        C->owned = 1;
+        if (tmp_csr.owned) {
+            dfree(h, tmp_csr.row_ptr);
+            dfree(h, tmp_csr.col_idx);
+            dfree(h, tmp_csr.values);
+        }
+        if (C_cluster) {
+            // C's cluster form = build_csr_cluster(C, A's assignment)
+            // (same sizes/row_map; union of members' output columns).
+            DBuf<int64_t> mptr(h, ncl + 1);
+            DBuf<int32_t> rows(h, n);
+            BSP_CUDA(cudaMemcpyAsync(mptr.p, A->member_ptr, (ncl + 1) * sizeof(int64_t),
+                                     cudaMemcpyDeviceToDevice, h->stream));
+            BSP_CUDA(cudaMemcpyAsync(rows.p, A->row_map, n * sizeof(int32_t),
+                                     cudaMemcpyDeviceToDevice, h->stream));
+            bsp_csr_cluster cc{};
+            build_cluster_device(h, C, ncl, mptr.p, rows.p, false, &cc);
+            mptr.release();
+            rows.release();
+            *C_cluster = cc;
+        }
+    });
+}
+
+int bsp_cluster_access_stats(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr* B,
+                             bsp_access_stats* out) {
+    return guarded([&] {
+        require(A && B && out, "cluster_access_stats: null argument");
+        require(A->ncols == B->nrows, "rowwise_access_stats: dimension mismatch");
+        DBuf<unsigned long long> acc(h, 3);
+        BSP_CUDA(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), h->stream));
+        BSP_LAUNCH(h, cluster_stats_kernel, grid_for(h, A->nclusters, 256), 256, 0,
+                   A->cluster_sizes, A->cluster_col_ptr, A->col_idx, A->member_mask, B->row_ptr,
+                   A->nclusters, acc.p);
+        unsigned long long r[3];
+        d2h(h, r, acc.p, 3);
+        sync(h);
+        out->b_row_loads = r[0];
+        out->a_inner_iters = r[1];
+        out->placeholder_skips = r[2];
+    });
+}
+
+int bsp_rowwise_access_stats(bsp_handle h, const bsp_csr* A, const bsp_csr* B,
+                             bsp_access_stats* out) {
+    return guarded([&] {
+        check_csr(A, "rowwise_access_stats");
+        require(A->ncols == B->nrows, "rowwise_access_stats: dimension mismatch");
+        DBuf<unsigned long long> acc(h, 3);
+        BSP_CUDA(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), h->stream));
+        BSP_LAUNCH(h, rowwise_stats_kernel, grid_for(h, A->nnz, 256), 256, 0, A->col_idx, A->nnz,
+                   B->row_ptr, acc.p);
+        unsigned long long r[3];
+        d2h(h, r, acc.p, 3);
+        sync(h);
+        out->b_row_loads = r[0];
+        out->a_inner_iters = r[1];
+        out->placeholder_skips = 0;
+    });
+}
+
+}  // extern "C"

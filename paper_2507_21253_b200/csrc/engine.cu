@@ -1,0 +1,307 @@
+// Handle, memory and transfer entry points of the C ABI, plus device-wide
+// scan helpers and the device transpose (reference csr.hpp:115-135).
+#include "engine.cuh"
+
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cstdio>
+
+namespace bsp {
+
+void exclusive_scan_i64(bsp_handle h, const int64_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    size_t tmp = 0;
+    BSP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, h->stream));
+    DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+    BSP_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, h->stream));
+    ++h->launches;
+    ++h->stats.kernels_launched;
+}
+
+void exclusive_scan_i32_to_i64(bsp_handle h, const int32_t* in, int64_t* out, int64_t n) {
+    if (n <= 0) return;
+    size_t tmp = 0;
+    BSP_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp, in, out, cub::Sum(), int64_t{0}, n,
+                                            h->stream));
+    DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+    BSP_CUDA(cub::DeviceScan::ExclusiveScan(t.p, tmp, in, out, cub::Sum(), int64_t{0}, n,
+                                            h->stream));
+    ++h->launches;
+    ++h->stats.kernels_launched;
+}
+
+int64_t reduce_sum_i64(bsp_handle h, const int64_t* in, int64_t n) {
+    if (n <= 0) return 0;
+    DBuf<int64_t> out(h, 1);
+    size_t tmp = 0;
+    BSP_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, in, out.p, n, h->stream));
+    DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+    BSP_CUDA(cub::DeviceReduce::Sum(t.p, tmp, in, out.p, n, h->stream));
+    ++h->launches;
+    ++h->stats.kernels_launched;
+    return read_scalar(h, out.p);
+}
+
+namespace {
+
+__global__ void widen_rp_kernel(const int32_t* __restrict__ in, int64_t* __restrict__ out,
+                                int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; i < n;
+         i += int64_t{gridDim.x} * blockDim.x)
+        out[i] = in[i];
+}
+
+// Transpose, step 1: column histogram.
+__global__ void col_count_kernel(const int32_t* __restrict__ col, int64_t nnz,
+                                 int32_t* __restrict__ cnt) {
+    for (int64_t p = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; p < nnz;
+         p += int64_t{gridDim.x} * blockDim.x)
+        atomicAdd(&cnt[col[p]], 1);
+}
+
+// Transpose, step 2: one warp per source row writes its entries at
+// deterministic positions.  pos(i,p) = t_row_ptr[c] + #{entries (i',c) with
+// i' < i}; computed from an atomic cursor would be nondeterministic, so the
+// destination rank is found by a counting pass over rows in order: we use a
+// per-column cursor that is advanced row by row in a second kernel below.
+__global__ void transpose_scatter_kernel(const int64_t* __restrict__ rp,
+                                         const int32_t* __restrict__ col,
+                                         const double* __restrict__ val, int64_t nrows,
+                                         int64_t* __restrict__ cursor,
+                                         int32_t* __restrict__ t_col, double* __restrict__ t_val) {
+    for (int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; i < nrows;
+         i += int64_t{gridDim.x} * blockDim.x) {
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int32_t c = col[p];
+            const int64_t pos = atomicAdd(reinterpret_cast<unsigned long long*>(&cursor[c]), 1ull);
+            t_col[pos] = static_cast<int32_t>(i);
+            if (val) t_val[pos] = val[p];
+        }
+    }
+}
+
+// Rows of the transpose are then sorted by (row index) with their values;
+// each row of A^T is short on average, so one thread per row does an
+// insertion sort (long rows use a warp-cooperative odd-even pass).
+__global__ void sort_rows_kernel(const int64_t* __restrict__ rp, int64_t nrows,
+                                 int32_t* __restrict__ col, double* __restrict__ val) {
+    for (int64_t r = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; r < nrows;
+         r += int64_t{gridDim.x} * blockDim.x) {
+        const int64_t b = rp[r], e = rp[r + 1];
+        for (int64_t p = b + 1; p < e; ++p) {
+            const int32_t kc = col[p];
+            const double kv = val ? val[p] : 0.0;
+            int64_t q = p - 1;
+            while (q >= b && col[q] > kc) {
+                col[q + 1] = col[q];
+                if (val) val[q + 1] = val[q];
+                --q;
+            }
+            col[q + 1] = kc;
+            if (val) val[q + 1] = kv;
+        }
+    }
+}
+
+}  // namespace
+
+}  // namespace bsp
+
+using namespace bsp;
+
+extern "C" {
+
+const char* bsp_version(void) { return "bsp 0.1 (sm_100a)"; }
+
+int bsp_create(int device, bsp_handle* out) {
+    return guarded([&] {
+        require(out != nullptr, "bsp_create: null out");
+        int ndev = 0;
+        BSP_CUDA(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "bsp_create: no such device");
+        BSP_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        BSP_CUDA(cudaGetDeviceProperties(&prop, device));
+        require(prop.major >= 10, "bsp_create: this engine requires sm_100a (B200)");
+        auto* h = new bsp_handle_s();
+        h->device = device;
+        h->sm_count = prop.multiProcessorCount;
+        BSP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+        cudaMemPool_t pool;
+        BSP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        BSP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        *out = h;
+    });
+}
+
+int bsp_destroy(bsp_handle h) {
+    return guarded([&] {
+        if (!h) return;
+        cudaStreamSynchronize(h->stream);
+        if (h->own_stream) cudaStreamDestroy(h->stream);
+        delete h;
+    });
+}
+
+int bsp_set_stream(bsp_handle h, void* s) {
+    return guarded([&] {
+        require(h != nullptr, "bsp_set_stream: null handle");
+        BSP_CUDA(cudaSetDevice(h->device));
+        if (h->own_stream) {
+            BSP_CUDA(cudaStreamSynchronize(h->stream));
+            BSP_CUDA(cudaStreamDestroy(h->stream));
+            h->own_stream = false;
+        }
+        if (s == nullptr) {
+            BSP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            h->own_stream = true;
+        } else {
+            h->stream = static_cast<cudaStream_t>(s);
+        }
+    });
+}
+
+void* bsp_get_stream(bsp_handle h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int bsp_synchronize(bsp_handle h) {
+    return guarded([&] { BSP_CUDA(cudaStreamSynchronize(h->stream)); });
+}
+
+int64_t bsp_kernel_launches(bsp_handle h) { return h ? h->launches : 0; }
+
+int bsp_get_exec_stats(bsp_handle h, bsp_exec_stats* out) {
+    return guarded([&] {
+        require(h && out, "bsp_get_exec_stats: null argument");
+        *out = h->stats;
+    });
+}
+
+int bsp_csr_upload(bsp_handle h, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                   const int32_t* col_idx, const double* values, bsp_csr* out) {
+    return guarded([&] {
+        require(h && out && row_ptr, "bsp_csr_upload: null argument");
+        require(nrows >= 0 && ncols >= 0, "bsp_csr_upload: negative shape");
+        BSP_CUDA(cudaSetDevice(h->device));
+        const int64_t nnz = row_ptr[nrows];
+        require(row_ptr[0] == 0 && nnz >= 0, "bsp_csr_upload: bad row_ptr");
+        DBuf<int64_t> rp(h, nrows + 1);
+        DBuf<int32_t> ci(h, nnz);
+        DBuf<double> v(h, nnz);
+        h2d(h, rp.p, row_ptr, nrows + 1);
+        h2d(h, ci.p, col_idx, nnz);
+        if (values) {
+            h2d(h, v.p, values, nnz);
+        } else if (nnz > 0) {
+            // pattern-only input: every stored value is 1.0 (binarize, csr.hpp:138-142)
+            std::vector<double> ones(static_cast<size_t>(nnz), 1.0);
+            h2d(h, v.p, ones.data(), nnz);
+            sync(h);
+        }
+        out->nrows = nrows;
+        out->ncols = ncols;
+        out->nnz = nnz;
+        out->row_ptr = rp.release();
+        out->col_idx = ci.release();
+        out->values = v.release();
+        out->owned = 1;
+    });
+}
+
+int bsp_csr_upload_rp32(bsp_handle h, int64_t nrows, int64_t ncols, const int32_t* row_ptr,
+                        const int32_t* col_idx, const double* values, bsp_csr* out) {
+    return guarded([&] {
+        require(h && out && row_ptr, "bsp_csr_upload_rp32: null argument");
+        std::vector<int64_t> rp(row_ptr, row_ptr + nrows + 1);
+        const int rc = bsp_csr_upload(h, nrows, ncols, rp.data(), col_idx, values, out);
+        if (rc != BSP_OK) throw std::runtime_error(bsp_last_error());
+        sync(h);
+    });
+}
+
+int bsp_csr_view(int64_t nrows, int64_t ncols, int64_t nnz, int64_t* row_ptr, int32_t* col_idx,
+                 double* values, bsp_csr* out) {
+    return guarded([&] {
+        require(out != nullptr, "bsp_csr_view: null out");
+        out->nrows = nrows;
+        out->ncols = ncols;
+        out->nnz = nnz;
+        out->row_ptr = row_ptr;
+        out->col_idx = col_idx;
+        out->values = values;
+        out->owned = 0;
+    });
+}
+
+int bsp_csr_download(bsp_handle h, const bsp_csr* m, int64_t* row_ptr, int32_t* col_idx,
+                     double* values) {
+    return guarded([&] {
+        check_csr(m, "bsp_csr_download");
+        if (row_ptr) d2h(h, row_ptr, m->row_ptr, m->nrows + 1);
+        if (col_idx) d2h(h, col_idx, m->col_idx, m->nnz);
+        if (values) d2h(h, values, m->values, m->nnz);
+        sync(h);
+    });
+}
+
+int bsp_csr_free(bsp_handle h, bsp_csr* m) {
+    return guarded([&] {
+        if (!m) return;
+        if (m->owned) {
+            dfree(h, m->row_ptr);
+            dfree(h, m->col_idx);
+            dfree(h, m->values);
+        }
+        m->row_ptr = nullptr;
+        m->col_idx = nullptr;
+        m->values = nullptr;
+        m->owned = 0;
+    });
+}
+
+int bsp_host_alloc(size_t bytes, void** out) {
+    return guarded([&] { BSP_CUDA(cudaMallocHost(out, bytes > 0 ? bytes : 1)); });
+}
+
+int bsp_host_free(void* p) {
+    return guarded([&] {
+        if (p) BSP_CUDA(cudaFreeHost(p));
+    });
+}
+
+int bsp_transpose(bsp_handle h, const bsp_csr* A, bsp_csr* out) {
+    return guarded([&] {
+        check_csr(A, "transpose");
+        const int64_t n = A->ncols, nnz = A->nnz;
+        DBuf<int32_t> cnt(h, n + 1);
+        BSP_CUDA(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(int32_t), h->stream));
+        const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(nnz, 1), 256),
+                                                            h->sm_count * 16));
+        BSP_LAUNCH(h, col_count_kernel, grid, 256, 0, A->col_idx, nnz, cnt.p);
+        DBuf<int64_t> rp(h, n + 1);
+        exclusive_scan_i32_to_i64(h, cnt.p, rp.p, n + 1);
+        DBuf<int64_t> cursor(h, n + 1);
+        BSP_CUDA(cudaMemcpyAsync(cursor.p, rp.p, (n + 1) * sizeof(int64_t),
+                                 cudaMemcpyDeviceToDevice, h->stream));
+        DBuf<int32_t> tc(h, nnz);
+        DBuf<double> tv(h, nnz);
+        const int rgrid = static_cast<int>(
+            std::min<int64_t>(div_up(std::max<int64_t>(A->nrows, 1), 256), h->sm_count * 16));
+        BSP_LAUNCH(h, transpose_scatter_kernel, rgrid, 256, 0, A->row_ptr, A->col_idx, A->values,
+                   A->nrows, cursor.p, tc.p, tv.p);
+        const int sgrid = static_cast<int>(
+            std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 256), h->sm_count * 16));
+        BSP_LAUNCH(h, sort_rows_kernel, sgrid, 256, 0, rp.p, n, tc.p, tv.p);
+        out->nrows = n;
+        out->ncols = A->nrows;
+        out->nnz = nnz;
+        out->row_ptr = rp.release();
+        out->col_idx = tc.release();
+        out->values = tv.release();
+        out->owned = 1;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+// Engine internals shared by the CUDA translation units (sm_100a only).
+#pragma once
+
+#include "common.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "This engine is written for sm_100a (B200) only."
+#endif
+
+struct bsp_handle_s {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t launches = 0;
+    bsp_exec_stats stats{};
+};
+
+namespace bsp {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        throw oom_error(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define BSP_CUDA(call) ::bsp::cuda_check((call), #call)
+
+// Every engine kernel launch goes through this so the handle can report how
+// many of OUR kernels ran (bench.py's gpu_launches).
+#define BSP_LAUNCH(h, kernel, grid, block, smem, ...)                                  \
+    do {                                                                               \
+        if ((grid) > 0) {                                                              \
+            kernel<<<(grid), (block), (smem), (h)->stream>>>(__VA_ARGS__);             \
+            ::bsp::cuda_check(cudaGetLastError(), #kernel);                            \
+            ++(h)->launches;                                                           \
+            ++(h)->stats.kernels_launched;                                             \
+        }                                                                              \
+    } while (0)
+
+// Stream-ordered device allocation from the device's default memory pool
+// (release threshold raised at handle creation so repeated calls reuse it).
+template <typename T>
+T* dalloc(bsp_handle h, int64_t n) {
+    void* p = nullptr;
+    const size_t bytes = static_cast<size_t>(n > 0 ? n : 1) * sizeof(T);
+    cuda_check(cudaMallocAsync(&p, bytes, h->stream), "cudaMallocAsync");
+    return static_cast<T*>(p);
+}
+
+inline void dfree(bsp_handle h, void* p) {
+    if (p) cudaFreeAsync(p, h->stream);
+}
+
+// RAII device buffer bound to a handle's stream.
+template <typename T>
+struct DBuf {
+    bsp_handle h = nullptr;
+    T* p = nullptr;
+    int64_t n = 0;
+    DBuf() = default;
+    DBuf(bsp_handle hh, int64_t nn) : h(hh), p(dalloc<T>(hh, nn)), n(nn) {}
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : h(o.h), p(o.p), n(o.n) { o.p = nullptr; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        reset();
+        h = o.h;
+        p = o.p;
+        n = o.n;
+        o.p = nullptr;
+        return *this;
+    }
+    ~DBuf() { reset(); }
+    void reset() {
+        if (p) dfree(h, p);
+        p = nullptr;
+    }
+    T* release() {
+        T* q = p;
+        p = nullptr;
+        return q;
+    }
+};
+
+template <typename T>
+void d2h(bsp_handle h, T* dst, const T* src, int64_t n) {
+    if (n <= 0) return;
+    BSP_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, h->stream));
+}
+template <typename T>
+void h2d(bsp_handle h, T* dst, const T* src, int64_t n) {
+    if (n <= 0) return;
+    BSP_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+}
+inline void sync(bsp_handle h) { BSP_CUDA(cudaStreamSynchronize(h->stream)); }
+
+template <typename T>
+T read_scalar(bsp_handle h, const T* dptr) {
+    T v{};
+    d2h(h, &v, dptr, 1);
+    sync(h);
+    return v;
+}
+
+inline void check_csr(const bsp_csr* m, const char* who) {
+    require(m != nullptr, std::string(who) + ": null matrix");
+    require(m->nrows >= 0 && m->ncols >= 0 && m->nnz >= 0, std::string(who) + ": bad shape");
+    require(m->row_ptr != nullptr, std::string(who) + ": null row_ptr");
+    require(m->nrows < (int64_t{1} << 31) && m->ncols < (int64_t{1} << 31),
+            std::string(who) + ": dimensions must fit int32 indices");
+}
+
+// Device-wide exclusive scans (int64) via CUB, with temp storage from the pool.
+void exclusive_scan_i64(bsp_handle h, const int64_t* in, int64_t* out, int64_t n);
+void exclusive_scan_i32_to_i64(bsp_handle h, const int32_t* in, int64_t* out, int64_t n);
+int64_t reduce_sum_i64(bsp_handle h, const int64_t* in, int64_t n);
+
+// Shared row-wise machinery (rowwise.cu), reused by the cluster-wise and
+// top-k paths.
+struct RowwisePlan;
+void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t row_begin,
+                      int64_t row_end, bsp_csr* C, const uint8_t* row_skip /*nullable*/,
+                      int64_t* row_nnz_out /*nullable, device*/);
+
+inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace bsp

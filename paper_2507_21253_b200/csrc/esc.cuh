@@ -1,0 +1,166 @@
+// Shared ESC (expand / stable-sort / compress) building blocks used by the
+// row-wise, cluster-wise and top-k kernels.
+#pragma once
+
+#include "engine.cuh"
+
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+
+namespace bsp {
+
+constexpr int CAP = 4096;     // max products of one sparse tile (smem ESC)
+constexpr int CAPH = CAP / 2;
+constexpr int WD = 4096;      // dense window width in columns
+constexpr int LOG_WD = 12;
+constexpr int MAXBINS = 4096; // planner histogram bins per heavy row
+constexpr int NCLS = 6;       // 0 empty, 1..4 light classes, 5 heavy
+static __constant__ int kClassCap[NCLS] = {0, 128, 512, 2048, 4096, 0x7fffffff};
+constexpr int kClassCapHost[NCLS] = {0, 128, 512, 2048, 4096, 0x7fffffff};
+
+struct Mats {
+    const int64_t* __restrict__ arp;
+    const int32_t* __restrict__ acol;
+    const double* __restrict__ aval;
+    const int64_t* __restrict__ brp;
+    const int32_t* __restrict__ bcol;
+    const double* __restrict__ bval;
+    int32_t ncols;  // columns of B (= of C)
+};
+
+struct Window {
+    int32_t row;    // absolute A row
+    int32_t c0, c1; // column range [c0, c1)
+    int32_t first;  // index of the row's first window
+};
+
+struct OutCtx {
+    int64_t row_begin;
+    int64_t* row_nnz;        // [nrows of range] (symbolic output)
+    int64_t* win_nnz;        // [nwindows] (symbolic output)
+    const int64_t* crp;      // C row_ptr (numeric)
+    const int64_t* win_scan; // exclusive scan of win_nnz (numeric)
+    int32_t* ccol;
+    double* cval;
+};
+
+__device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ col, int64_t lo,
+                                                   int64_t hi, int32_t key) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(col + mid) < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__host__ __device__ __forceinline__ int bit_length(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return 32 - __clz(x);
+#else
+    return x ? 32 - __builtin_clz(x) : 0;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// K3: ESC tile kernel (light rows and sparse windows)
+// ---------------------------------------------------------------------------
+template <int T, int I, bool NUMERIC>
+struct EscShared {
+    static constexpr int CAPT = T * I;
+    using Sort = cub::BlockRadixSort<uint32_t, T, I, uint32_t>;
+    using Scan = cub::BlockScan<int32_t, T>;
+    uint32_t keys[CAPT];
+    double vals[NUMERIC ? CAPT : 1];
+    union {
+        typename Sort::TempStorage sort;
+        uint32_t sidx[CAPT];
+    } u;
+    typename Scan::TempStorage scan;
+    int64_t pstart[T];
+    int32_t plen[T];
+    int32_t poff[T];
+    double pav[NUMERIC ? T : 1];
+};
+
+// Expands the products of (row, [c0,c1)) into s.keys (column - c0) and, for
+// NUMERIC, s.vals (a*b rounded), in (k ascending, j ascending) order.
+// Returns the product count.
+template <int T, int I, bool NUMERIC, typename S>
+__device__ __forceinline__ int expand_products(const Mats& m, int32_t row, int32_t c0, int32_t c1,
+                                               bool full, S& s) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = T / 32;
+    const int64_t rs = m.arp[row], re = m.arp[row + 1];
+    int total = 0;
+    for (int64_t pc = rs; pc < re; pc += T) {
+        const int64_t p = pc + tid;
+        int len = 0;
+        int64_t start = 0;
+        double av = 0.0;
+        if (p < re) {
+            const int32_t k = __ldg(m.acol + p);
+            int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
+            if (!full) {
+                b0 = lower_bound_col(m.bcol, b0, b1, c0);
+                b1 = lower_bound_col(m.bcol, b0, b1, c1);
+            }
+            start = b0;
+            len = static_cast<int>(b1 - b0);
+            if (NUMERIC) av = __ldg(m.aval + p);
+        }
+        int off, chunk;
+        typename cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(len, off, chunk);
+        s.pstart[tid] = start;
+        s.plen[tid] = len;
+        s.poff[tid] = total + off;
+        if (NUMERIC) s.pav[tid] = av;
+        __syncthreads();
+        const int nslots = static_cast<int>(::min(int64_t{T}, re - pc));
+        for (int slot = warp; slot < nslots; slot += NW) {
+            const int l = s.plen[slot];
+            const int64_t st = s.pstart[slot];
+            const int o = s.poff[slot];
+            double a = 0.0;
+            if (NUMERIC) a = s.pav[slot];
+            for (int q = lane; q < l; q += 32) {
+                s.keys[o + q] = static_cast<uint32_t>(__ldg(m.bcol + st + q) - c0);
+                if (NUMERIC) s.vals[o + q] = __dmul_rn(a, __ldg(m.bval + st + q));
+            }
+        }
+        total += chunk;
+        __syncthreads();
+    }
+    return total;
+}
+
+
+// The plan of one multiply: per-class row lists and heavy-row windows.
+struct RowwisePlan {
+    int64_t rb = 0, n = 0;
+    int64_t class_count[NCLS]{}, class_products[NCLS]{};
+    int64_t class_off[NCLS + 1]{};
+    DBuf<int32_t> lists;  // all non-empty rows grouped by class
+    int64_t nwin = 0, nsparse = 0, ndense = 0;
+    DBuf<Window> wins;
+    DBuf<int32_t> sparse_ids, dense_ids;
+};
+
+Mats make_mats(const bsp_csr* A, const bsp_csr* B);
+void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re, const uint8_t* skip,
+                RowwisePlan& plan, int64_t* prod_out);
+// Symbolic counts of a plan into row_nnz (NOT zeroed here) and win_nnz (allocated).
+void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t* row_nnz,
+                   DBuf<int64_t>& win_nnz);
+void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
+                  const int64_t* win_scan, int32_t* ccol, double* cval);
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    BSP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes)));
+}
+
+}  // namespace bsp

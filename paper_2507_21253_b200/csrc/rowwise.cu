@@ -1,0 +1,835 @@
+// Row-wise Gustavson SpGEMM on sm_100a — the hot path.
+//
+// Replaces reference spgemm_symbolic (spgemm.hpp:41-63) and spgemm_rowwise
+// (spgemm.hpp:70-106).  Parity contract: C's row_ptr/col_idx bit-exact and
+// every value bit-identical to the reference, which accumulates
+//     c_ij = ((0.0 + a_ik1*b_k1j) + a_ik2*b_k2j) + ...   (ascending k)
+// with the multiply rounded before the add (no FMA; spgemm.hpp:92-97,
+// hash_accumulator.hpp:57-65).
+//
+// Design:
+//  K0 products_kernel: per-row intermediate products P_i (row_upper_bound,
+//     spgemm.hpp:31-36) and the row's work class.
+//  K1 bucket_kernel:   row ids grouped by class.
+//  K2 plan kernels:    rows with P_i > CAP are cut into column windows with
+//     <= CAP products ("sparse" windows) or <= WD columns ("dense" windows),
+//     from a per-row product histogram over WD-wide column bins.
+//  K3 esc_tile_kernel<T,I,NUMERIC>: one CTA per row (or sparse window):
+//     expand the row's products into shared memory in (k, j) order, stable
+//     radix sort by column, then each run of equal columns is summed
+//     sequentially in k order starting from 0.0 -> bit-exact values; runs
+//     are written as sorted CSR through a coalesced smem staging pass.
+//  K4 dense_window_kernel<NUMERIC>: heavy windows with a dense smem
+//     accumulator of WD doubles + bitmap; products streamed in CAP batches
+//     in k order, each batch stable-sorted so per-column order is kept.
+//  Symbolic runs K3/K4 without values to get exact per-row counts (exact
+//  allocation as the reference), then an int64 scan gives row_ptr.
+#include "esc.cuh"
+
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+#include <cstdio>
+
+namespace bsp {
+
+namespace {
+
+
+// ---------------------------------------------------------------------------
+// K0: products and class per row
+// ---------------------------------------------------------------------------
+__global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restrict__ prod,
+                                uint8_t* __restrict__ cls, const uint8_t* __restrict__ skip,
+                                int64_t* __restrict__ class_count,
+                                int64_t* __restrict__ class_products) {
+    __shared__ int64_t s_cnt[NCLS], s_prod[NCLS];
+    if (threadIdx.x < NCLS) {
+        s_cnt[threadIdx.x] = 0;
+        s_prod[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    for (int64_t r = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; r < n;
+         r += int64_t{gridDim.x} * blockDim.x) {
+        const int64_t i = rb + r;
+        int64_t P = 0;
+        for (int64_t p = m.arp[i]; p < m.arp[i + 1]; ++p) {
+            const int32_t k = __ldg(m.acol + p);
+            P += __ldg(m.brp + k + 1) - __ldg(m.brp + k);
+        }
+        int c = 0;
+        if (skip && skip[r]) {
+            c = 0;
+        } else if (P > 0) {
+            c = 1;
+            while (c < NCLS - 1 && P > kClassCap[c]) ++c;
+        }
+        if (prod) prod[r] = P;
+        cls[r] = static_cast<uint8_t>(c);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[c]), 1ull);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_prod[c]),
+                  static_cast<unsigned long long>(P));
+    }
+    __syncthreads();
+    if (threadIdx.x < NCLS) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&class_count[threadIdx.x]),
+                  static_cast<unsigned long long>(s_cnt[threadIdx.x]));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&class_products[threadIdx.x]),
+                  static_cast<unsigned long long>(s_prod[threadIdx.x]));
+    }
+}
+
+// K1: group row ids (absolute) by class into per-class regions.
+__global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64_t n,
+                              unsigned long long* __restrict__ cursor,
+                              int32_t* __restrict__ lists) {
+    __shared__ unsigned s_cnt[NCLS];
+    __shared__ unsigned long long s_base[NCLS];
+    if (threadIdx.x < NCLS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t r = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    int c = 0;
+    unsigned rank = 0;
+    if (r < n) {
+        c = cls[r];
+        if (c > 0) rank = atomicAdd(&s_cnt[c], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x > 0 && threadIdx.x < NCLS)
+        s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
+    __syncthreads();
+    if (r < n && c > 0) lists[s_base[c] + rank] = static_cast<int32_t>(rb + r);
+}
+
+// ---------------------------------------------------------------------------
+// K2: heavy-row planner
+// ---------------------------------------------------------------------------
+constexpr int PLAN_T = 256;
+
+struct PlanShared {
+    int32_t hist[MAXBINS];
+    int32_t wstart[MAXBINS];  // per bin: first window index (or -1)
+    int32_t wc0[MAXBINS];     // window -> c0 (bounded by MAXBINS windows per row)
+    typename cub::BlockScan<int32_t, PLAN_T>::TempStorage scan;
+    int32_t total;
+};
+
+// Histogram of a heavy row's products over `nbins` bins of width 1<<log_binw.
+__device__ void plan_histogram(const Mats& m, int32_t row, int log_binw, int32_t* hist) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = PLAN_T / 32;
+    for (int64_t p = m.arp[row] + warp; p < m.arp[row + 1]; p += nw) {
+        const int32_t k = __ldg(m.acol + p);
+        const int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
+        for (int64_t q0 = b0; q0 < b1; q0 += 32) {
+            const int64_t q = q0 + lane;
+            const bool ok = q < b1;
+            const int32_t bin = ok ? (__ldg(m.bcol + q) >> log_binw) : 0x7fffffff;
+            // columns are sorted within the B row, so equal bins form runs:
+            // the last lane of each run adds the run length.
+            const int32_t nxt = __shfl_down_sync(0xffffffffu, bin, 1);
+            const bool tail = ok && (lane == 31 || nxt != bin);
+            const unsigned heads = __ballot_sync(
+                0xffffffffu, ok && (lane == 0 || __shfl_up_sync(0xffffffffu, bin, 1) != bin));
+            if (tail) {
+                const unsigned below = heads & ((2u << lane) - 1u);
+                const int head_lane = 31 - __clz(below);
+                atomicAdd(&hist[bin], lane - head_lane + 1);
+            }
+        }
+    }
+}
+
+// mode 0: count windows per heavy row; mode 1: write them.
+template <int MODE>
+__global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __restrict__ heavy,
+                                                      int32_t nbins, int log_binw,
+                                                      int32_t* __restrict__ nwin,
+                                                      const int64_t* __restrict__ win_off,
+                                                      Window* __restrict__ wins,
+                                                      uint8_t* __restrict__ win_dense) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PlanShared& s = *reinterpret_cast<PlanShared*>(smem_raw);
+    const int32_t hrow = blockIdx.x;
+    const int32_t row = heavy[hrow];
+    for (int b = threadIdx.x; b < nbins; b += PLAN_T) s.hist[b] = 0;
+    __syncthreads();
+    plan_histogram(m, row, log_binw, s.hist);
+    __syncthreads();
+    const int sub = 1 << (log_binw - LOG_WD);  // dense sub-windows per big bin
+    // Per-bin window-start counts, in blocked arrangement (ITEMS bins/thread).
+    constexpr int ITEMS = MAXBINS / PLAN_T;
+    int32_t excl[ITEMS];
+    int32_t cnt[ITEMS];
+    int32_t local = 0;
+    for (int i = 0; i < ITEMS; ++i) {
+        const int b = threadIdx.x * ITEMS + i;
+        cnt[i] = b < nbins ? s.hist[b] : 0;
+        excl[i] = local;
+        local += cnt[i];
+    }
+    int32_t base, tot;
+    cub::BlockScan<int32_t, PLAN_T>(s.scan).ExclusiveSum(local, base, tot);
+    __syncthreads();
+    // Bin b's exclusive product prefix: base + excl[i].  Window starts:
+    //   big bin (cnt > CAPH): 1 sparse window if cnt <= CAP, else `sub` dense
+    //   small bin: starts a window if first, after a big bin, or when
+    //   floor(prefix / CAPH) changes  (sum of such a run <= CAP).
+    int32_t nstart[ITEMS];
+    int32_t mine = 0;
+    for (int i = 0; i < ITEMS; ++i) {
+        const int b = threadIdx.x * ITEMS + i;
+        nstart[i] = 0;
+        if (b >= nbins) continue;
+        const int32_t pre = base + excl[i];
+        const bool big = cnt[i] > CAPH;
+        if (big) {
+            nstart[i] = cnt[i] > CAP ? sub : 1;
+        } else {
+            bool start = (b == 0);
+            if (!start) {
+                const int32_t pc = s.hist[b - 1];
+                const int32_t ppre = pre - pc;
+                start = (pc > CAPH) || (ppre / CAPH != pre / CAPH);
+            }
+            nstart[i] = start ? 1 : 0;
+        }
+        mine += nstart[i];
+    }
+    int32_t wbase, wtot;
+    cub::BlockScan<int32_t, PLAN_T>(s.scan).ExclusiveSum(mine, wbase, wtot);
+    if (MODE == 0) {
+        if (threadIdx.x == 0) nwin[hrow] = wtot;
+        return;
+    }
+    // MODE 1: record c0 of every window, then emit [c0, c1).
+    int32_t w = wbase;
+    for (int i = 0; i < ITEMS; ++i) {
+        const int b = threadIdx.x * ITEMS + i;
+        if (b >= nbins || nstart[i] == 0) continue;
+        const int32_t c0 = b << log_binw;
+        if (nstart[i] == 1) {
+            s.wc0[w] = c0;
+            s.wstart[w] = (cnt[i] > CAP) ? 1 : 0;  // dense flag
+            ++w;
+        } else {
+            for (int j = 0; j < nstart[i]; ++j) {
+                s.wc0[w] = c0 + (j << LOG_WD);
+                s.wstart[w] = 1;
+                ++w;
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t off = win_off[hrow];
+    for (int k = threadIdx.x; k < wtot; k += PLAN_T) {
+        Window wd;
+        wd.row = row;
+        wd.c0 = s.wc0[k];
+        int64_t c1 = (k + 1 < wtot) ? s.wc0[k + 1] : m.ncols;
+        if (s.wstart[k]) c1 = ::min(c1, int64_t{wd.c0} + WD);
+        wd.c1 = static_cast<int32_t>(::min(c1, int64_t{m.ncols}));
+        wd.first = static_cast<int32_t>(off);
+        wins[off + k] = wd;
+        win_dense[off + k] = static_cast<uint8_t>(s.wstart[k]);
+    }
+}
+
+// Split window ids into sparse / dense lists.
+__global__ void split_windows_kernel(const uint8_t* __restrict__ dense, int64_t nw,
+                                     unsigned long long* __restrict__ cursor,
+                                     int32_t* __restrict__ sparse_ids,
+                                     int32_t* __restrict__ dense_ids) {
+    __shared__ unsigned s_cnt[2];
+    __shared__ unsigned long long s_base[2];
+    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t w = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    int d = 0;
+    unsigned rank = 0;
+    if (w < nw) {
+        d = dense[w];
+        rank = atomicAdd(&s_cnt[d], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
+    __syncthreads();
+    if (w < nw) (d ? dense_ids : sparse_ids)[s_base[d] + rank] = static_cast<int32_t>(w);
+}
+
+template <int T, int I, bool NUMERIC>
+__global__ void __launch_bounds__(T) esc_tile_kernel(Mats m, const int32_t* __restrict__ ids,
+                                                     const Window* __restrict__ wins, OutCtx out) {
+    using S = EscShared<T, I, NUMERIC>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S& s = *reinterpret_cast<S*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int32_t id = ids[blockIdx.x];
+    int32_t row, c0, c1, w = -1;
+    if (wins) {
+        w = id;
+        const Window wd = wins[w];
+        row = wd.row;
+        c0 = wd.c0;
+        c1 = wd.c1;
+    } else {
+        row = id;
+        c0 = 0;
+        c1 = m.ncols;
+    }
+    const bool full = (wins == nullptr);
+    const int total = expand_products<T, I, NUMERIC>(m, row, c0, c1, full, s);
+
+    // Stable LSD radix sort of (column, position) pairs.
+    const uint32_t width = static_cast<uint32_t>(c1 - c0);
+    const int bits = bit_length(width);
+    uint32_t k[I], v[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = tid * I + i;
+        k[i] = e < total ? s.keys[e] : width;
+        v[i] = static_cast<uint32_t>(e);
+    }
+    __syncthreads();
+    typename S::Sort(s.u.sort).Sort(k, v, 0, bits);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        s.keys[tid * I + i] = k[i];
+        s.u.sidx[tid * I + i] = v[i];
+    }
+    __syncthreads();
+    // Run heads = first position of every distinct column.
+    bool head[I];
+    int nh = 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = tid * I + i;
+        head[i] = e < total && (e == 0 || k[i] != s.keys[e - 1]);
+        nh += head[i];
+    }
+    int hoff, tile_cnt;
+    typename S::Scan(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
+    if (!NUMERIC) {
+        if (tid == 0) {
+            if (w >= 0) {
+                out.win_nnz[w] = tile_cnt;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&out.row_nnz[row - out.row_begin]),
+                          static_cast<unsigned long long>(tile_cnt));
+            } else {
+                out.row_nnz[row - out.row_begin] = tile_cnt;
+            }
+        }
+        return;
+    }
+    // Ordered reduction: each run summed left to right from 0.0.
+    double res[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        res[i] = 0.0;
+        if (head[i]) {
+            const int e0 = tid * I + i;
+            double acc = 0.0;
+            int e = e0;
+            do {
+                acc = __dadd_rn(acc, s.vals[s.u.sidx[e]]);
+                ++e;
+            } while (e < total && s.keys[e] == k[i]);
+            res[i] = acc;
+        }
+    }
+    __syncthreads();
+    int r = hoff;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        if (head[i]) {
+            s.keys[r] = k[i] + static_cast<uint32_t>(c0);
+            s.vals[r] = res[i];
+            ++r;
+        }
+    }
+    __syncthreads();
+    int64_t base = out.crp[row - out.row_begin];
+    if (w >= 0) base += out.win_scan[w] - out.win_scan[wins[w].first];
+    for (int e = tid; e < tile_cnt; e += T) {
+        out.ccol[base + e] = static_cast<int32_t>(s.keys[e]);
+        out.cval[base + e] = s.vals[e];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: dense window kernel (heavy windows, width <= WD, any product count)
+// ---------------------------------------------------------------------------
+constexpr int DT = 256;
+constexpr int DI = CAP / DT;
+
+struct DenseShared {
+    using Sort = cub::BlockRadixSort<uint32_t, DT, DI, uint32_t>;
+    using Scan = cub::BlockScan<int32_t, DT>;
+    double acc[WD];
+    uint32_t bitmap[WD / 32];
+    uint32_t keys[CAP];
+    double vals[CAP];
+    union {
+        typename Sort::TempStorage sort;
+        uint32_t sidx[CAP];
+    } u;
+    typename Scan::TempStorage scan;
+    int64_t pstart[DT];
+    int32_t plen[DT];
+    int32_t poff[DT];
+    double pav[DT];
+};
+
+template <bool NUMERIC>
+__global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t* __restrict__ ids,
+                                                          const Window* __restrict__ wins,
+                                                          OutCtx out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DenseShared& s = *reinterpret_cast<DenseShared*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = DT / 32;
+    const int32_t w = ids[blockIdx.x];
+    const Window wd = wins[w];
+    const int32_t row = wd.row, c0 = wd.c0, c1 = wd.c1;
+    for (int e = tid; e < WD / 32; e += DT) s.bitmap[e] = 0u;
+    if (NUMERIC)
+        for (int e = tid; e < WD; e += DT) s.acc[e] = 0.0;
+    __syncthreads();
+    const int64_t rs = m.arp[row], re = m.arp[row + 1];
+    for (int64_t pc = rs; pc < re; pc += DT) {
+        const int64_t p = pc + tid;
+        int len = 0;
+        int64_t start = 0;
+        double av = 0.0;
+        if (p < re) {
+            const int32_t k = __ldg(m.acol + p);
+            int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
+            b0 = lower_bound_col(m.bcol, b0, b1, c0);
+            b1 = lower_bound_col(m.bcol, b0, b1, c1);
+            start = b0;
+            len = static_cast<int>(b1 - b0);
+            if (NUMERIC) av = __ldg(m.aval + p);
+        }
+        int off, chunk;
+        DenseShared::Scan(s.scan).ExclusiveSum(len, off, chunk);
+        s.pstart[tid] = start;
+        s.plen[tid] = len;
+        s.poff[tid] = off;
+        s.pav[tid] = av;
+        __syncthreads();
+        const int nslots = static_cast<int>(::min(int64_t{DT}, re - pc));
+        if (!NUMERIC) {
+            for (int slot = warp; slot < nslots; slot += NW) {
+                const int l = s.plen[slot];
+                const int64_t st = s.pstart[slot];
+                for (int q = lane; q < l; q += 32) {
+                    const uint32_t c = static_cast<uint32_t>(__ldg(m.bcol + st + q) - c0);
+                    atomicOr(&s.bitmap[c >> 5], 1u << (c & 31));
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+        // NUMERIC: batches of CAP products in (k, j) order.
+        for (int b0 = 0; b0 < chunk; b0 += CAP) {
+            const int b1 = min(chunk, b0 + CAP);
+            for (int slot = warp; slot < nslots; slot += NW) {
+                const int o = s.poff[slot], l = s.plen[slot];
+                const int lo = max(o, b0), hi = min(o + l, b1);
+                if (lo >= hi) continue;
+                const int64_t st = s.pstart[slot] + (lo - o);
+                const double a = s.pav[slot];
+                for (int q = lane; q < hi - lo; q += 32) {
+                    s.keys[lo - b0 + q] = static_cast<uint32_t>(__ldg(m.bcol + st + q) - c0);
+                    s.vals[lo - b0 + q] = __dmul_rn(a, __ldg(m.bval + st + q));
+                }
+            }
+            __syncthreads();
+            const int n = b1 - b0;
+            uint32_t k[DI], v[DI];
+#pragma unroll
+            for (int i = 0; i < DI; ++i) {
+                const int e = tid * DI + i;
+                k[i] = e < n ? s.keys[e] : static_cast<uint32_t>(WD);
+                v[i] = static_cast<uint32_t>(e);
+            }
+            __syncthreads();
+            DenseShared::Sort(s.u.sort).Sort(k, v, 0, LOG_WD + 1);
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < DI; ++i) {
+                s.keys[tid * DI + i] = k[i];
+                s.u.sidx[tid * DI + i] = v[i];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < DI; ++i) {
+                const int e0 = tid * DI + i;
+                if (e0 < n && (e0 == 0 || s.keys[e0 - 1] != k[i])) {
+                    double acc = s.acc[k[i]];
+                    int e = e0;
+                    do {
+                        acc = __dadd_rn(acc, s.vals[s.u.sidx[e]]);
+                        ++e;
+                    } while (e < n && s.keys[e] == k[i]);
+                    s.acc[k[i]] = acc;
+                    atomicOr(&s.bitmap[k[i] >> 5], 1u << (k[i] & 31));
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // Bitmap -> count (and sorted output).
+    constexpr int NWORD = WD / 32;  // 128 <= DT
+    const uint32_t word = tid < NWORD ? s.bitmap[tid] : 0u;
+    const int pc = __popc(word);
+    int woff, tot;
+    DenseShared::Scan(s.scan).ExclusiveSum(pc, woff, tot);
+    if (!NUMERIC) {
+        if (tid == 0) {
+            out.win_nnz[w] = tot;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&out.row_nnz[row - out.row_begin]),
+                      static_cast<unsigned long long>(tot));
+        }
+        return;
+    }
+    const int64_t base = out.crp[row - out.row_begin] + out.win_scan[w] - out.win_scan[wd.first];
+    // stage sorted output in keys/vals (batch buffers are free now)
+    uint32_t wbits = word;
+    int r = woff;
+    while (wbits) {
+        const int b = __ffs(wbits) - 1;
+        wbits &= wbits - 1;
+        const uint32_t c = static_cast<uint32_t>(tid * 32 + b);
+        s.keys[r] = c + static_cast<uint32_t>(c0);
+        s.vals[r] = s.acc[c];
+        ++r;
+    }
+    __syncthreads();
+    for (int e = tid; e < tot; e += DT) {
+        out.ccol[base + e] = static_cast<int32_t>(s.keys[e]);
+        out.cval[base + e] = s.vals[e];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+template <int T, int I, bool NUMERIC>
+void launch_esc(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, const Window* wins,
+                const OutCtx& out) {
+    if (n <= 0) return;
+    using S = EscShared<T, I, NUMERIC>;
+    auto k = esc_tile_kernel<T, I, NUMERIC>;
+    set_smem(k, sizeof(S));
+    BSP_LAUNCH(h, k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
+}
+
+template <bool NUMERIC>
+void launch_light(bsp_handle h, int cls, const Mats& m, const int32_t* ids, int64_t n,
+                  const OutCtx& out) {
+    switch (cls) {
+        case 1: launch_esc<32, 4, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 2: launch_esc<64, 8, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 3: launch_esc<128, 16, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 4: launch_esc<256, 16, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        default: break;
+    }
+}
+
+template <bool NUMERIC>
+void launch_dense(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, const Window* wins,
+                  const OutCtx& out) {
+    if (n <= 0) return;
+    auto k = dense_window_kernel<NUMERIC>;
+    set_smem(k, sizeof(DenseShared));
+    BSP_LAUNCH(h, k, static_cast<unsigned>(n), DT, sizeof(DenseShared), m, ids, wins, out);
+}
+
+}  // namespace
+
+Mats make_mats(const bsp_csr* A, const bsp_csr* B) {
+    return Mats{A->row_ptr, A->col_idx, A->values, B->row_ptr, B->col_idx, B->values,
+                static_cast<int32_t>(B->ncols)};
+}
+
+void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
+                       const uint8_t* skip, RowwisePlan& plan, int64_t* prod_out) {
+    const int64_t n = re - rb;
+    plan.rb = rb;
+    plan.n = n;
+    DBuf<uint8_t> cls(h, n);
+    DBuf<int64_t> counters(h, 2 * NCLS);
+    BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * NCLS * sizeof(int64_t), h->stream));
+    const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 256),
+                                                        int64_t{h->sm_count} * 8));
+    BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, rb, n, prod_out, cls.p, skip, counters.p,
+               counters.p + NCLS);
+    int64_t hc[2 * NCLS];
+    d2h(h, hc, counters.p, 2 * NCLS);
+    sync(h);
+    int64_t tot_listed = 0;
+    for (int c = 0; c < NCLS; ++c) {
+        plan.class_count[c] = hc[c];
+        plan.class_products[c] = hc[NCLS + c];
+        plan.class_off[c] = (c == 0) ? 0 : tot_listed;
+        if (c > 0) tot_listed += hc[c];
+    }
+    plan.class_off[NCLS] = tot_listed;
+    h->stats.products = 0;
+    for (int c = 0; c < NCLS; ++c) h->stats.products += plan.class_products[c];
+    plan.lists = DBuf<int32_t>(h, tot_listed);
+    if (tot_listed > 0) {
+        DBuf<unsigned long long> cursor(h, NCLS);
+        std::vector<unsigned long long> cur(NCLS, 0);
+        for (int c = 1; c < NCLS; ++c) cur[c] = static_cast<unsigned long long>(plan.class_off[c]);
+        h2d(h, cursor.p, cur.data(), NCLS);
+        BSP_LAUNCH(h, bucket_kernel, static_cast<unsigned>(div_up(n, 256)), 256, 0, cls.p, rb, n,
+                   cursor.p, plan.lists.p);
+    }
+    // Heavy rows -> windows.
+    const int64_t nh = plan.class_count[NCLS - 1];
+    if (nh > 0) {
+        const int32_t* heavy = plan.lists.p + plan.class_off[NCLS - 1];
+        int log_binw = LOG_WD;
+        while (div_up(m.ncols, int64_t{1} << log_binw) > MAXBINS) ++log_binw;
+        const int32_t nbins = static_cast<int32_t>(div_up(m.ncols, int64_t{1} << log_binw));
+        require(log_binw == LOG_WD,
+                "planner: heavy rows need ncols <= 16M (MAXBINS*WD) in this build");
+        DBuf<int32_t> nwin(h, nh + 1);
+        BSP_CUDA(cudaMemsetAsync(nwin.p, 0, (nh + 1) * sizeof(int32_t), h->stream));
+        auto k0 = plan_kernel<0>;
+        auto k1 = plan_kernel<1>;
+        set_smem(k0, sizeof(PlanShared));
+        set_smem(k1, sizeof(PlanShared));
+        BSP_LAUNCH(h, k0, static_cast<unsigned>(nh), PLAN_T, sizeof(PlanShared), m, heavy, nbins,
+                   log_binw, nwin.p, nullptr, nullptr, nullptr);
+        DBuf<int64_t> woff(h, nh + 1);
+        exclusive_scan_i32_to_i64(h, nwin.p, woff.p, nh + 1);
+        plan.nwin = read_scalar(h, woff.p + nh);
+        plan.wins = DBuf<Window>(h, plan.nwin);
+        DBuf<uint8_t> dense(h, plan.nwin);
+        BSP_LAUNCH(h, k1, static_cast<unsigned>(nh), PLAN_T, sizeof(PlanShared), m, heavy, nbins,
+                   log_binw, nullptr, woff.p, plan.wins.p, dense.p);
+        plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
+        plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
+        DBuf<unsigned long long> cursor(h, 2);
+        BSP_CUDA(cudaMemsetAsync(cursor.p, 0, 2 * sizeof(unsigned long long), h->stream));
+        BSP_LAUNCH(h, split_windows_kernel, static_cast<unsigned>(div_up(plan.nwin, 256)), 256, 0,
+                   dense.p, plan.nwin, cursor.p, plan.sparse_ids.p, plan.dense_ids.p);
+        unsigned long long hcur[2];
+        d2h(h, hcur, cursor.p, 2);
+        sync(h);
+        plan.nsparse = static_cast<int64_t>(hcur[0]);
+        plan.ndense = static_cast<int64_t>(hcur[1]);
+    }
+    for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];
+    h->stats.units[6] = plan.nsparse;
+    h->stats.units[7] = plan.ndense;
+}
+
+template <bool NUMERIC>
+void run_plan(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx& out) {
+    for (int c = 1; c < NCLS - 1; ++c)
+        launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
+    launch_esc<256, 16, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse, plan.wins.p, out);
+    launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
+}
+
+// Symbolic pass of a plan: exact per-row counts (row_nnz must be zeroed by
+// the caller) and per-window counts.
+void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t* row_nnz,
+                   DBuf<int64_t>& win_nnz) {
+    win_nnz = DBuf<int64_t>(h, plan.nwin + 1);
+    BSP_CUDA(cudaMemsetAsync(win_nnz.p, 0, (plan.nwin + 1) * sizeof(int64_t), h->stream));
+    OutCtx out{};
+    out.row_begin = plan.rb;
+    out.row_nnz = row_nnz;
+    out.win_nnz = win_nnz.p;
+    run_plan<false>(h, m, plan, out);
+}
+
+void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
+                  const int64_t* win_scan, int32_t* ccol, double* cval) {
+    OutCtx out{};
+    out.row_begin = plan.rb;
+    out.crp = crp;
+    out.win_scan = win_scan;
+    out.ccol = ccol;
+    out.cval = cval;
+    run_plan<true>(h, m, plan, out);
+}
+
+void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t rb, int64_t re,
+                      bsp_csr* C, const uint8_t* row_skip, int64_t* row_nnz_out) {
+    check_csr(A, "spgemm_rowwise");
+    check_csr(B, "spgemm_rowwise");
+    require(A->ncols == B->nrows, "spgemm: dimension mismatch (a.ncols != b.nrows)");
+    require(rb >= 0 && rb <= re && re <= A->nrows, "spgemm: bad row range");
+    BSP_CUDA(cudaSetDevice(h->device));
+    h->stats = bsp_exec_stats{};
+    h->stats.chunks = 1;
+    const Mats m = make_mats(A, B);
+    const int64_t n = re - rb;
+    RowwisePlan plan;
+    build_plan(h, m, rb, re, row_skip, plan, nullptr);
+    DBuf<int64_t> crp(h, n + 1);
+    BSP_CUDA(cudaMemsetAsync(crp.p, 0, (n + 1) * sizeof(int64_t), h->stream));
+    DBuf<int64_t> win_nnz;
+    plan_symbolic(h, m, plan, crp.p, win_nnz);
+    // crp currently holds per-row counts in [0, n); scan in place over n+1.
+    BSP_CUDA(cudaMemsetAsync(crp.p + n, 0, sizeof(int64_t), h->stream));
+    if (row_nnz_out)
+        BSP_CUDA(cudaMemcpyAsync(row_nnz_out, crp.p, n * sizeof(int64_t),
+                                 cudaMemcpyDeviceToDevice, h->stream));
+    DBuf<int64_t> rp(h, n + 1);
+    exclusive_scan_i64(h, crp.p, rp.p, n + 1);
+    DBuf<int64_t> win_scan(h, plan.nwin + 1);
+    if (plan.nwin > 0) exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
+    const int64_t nnz = read_scalar(h, rp.p + n);
+    h->stats.nnz_out = nnz;
+    DBuf<int32_t> ccol(h, nnz);
+    DBuf<double> cval(h, nnz);
+    plan_numeric(h, m, plan, rp.p, win_scan.p, ccol.p, cval.p);
+    C->nrows = n;
+    C->ncols = B->ncols;
+    C->nnz = nnz;
+    C->row_ptr = rp.release();
+    C->col_idx = ccol.release();
+    C->values = cval.release();
+    C->owned = 1;
+}
+
+}  // namespace bsp
+
+using namespace bsp;
+
+extern "C" {
+
+int bsp_spgemm_products(bsp_handle h, const bsp_csr* A, const bsp_csr* B,
+                        int64_t* row_products_dev, int64_t* total_out) {
+    return guarded([&] {
+        check_csr(A, "spgemm_products");
+        check_csr(B, "spgemm_products");
+        require(A->ncols == B->nrows, "spgemm: dimension mismatch (a.ncols != b.nrows)");
+        BSP_CUDA(cudaSetDevice(h->device));
+        const Mats m = make_mats(A, B);
+        RowwisePlan plan;
+        DBuf<int64_t> tmp;
+        int64_t* prod = row_products_dev;
+        if (!prod) {
+            tmp = DBuf<int64_t>(h, A->nrows);
+            prod = tmp.p;
+        }
+        const int64_t n = A->nrows;
+        DBuf<uint8_t> cls(h, n);
+        DBuf<int64_t> counters(h, 2 * NCLS);
+        BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * NCLS * sizeof(int64_t), h->stream));
+        const int grid = static_cast<int>(std::min<int64_t>(
+            div_up(std::max<int64_t>(n, 1), 256), int64_t{h->sm_count} * 8));
+        BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, 0, n, prod, cls.p, nullptr, counters.p,
+                   counters.p + NCLS);
+        int64_t hc[2 * NCLS];
+        d2h(h, hc, counters.p, 2 * NCLS);
+        sync(h);
+        int64_t tot = 0;
+        for (int c = 0; c < NCLS; ++c) tot += hc[NCLS + c];
+        if (total_out) *total_out = tot;
+    });
+}
+
+int bsp_spgemm_symbolic(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t* counts_dev) {
+    return guarded([&] {
+        check_csr(A, "spgemm_symbolic");
+        check_csr(B, "spgemm_symbolic");
+        require(A->ncols == B->nrows, "spgemm: dimension mismatch (a.ncols != b.nrows)");
+        BSP_CUDA(cudaSetDevice(h->device));
+        const Mats m = make_mats(A, B);
+        RowwisePlan plan;
+        build_plan(h, m, 0, A->nrows, nullptr, plan, nullptr);
+        BSP_CUDA(cudaMemsetAsync(counts_dev, 0, std::max<int64_t>(A->nrows, 1) * sizeof(int64_t),
+                                 h->stream));
+        DBuf<int64_t> win_nnz;
+        plan_symbolic(h, m, plan, counts_dev, win_nnz);
+        sync(h);
+    });
+}
+
+int bsp_spgemm_rowwise(bsp_handle h, const bsp_csr* A, const bsp_csr* B, bsp_csr* C) {
+    return guarded([&] {
+        require(C != nullptr, "spgemm_rowwise: null output");
+        check_csr(A, "spgemm_rowwise");
+        rowwise_multiply(h, A, B, 0, A->nrows, C, nullptr, nullptr);
+    });
+}
+
+int bsp_spgemm_rowwise_range(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t row_begin,
+                             int64_t row_end, bsp_csr* C) {
+    return guarded([&] {
+        require(C != nullptr, "spgemm_rowwise_range: null output");
+        rowwise_multiply(h, A, B, row_begin, row_end, C, nullptr, nullptr);
+    });
+}
+
+int bsp_spgemm_rowwise_host(bsp_handle h, const bsp_host_csr* A, const bsp_host_csr* B,
+                            bsp_host_csr* C) {
+    return guarded([&] {
+        check_host_csr(A, "spgemm_rowwise_host");
+        check_host_csr(B, "spgemm_rowwise_host");
+        require(A->ncols == B->nrows, "spgemm: dimension mismatch (a.ncols != b.nrows)");
+        bsp_csr dA{}, dB{}, dC{};
+        auto check = [](int rc) {
+            if (rc != BSP_OK) throw std::runtime_error(bsp_last_error());
+        };
+        check(bsp_csr_upload(h, A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values, &dA));
+        const bool alias = (A == B) || (A->row_ptr == B->row_ptr && A->col_idx == B->col_idx &&
+                                        A->values == B->values);
+        if (!alias)
+            check(bsp_csr_upload(h, B->nrows, B->ncols, B->row_ptr, B->col_idx, B->values, &dB));
+        int rc = bsp_spgemm_rowwise(h, &dA, alias ? &dA : &dB, &dC);
+        if (rc == BSP_OK) {
+            C->nrows = dC.nrows;
+            C->ncols = dC.ncols;
+            C->nnz = dC.nnz;
+            C->row_ptr = host_malloc<int64_t>(dC.nrows + 1);
+            C->col_idx = host_malloc<int32_t>(dC.nnz);
+            C->values = host_malloc<double>(dC.nnz);
+            rc = bsp_csr_download(h, &dC, C->row_ptr, C->col_idx, C->values);
+        }
+        bsp_csr_free(h, &dC);
+        bsp_csr_free(h, &dA);
+        if (!alias) bsp_csr_free(h, &dB);
+        check(rc);
+    });
+}
+
+int bsp_partition_rows(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int32_t nparts,
+                       int64_t* bounds_out) {
+    return guarded([&] {
+        require(nparts >= 1, "partition_rows: nparts must be >= 1");
+        const int64_t n = A->nrows;
+        DBuf<int64_t> prod(h, n + 1);
+        int64_t total = 0;
+        const int rc = bsp_spgemm_products(h, A, B, prod.p, &total);
+        if (rc != BSP_OK) throw std::runtime_error(bsp_last_error());
+        BSP_CUDA(cudaMemsetAsync(prod.p + n, 0, sizeof(int64_t), h->stream));
+        DBuf<int64_t> scan(h, n + 1);
+        exclusive_scan_i64(h, prod.p, scan.p, n + 1);
+        std::vector<int64_t> hs(n + 1);
+        d2h(h, hs.data(), scan.p, n + 1);
+        sync(h);
+        bounds_out[0] = 0;
+        for (int32_t g = 1; g < nparts; ++g) {
+            // first row whose exclusive prefix reaches total*g/nparts
+            const int64_t target = static_cast<int64_t>(
+                (static_cast<__int128>(hs[n]) * g) / nparts);
+            const int64_t r = std::lower_bound(hs.begin(), hs.end(), target) - hs.begin();
+            bounds_out[g] = std::max(bounds_out[g - 1], std::min<int64_t>(r, n));
+        }
+        bounds_out[nparts] = n;
+    });
+}
+
+}  // extern "C"
