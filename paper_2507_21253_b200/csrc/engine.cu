@@ -9,6 +9,22 @@
 
 namespace bsp {
 
+bool trace_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("BSP_TRACE");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
+void trace_launch(bsp_handle h, const char* name, long long grid) {
+    std::fprintf(stderr, "[bsp] launch %s grid=%lld ...", name, grid);
+    std::fflush(stderr);
+    const cudaError_t e = cudaStreamSynchronize(h->stream);
+    std::fprintf(stderr, " %s\n", e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+    std::fflush(stderr);
+}
+
 void exclusive_scan_i64(bsp_handle h, const int64_t* in, int64_t* out, int64_t n) {
     if (n <= 0) return;
     size_t tmp = 0;

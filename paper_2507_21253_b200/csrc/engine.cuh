@@ -43,8 +43,13 @@ inline void cuda_check(cudaError_t e, const char* what) {
             ::bsp::cuda_check(cudaGetLastError(), #kernel);                            \
             ++(h)->launches;                                                           \
             ++(h)->stats.kernels_launched;                                             \
+            if (::bsp::trace_enabled()) ::bsp::trace_launch((h), #kernel, (grid));     \
         }                                                                              \
     } while (0)
+
+// BSP_TRACE=1: synchronise and log every engine launch (debugging only).
+bool trace_enabled();
+void trace_launch(bsp_handle h, const char* name, long long grid);
 
 // Stream-ordered device allocation from the device's default memory pool
 // (release threshold raised at handle creation so repeated calls reuse it).

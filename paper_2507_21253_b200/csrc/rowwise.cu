@@ -129,9 +129,9 @@ __device__ void plan_histogram(const Mats& m, int32_t row, int log_binw, int32_t
             // columns are sorted within the B row, so equal bins form runs:
             // the last lane of each run adds the run length.
             const int32_t nxt = __shfl_down_sync(0xffffffffu, bin, 1);
+            const int32_t prv = __shfl_up_sync(0xffffffffu, bin, 1);
             const bool tail = ok && (lane == 31 || nxt != bin);
-            const unsigned heads = __ballot_sync(
-                0xffffffffu, ok && (lane == 0 || __shfl_up_sync(0xffffffffu, bin, 1) != bin));
+            const unsigned heads = __ballot_sync(0xffffffffu, ok && (lane == 0 || prv != bin));
             if (tail) {
                 const unsigned below = heads & ((2u << lane) - 1u);
                 const int head_lane = 31 - __clz(below);

@@ -1,0 +1,168 @@
+"""GPU parity of the cluster-wise path, CSR_Cluster format and candidate
+generation against the oracle / reference (cluster_spgemm_test.cpp,
+cluster_format_test.cpp, clustering_test.cpp, spgemm_rowwise_test.cpp:148-207).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2507_21253_b200 as B
+from helpers import (assert_csr_identical, csr_from_rows, grouped_identical_rows, identity_csr,
+                     random_assignment, random_csr)
+
+pytestmark = pytest.mark.gpu
+
+
+def clusterwise(engine, a, asg, b=None):
+    A = engine.upload(a)
+    Bd = A if b is None else engine.upload(b)
+    Ac = engine.build_csr_cluster(A, asg)
+    return engine.spgemm_clusterwise(Ac, Bd).download()
+
+
+@pytest.mark.parametrize("cfg,scale", [(2, 512), (2, 2048), (4, 16), (5, 13), (3, 12)])
+def test_hierarchical_clusterwise_equals_rowwise(engine, cfg, scale):
+    a = B.make_config(cfg, scale)
+    asg = engine.hierarchical_clusters(a)
+    c = clusterwise(engine, a, asg)
+    assert_csr_identical(c, O.spgemm_rowwise(a, a), f"cfg{cfg} cluster-wise")
+
+
+def test_strategies_corpus(engine):
+    """acceptance_main.cpp:53-77 style: random matrices x 4 strategies."""
+    rng = np.random.default_rng(11)
+    for seed in range(24):
+        n = int(rng.integers(1, 101))
+        a = random_csr(n, n, 0.01 + 0.29 * rng.random(), seed)
+        for asg in (B.fixed_length_clusters(n, 1), B.fixed_length_clusters(n, 4),
+                    B.variable_length_clusters(a), engine.hierarchical_clusters(a),
+                    random_assignment(n, 8, seed)):
+            assert_csr_identical(clusterwise(engine, a, asg), O.spgemm_rowwise(a, a), f"seed {seed}")
+
+
+def test_singletons_equal_rowwise_exactly(engine):
+    """cluster_spgemm_test.cpp:20-26."""
+    a = random_csr(40, 40, 0.15, 5)
+    assert_csr_identical(clusterwise(engine, a, B.ClusterAssignment.singletons(40)),
+                         O.spgemm_rowwise(a, a))
+
+
+def test_identity_times_b(engine):
+    """cluster_spgemm_test.cpp:28-36."""
+    b = random_csr(12, 9, 0.3, 8)
+    c = clusterwise(engine, identity_csr(12), B.fixed_length_clusters(12, 4), b)
+    assert B.csr_equal_canonical(c, b, 0.0)
+
+
+def test_format_matches_oracle(engine):
+    """CSR_Cluster layout: merged columns, values, valid bits, slots
+    (cluster_format_test.cpp:44-101)."""
+    for seed in range(6):
+        a = random_csr(50, 45, 0.12, 100 + seed)
+        asg = random_assignment(50, 8, seed)
+        Ac = engine.build_csr_cluster(engine.upload(a), asg)
+        got = Ac.download()
+        ref = O.build_csr_cluster(a, asg.cluster_ptr, asg.rows)
+        for k in ("cluster_sizes", "cluster_col_ptr", "col_idx", "value_ptr", "row_map"):
+            assert np.array_equal(got[k], ref[k]), k
+        assert np.array_equal(got["values"].view(np.uint64), ref["values"].view(np.uint64))
+        assert np.array_equal(got["valid"], ref["valid"])
+        back = engine.cluster_to_csr(Ac).download()
+        assert B.csr_equal_canonical(back, a, 0.0)  # round trip (acceptance 6)
+
+
+def test_fig5_padding_kat(engine):
+    """cluster_format_test.cpp: cluster {0,5},{0},{0,5} -> 2 cols x 3 members, 1 placeholder."""
+    a = csr_from_rows(6, [[0, 5], [0], [0, 5]])
+    Ac = engine.build_csr_cluster(engine.upload(a), B.ClusterAssignment.from_lists([[0, 1, 2]]))
+    d = Ac.download()
+    assert list(d["col_idx"]) == [0, 5] and Ac.value_slots() == 6 and d["placeholders"] == 1
+
+
+def test_cluster_output_format(engine):
+    """Optional CSR_Cluster C equals the reference's C format."""
+    a = B.make_config(2, 256)
+    asg = engine.hierarchical_clusters(a)
+    A = engine.upload(a)
+    Ac = engine.build_csr_cluster(A, asg)
+    c, cc = engine.spgemm_clusterwise(Ac, A, want_cluster=True)
+    csr, d, _ = O.spgemm_clusterwise(a, asg.cluster_ptr, asg.rows, a)
+    got = cc.download()
+    for k in ("cluster_sizes", "cluster_col_ptr", "col_idx", "value_ptr", "row_map", "valid"):
+        assert np.array_equal(got[k], d[k]), k
+    assert np.array_equal(got["values"].view(np.uint64), d["values"].view(np.uint64))
+
+
+def test_access_stats_match_oracle(engine):
+    """cluster_spgemm_test.cpp:86-130 / acceptance 5: exact counters."""
+    a = grouped_identical_rows(6, 8, 5)
+    asg = engine.hierarchical_clusters(a)
+    A = engine.upload(a)
+    st = engine.cluster_access_stats(engine.build_csr_cluster(A, asg), A)
+    rw = engine.rowwise_access_stats(A, A)
+    assert st.b_row_loads * 8 == rw.b_row_loads == a.nnz()
+    b = B.make_config(2, 512)
+    asg = engine.hierarchical_clusters(b)
+    Bd = engine.upload(b)
+    st = engine.cluster_access_stats(engine.build_csr_cluster(Bd, asg), Bd)
+    _, _, ost = O.spgemm_clusterwise(b, asg.cluster_ptr, asg.rows, b)
+    assert (st.b_row_loads, st.a_inner_iters, st.placeholder_skips) == ost
+
+
+# ----------------------------------------------------------------- candidates
+@pytest.mark.parametrize("cfg,scale", [(2, 512), (2, 4096), (4, 16), (5, 13), (3, 12), (3, 14)])
+def test_topk_identical_to_reference(engine, cfg, scale):
+    a = B.make_config(cfg, scale)
+    A = engine.upload(B.binarize(a))
+    got = engine.spgemm_topk(A, engine.transpose(A), 7, 0.3)
+    ref = O.spgemm_topk(a, 7, 0.3)
+    assert got.size == ref.size
+    assert np.array_equal(got["i"], ref["i"]) and np.array_equal(got["j"], ref["j"])
+    assert np.array_equal(got["score"].view(np.uint64), ref["score"].view(np.uint64))
+
+
+def test_topk_kats(engine):
+    """spgemm_rowwise_test.cpp:148-169."""
+    e = engine
+    i9 = identity_csr(9)
+    I = e.upload(i9)
+    assert e.spgemm_topk(I, e.transpose(I), 7, 0.3).size == 0
+    a = csr_from_rows(6, [[0, 1, 2], [0, 1, 2], [5]])
+    A = e.upload(a)
+    p = e.spgemm_topk(A, e.transpose(A), 7, 0.3)
+    assert p.size == 1 and (p[0]["i"], p[0]["j"], p[0]["score"]) == (0, 1, 1.0)
+    a = csr_from_rows(3, [[0, 1], [1, 2]])
+    A = e.upload(a)
+    assert e.spgemm_topk(A, e.transpose(A), 7, 0.3).size == 1
+    assert e.spgemm_topk(A, e.transpose(A), 7, 0.4).size == 0
+
+
+def test_hierarchical_identical_to_reference(engine):
+    """clustering_test.cpp:109-137 KATs + seeded recipes vs the reference merge."""
+    a = csr_from_rows(6, [[0, 1, 2], [5], [0, 1, 2]])
+    assert engine.hierarchical_clusters(a).clusters == [[0, 2], [1]]
+    ten = grouped_identical_rows(1, 10, 4)
+    sizes = sorted(engine.hierarchical_clusters(ten).sizes().tolist(), reverse=True)[:3]
+    assert sizes == [8, 1, 1]
+    for cfg, sc in [(2, 1024), (4, 16), (5, 13)]:
+        m = B.make_config(cfg, sc)
+        ptr, rows = O.merge_candidates(m, O.spgemm_topk(m, 7, 0.3), 0.3, 8)
+        got = engine.hierarchical_clusters(m)
+        assert np.array_equal(got.cluster_ptr, ptr) and np.array_equal(got.rows, rows)
+
+
+def test_minhash_invariants(engine):
+    """Minhash/LSH (north-star item 4; unpinned): partition, size cap, every
+    candidate's score is the exact Jaccard >= threshold, planted clusters found."""
+    a = B.make_config(2, 1024)
+    A = engine.upload(a)
+    pairs = engine.minhash_candidates(A, 64, 32, 1, 7, 0.3)
+    assert pairs.size > 0
+    for p in pairs[:: max(1, pairs.size // 200)]:
+        assert p["score"] >= 0.3
+        assert p["score"] == O.jaccard(a, int(p["i"]), int(p["j"]))
+    asg = engine.hierarchical_clusters(a, method="minhash")
+    asg.validate(a.nrows)
+    assert asg.sizes().max() <= 8
+    c = clusterwise(engine, a, asg)
+    assert_csr_identical(c, O.spgemm_rowwise(a, a), "minhash cluster-wise")
