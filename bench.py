@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""bench.py — A·B SpGEMM GFLOP/s (2 x intermediate products / s) and % of the
+HBM roofline on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE cfg5, R-MAT scale 22 / edge factor 8 /
+(0.45, 0.22, 0.22, 0.11), symmetrised, C = A·A row-wise (the largest
+single-GPU configuration).  N>1 (torchrun): the same matrix,
+A rows sharded by cumulative products, B replicated with an NCCL broadcast
+(outside the timed region), no collective during the multiply.
+
+One step = one complete multiply (products/binning, symbolic, int64 scan,
+C allocation from the stream-ordered pool, numeric) on inputs already
+resident in HBM.  Inputs (A = B, 0.81 GB) exceed the 126 MB L2, so no L2
+flush is needed between steps.
+
+Keys beyond the driver contract:
+  e2e          the same metric through the reference-shaped host-buffer
+               pipeline (pinned host A -> H2D -> multiply in row chunks ->
+               D2H of every chunk of C into pinned host buffers), timed per
+               step on the wall clock with the copies inside.
+  roofline     bytes_alg = 12(nnzA+nnzB+nnzC) + 8(rowsA+rowsB+rowsC+3)
+                / measured step time vs MEASURED_PEAKS hbm_gbs.
+  cpu_baseline the UNMODIFIED reference (oracle/_ref, OpenMP, all host cores)
+               on a bounded strided row sample of the same matrix.
+
+--impl reference: times the reference's CPU row-wise SpGEMM (oracle/_ref)
+on bounded row samples of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG = 5
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        d = json.loads(PEAKS.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def bytes_alg(nnz_a, nnz_b, nnz_c, rows_a, rows_b, rows_c):
+    return 12 * (nnz_a + nnz_b + nnz_c) + 8 * (rows_a + rows_b + rows_c + 3)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+def cpu_reference_sample(a, stride: int, offset: int, threads: int):
+    """Reference row-wise SpGEMM (oracle/_ref) on the strided row sample
+    {offset, offset+stride, ...} of A against the full B = A.  Returns
+    (seconds, products in the sample)."""
+    import oracle as O
+
+    rows = np.arange(offset, a.nrows, stride, dtype=np.int64)
+    lens = np.diff(a.row_ptr)[rows]
+    rp = np.zeros(rows.size + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    idx = np.concatenate([np.arange(a.row_ptr[r], a.row_ptr[r + 1]) for r in rows]) \
+        if rows.size else np.zeros(0, np.int64)
+    sub = O.Csr(rows.size, a.ncols, rp, a.col_idx[idx], a.values[idx])
+    blen = np.diff(a.row_ptr)
+    products = int(blen[sub.col_idx].sum())
+    t0 = time.perf_counter()
+    O.ref_spgemm_rowwise(sub, a, threads=threads)
+    return time.perf_counter() - t0, products
+
+
+def run_reference(args, a, rank: int):
+    import oracle as O
+
+    cfg = {"workload": "cfg5_rmat22_ef8_AxA_rowwise", "matrix": "R-MAT s22 ef8 (0.45,0.22,0.22)",
+           "n": a.nrows, "nnz_a": a.nnz()}
+    if not O.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    threads = os.cpu_count() or 1
+    stride = args.ref_stride
+    vals = []
+    secs, prods = 0.0, 0
+    for s in range(args.warmup + args.steps):
+        t, p = cpu_reference_sample(a, stride, s % stride, threads)
+        if s >= args.warmup:
+            vals.append(2.0 * p / t / 1e9)
+            secs += t
+            prods += p
+    value = 2.0 * prods / secs / 1e9
+    line = {
+        "impl": "reference", "metric": "A·B SpGEMM GFLOP/s (2×products/s)", "value": value,
+        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT, BASELINE cfg5)",
+        "config": dict(cfg, sample=f"rows i = s mod {stride} per step (1/{stride} of rows)"),
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                         "sample": f"1/{stride} strided row sample per step, B = full A"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=None, help="override R-MAT scale (debug)")
+    ap.add_argument("--ref-stride", type=int, default=512)
+    ap.add_argument("--cpu-stride", type=int, default=128)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=8)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import paper_2507_21253_b200 as B
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        a = B.make_config(CFG, args.scale)
+        run_reference(args, a, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    # ---- input: generated on rank 0, replicated with an NCCL broadcast ----
+    if rank == 0:
+        a = B.make_config(CFG, args.scale)
+        meta = torch.tensor([a.nrows, a.ncols, a.nnz()], dtype=torch.int64, device="cuda")
+    else:
+        a = None
+        meta = torch.zeros(3, dtype=torch.int64, device="cuda")
+    if dist:
+        dist.broadcast(meta, 0)
+    n, ncols, nnz = (int(x) for x in meta.tolist())
+    if rank == 0:
+        rp_t = torch.from_numpy(a.row_ptr).cuda()
+        ci_t = torch.from_numpy(a.col_idx).cuda()
+        v_t = torch.from_numpy(a.values).cuda()
+    else:
+        rp_t = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        ci_t = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        v_t = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    if dist:
+        for t in (rp_t, ci_t, v_t):
+            dist.broadcast(t, 0)
+    torch.cuda.synchronize()
+
+    eng = B.Engine(local)
+    stream = torch.cuda.Stream()
+    eng.set_stream(stream.cuda_stream)
+    A = eng.view_torch(n, ncols, rp_t, ci_t, v_t)
+    total_products = eng.spgemm_products(A, A)
+    bounds = eng.partition_rows(A, A, world) if world > 1 else np.array([0, n])
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+
+    def step():
+        C = eng.spgemm_rowwise(A, A) if world == 1 else eng.spgemm_rowwise_range(A, A, r0, r1)
+        return C
+
+    for _ in range(args.warmup):
+        C = step()
+        C.free()
+    torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps, events on the engine's stream ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    nnz_c_local = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = eng.kernel_launches()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for s in range(args.steps):
+            evs[s][0].record(stream)
+            C = step()
+            evs[s][1].record(stream)
+            nnz_c_local = C.nnz()
+            C.free()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    launches = eng.kernel_launches() - l0
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    local_ms = float(sum(step_ms))
+    # per-kernel breakdown of one extra (untimed) profiled step
+    eng.profile(True)
+    C = step()
+    C.free()
+    kprof = eng.profile_report()
+    eng.profile(False)
+
+    t = torch.tensor([local_ms, float(nnz_c_local)], dtype=torch.float64, device="cuda")
+    if dist:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+        total_ms, nnz_c = float(tmax[0]), int(tsum[1])
+    else:
+        total_ms, nnz_c = local_ms, nnz_c_local
+    ms_per_step = total_ms / args.steps
+    value = 2.0 * total_products / (ms_per_step * 1e-3) / 1e9
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = hbm_peak()
+    bal = bytes_alg(nnz, nnz, nnz_c, n, n, n)
+    achieved = bal / (ms_per_step * 1e-3) / 1e9
+    ktot = sum(v[1] for v in kprof.values()) or 1.0
+    top = max(kprof.items(), key=lambda kv: kv[1][1]) if kprof else ("none", (0, 0.0))
+    kernels = {k: {"launches": v[0], "ms": round(v[1], 3), "share": round(v[1] / ktot, 4)}
+               for k, v in sorted(kprof.items(), key=lambda kv: -kv[1][1])}
+    traffic = None
+    tf = ROOT / "profiles" / "traffic_cfg5.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "A·B SpGEMM GFLOP/s (2×products/s)",
+        "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded R-MAT, BASELINE cfg5; inputs 0.81 GB > L2, no flush)",
+        "config": {"workload": "cfg5_rmat22_ef8_AxA_rowwise" if args.scale is None
+                   else f"rmat{args.scale}_ef8_AxA_rowwise",
+                   "n": n, "nnz_a": nnz, "products": total_products, "nnz_c": nnz_c,
+                   "parallelism": f"row-shard x{world}", "l2": "inputs larger than L2"},
+        "gpu_launches": launches,
+        "wall_ms_per_step": 1e3 * t_wall / args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+                     "frac": achieved / (peak * world), "traffic": traffic,
+                     "bytes_alg_per_step": bal, "peak_source": peak_kind,
+                     "unit_of_work": "one full multiply (all kernels of the step)",
+                     "dominant_kernel": top[0], "dominant_share": round(top[1][1] / ktot, 4)},
+        "kernels": kernels,
+        "clocks": clk.summary(),
+    }
+
+    # ---- e2e: host-buffer pipeline through the public API ----------------
+    if not args.no_e2e and world == 1:
+        line["e2e"] = run_e2e(B, eng, a, args, total_products)
+    # ---- cpu baseline (rank 0, N=1) --------------------------------------
+    if not args.no_cpu and world == 1:
+        import oracle as O
+
+        if O.have_ref():
+            secs, prods = cpu_reference_sample(a, args.cpu_stride, 0, os.cpu_count() or 1)
+            line["cpu_baseline"] = {
+                "value": 2.0 * prods / secs / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(),
+                "kind": "reference",
+                "sample": f"rows i = 0 mod {args.cpu_stride} (1/{args.cpu_stride} of rows), "
+                          f"{prods} products, {secs:.2f} s; B = full A"}
+        else:
+            line["cpu_baseline"] = None
+    print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(B, eng, a, args, total_products):
+    """Reference-shaped call with HOST buffers: pinned A -> device (H2D), the
+    multiply in row chunks, each chunk of C copied back (D2H) into a pinned
+    host ring by a second engine handle whose stream waits on the compute
+    stream, so the copy engine overlaps the next chunk's kernels."""
+    import torch
+
+    nchunks = args.e2e_chunks
+    hp = [torch.from_numpy(x).pin_memory() for x in (a.row_ptr, a.col_idx, a.values)]
+    h2d = sum(x.numel() * x.element_size() for x in hp)
+    ce = B.Engine(eng.device)  # copy handle (own stream)
+    cstream = torch.cuda.ExternalStream(ce.stream_ptr())
+    # size the pinned ring from one untimed pass
+    dev = [x.cuda() for x in hp]
+    torch.cuda.synchronize()
+    A = eng.view_torch(a.nrows, a.ncols, *dev)
+    bounds = eng.partition_rows(A, A, nchunks)
+    sizes = []
+    for g in range(nchunks):
+        C = eng.spgemm_rowwise_range(A, A, int(bounds[g]), int(bounds[g + 1]))
+        sizes.append((C.nrows, C.nnz()))
+        C.free()
+    max_rows = max(r for r, _ in sizes)
+    max_nnz = max(z for _, z in sizes)
+    ring = [(torch.empty(max_rows + 1, dtype=torch.int64).pin_memory(),
+             torch.empty(max(max_nnz, 1), dtype=torch.int32).pin_memory(),
+             torch.empty(max(max_nnz, 1), dtype=torch.float64).pin_memory()) for _ in range(2)]
+    del dev, A
+    torch.cuda.synchronize()
+    times, d2h = [], 0
+    steps = max(1, min(args.steps, 3))
+    mstream = torch.cuda.ExternalStream(eng.stream_ptr())
+    for s in range(1 + steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(mstream):
+            dev = [x.cuda(non_blocking=True) for x in hp]
+        A = eng.view_torch(a.nrows, a.ncols, *dev)
+        slot_ev = [None, None]
+        d2h = 0
+        for g in range(nchunks):
+            C = eng.spgemm_rowwise_range(A, A, int(bounds[g]), int(bounds[g + 1]))
+            slot = g % 2
+            if slot_ev[slot] is not None:
+                slot_ev[slot].synchronize()  # host ring slot free again
+            ce.wait_for(eng)
+            rp, ci, v = ring[slot]
+            C.download_async(rp.data_ptr(), ci.data_ptr(), v.data_ptr(), engine=ce)
+            d2h += (C.nrows + 1) * 8 + C.nnz() * 12
+            ev = torch.cuda.Event()
+            ev.record(cstream)
+            slot_ev[slot] = ev
+            C.free(engine=ce)  # stream-ordered after its copy
+        ce.synchronize()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if s > 0:
+            times.append(dt)
+        del dev, A
+    ce.close()
+    t = statistics.median(times)
+    return {"value": 2.0 * total_products / t / 1e9, "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t,
+            "chunks": nchunks,
+            "path": "pinned H2D of A + bsp_spgemm_rowwise_range per row chunk + "
+                    "bsp_csr_download_async of every chunk of C into a pinned host ring"}
+
+
+if __name__ == "__main__":
+    main()

@@ -126,8 +126,14 @@ const char* bsp_last_error(void);
 const char* bsp_version(void);
 int bsp_create(int device, bsp_handle* out);
 int bsp_destroy(bsp_handle h);
-/* Run on an external stream (e.g. torch.cuda.current_stream()); NULL = own. */
+/* Run on an external stream (e.g. torch's current stream); NULL = the legacy
+ * default stream. */
 int bsp_set_stream(bsp_handle h, void* cuda_stream);
+/* Per-launch CUDA-event profiling of engine kernels (bench / diagnostics).
+ * bsp_profile_report synchronises, writes "name\tlaunches\tms\n" lines into
+ * buf (NUL-terminated, truncated to cap) and returns the full length. */
+int bsp_profile(bsp_handle h, int on);
+int64_t bsp_profile_report(bsp_handle h, char* buf, int64_t cap);
 void* bsp_get_stream(bsp_handle h);
 int bsp_synchronize(bsp_handle h);
 /* Number of engine kernels launched by this handle since creation. */
@@ -145,6 +151,11 @@ int bsp_csr_view(int64_t nrows, int64_t ncols, int64_t nnz, int64_t* row_ptr,
 /* Copy a device CSR into caller-provided host arrays (sizes from the struct). */
 int bsp_csr_download(bsp_handle h, const bsp_csr* m, int64_t* row_ptr, int32_t* col_idx,
                      double* values);
+/* Same, enqueued on the handle's stream without synchronising. */
+int bsp_csr_download_async(bsp_handle h, const bsp_csr* m, int64_t* row_ptr, int32_t* col_idx,
+                           double* values);
+/* Make `waiter`'s stream wait for all work enqueued so far on `signaler`'s. */
+int bsp_stream_wait(bsp_handle waiter, bsp_handle signaler);
 int bsp_csr_free(bsp_handle h, bsp_csr* m);
 /* Pinned host allocation helpers (for end-to-end host-buffer calls). */
 int bsp_host_alloc(size_t bytes, void** out);

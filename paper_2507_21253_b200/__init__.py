@@ -340,9 +340,17 @@ class DeviceCsr:
                                                 _ptr(v)))
         return CsrMatrix(n, self.ncols, rp, ci, v)
 
-    def free(self) -> None:
-        if self.s is not None and self.engine.h:
-            self.engine.lib.bsp_csr_free(self.engine.h, C.byref(self.s))
+    def download_async(self, row_ptr: int, col_idx: int, values: int,
+                       engine: Optional["Engine"] = None) -> None:
+        """Enqueue D2H copies into caller buffers (e.g. pinned) on `engine`'s stream."""
+        e = engine or self.engine
+        _check(e.lib.bsp_csr_download_async(e.h, C.byref(self.s), row_ptr, col_idx, values))
+
+    def free(self, engine: Optional["Engine"] = None) -> None:
+        """Release (stream-ordered on `engine`'s stream, default the owner's)."""
+        e = engine or self.engine
+        if self.s is not None and e.h:
+            e.lib.bsp_csr_free(e.h, C.byref(self.s))
         self.s = None
 
     def __del__(self):
@@ -418,8 +426,30 @@ class Engine:
     def set_stream(self, stream_ptr: Optional[int]) -> None:
         _check(self.lib.bsp_set_stream(self.h, stream_ptr))
 
+    def stream_ptr(self) -> int:
+        return int(self.lib.bsp_get_stream(self.h) or 0)
+
+    def wait_for(self, other: "Engine") -> None:
+        """This engine's stream waits for the work enqueued on `other`'s."""
+        _check(self.lib.bsp_stream_wait(self.h, other.h))
+
     def synchronize(self) -> None:
         _check(self.lib.bsp_synchronize(self.h))
+
+    def profile(self, on: bool = True) -> None:
+        _check(self.lib.bsp_profile(self.h, 1 if on else 0))
+
+    def profile_report(self) -> dict:
+        """{kernel name: (launches, total ms)} since the last report."""
+        buf = C.create_string_buffer(1 << 16)
+        n = self.lib.bsp_profile_report(self.h, buf, 1 << 16)
+        if n < 0:
+            raise BspError(self.lib.bsp_last_error().decode())
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split("\t")
+            out[name] = (int(cnt), float(ms))
+        return out
 
     def kernel_launches(self) -> int:
         return int(self.lib.bsp_kernel_launches(self.h))

@@ -71,6 +71,8 @@ SIGNATURES = {
     "bsp_destroy": (C.c_int, [vp]),
     "bsp_set_stream": (C.c_int, [vp, vp]),
     "bsp_get_stream": (vp, [vp]),
+    "bsp_profile": (C.c_int, [vp, C.c_int]),
+    "bsp_profile_report": (i64, [vp, C.c_char_p, i64]),
     "bsp_synchronize": (C.c_int, [vp]),
     "bsp_kernel_launches": (i64, [vp]),
     "bsp_get_exec_stats": (C.c_int, [vp, P(bsp_exec_stats)]),
@@ -78,6 +80,8 @@ SIGNATURES = {
     "bsp_csr_upload_rp32": (C.c_int, [vp, i64, i64, vp, vp, vp, P(bsp_csr)]),
     "bsp_csr_view": (C.c_int, [i64, i64, i64, vp, vp, vp, P(bsp_csr)]),
     "bsp_csr_download": (C.c_int, [vp, P(bsp_csr), vp, vp, vp]),
+    "bsp_csr_download_async": (C.c_int, [vp, P(bsp_csr), vp, vp, vp]),
+    "bsp_stream_wait": (C.c_int, [vp, vp]),
     "bsp_csr_free": (C.c_int, [vp, P(bsp_csr)]),
     "bsp_host_alloc": (C.c_int, [C.c_size_t, P(vp)]),
     "bsp_host_free": (C.c_int, [vp]),

@@ -360,8 +360,10 @@ void launch_cluster(bsp_handle h, const ClusterMats& m, const int32_t* ids, int6
     if (n <= 0) return;
     using S = ClusterShared<T, I, NUMERIC>;
     auto k = cluster_tile_kernel<T, I, NUMERIC>;
+    static const std::string nm = std::string(NUMERIC ? "cluster_numeric<" : "cluster_symbolic<") +
+                                  std::to_string(T) + "x" + std::to_string(I) + ">";
     set_smem(k, sizeof(S));
-    BSP_LAUNCH(h, k, static_cast<unsigned>(n), T, sizeof(S), m, ids, cbits, row_nnz, crp, ocol,
+    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, cbits, row_nnz, crp, ocol,
                oval);
 }
 

@@ -5,7 +5,9 @@
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 namespace bsp {
 
@@ -25,12 +27,39 @@ void trace_launch(bsp_handle h, const char* name, long long grid) {
     std::fflush(stderr);
 }
 
+static cudaEvent_t prof_event(bsp_handle h) {
+    if (!h->prof_pool.empty()) {
+        cudaEvent_t e = h->prof_pool.back();
+        h->prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    BSP_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+int prof_begin(bsp_handle h) {
+    if (!h->prof) return -1;
+    bsp_prof_rec r{nullptr, prof_event(h), prof_event(h)};
+    BSP_CUDA(cudaEventRecord(r.a, h->stream));
+    h->prof_recs.push_back(r);
+    return static_cast<int>(h->prof_recs.size()) - 1;
+}
+
+void prof_end(bsp_handle h, int slot, const char* name) {
+    if (slot < 0) return;
+    h->prof_recs[slot].name = name;
+    BSP_CUDA(cudaEventRecord(h->prof_recs[slot].b, h->stream));
+}
+
 void exclusive_scan_i64(bsp_handle h, const int64_t* in, int64_t* out, int64_t n) {
     if (n <= 0) return;
     size_t tmp = 0;
     BSP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, h->stream));
     DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+    const int slot = prof_begin(h);
     BSP_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, in, out, n, h->stream));
+    prof_end(h, slot, "cub_scan_i64");
     ++h->launches;
     ++h->stats.kernels_launched;
 }
@@ -41,8 +70,10 @@ void exclusive_scan_i32_to_i64(bsp_handle h, const int32_t* in, int64_t* out, in
     BSP_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp, in, out, cub::Sum(), int64_t{0}, n,
                                             h->stream));
     DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+    const int slot = prof_begin(h);
     BSP_CUDA(cub::DeviceScan::ExclusiveScan(t.p, tmp, in, out, cub::Sum(), int64_t{0}, n,
                                             h->stream));
+    prof_end(h, slot, "cub_scan_i32");
     ++h->launches;
     ++h->stats.kernels_launched;
 }
@@ -171,13 +202,53 @@ int bsp_set_stream(bsp_handle h, void* s) {
             BSP_CUDA(cudaStreamDestroy(h->stream));
             h->own_stream = false;
         }
-        if (s == nullptr) {
-            BSP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-            h->own_stream = true;
-        } else {
-            h->stream = static_cast<cudaStream_t>(s);
+        // NULL is the legacy default stream (torch's default stream).
+        h->stream = static_cast<cudaStream_t>(s);
+    });
+}
+
+int bsp_profile(bsp_handle h, int on) {
+    return guarded([&] {
+        require(h != nullptr, "bsp_profile: null handle");
+        h->prof = on != 0;
+    });
+}
+
+int64_t bsp_profile_report(bsp_handle h, char* buf, int64_t cap) {
+    std::string out;
+    const int rc = guarded([&] {
+        require(h != nullptr, "bsp_profile_report: null handle");
+        BSP_CUDA(cudaStreamSynchronize(h->stream));
+        std::vector<std::pair<std::string, std::pair<int, double>>> acc;
+        for (auto& r : h->prof_recs) {
+            float ms = 0.f;
+            BSP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            const std::string nm = r.name ? r.name : "?";
+            auto it = std::find_if(acc.begin(), acc.end(), [&](auto& x) { return x.first == nm; });
+            if (it == acc.end()) {
+                acc.push_back({nm, {1, ms}});
+            } else {
+                it->second.first += 1;
+                it->second.second += ms;
+            }
+            h->prof_pool.push_back(r.a);
+            h->prof_pool.push_back(r.b);
+        }
+        h->prof_recs.clear();
+        char line[256];
+        for (auto& x : acc) {
+            std::snprintf(line, sizeof line, "%s\t%d\t%.6f\n", x.first.c_str(), x.second.first,
+                          x.second.second);
+            out += line;
         }
     });
+    if (rc != BSP_OK) return -1;
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(out.size()));
+        std::memcpy(buf, out.data(), n);
+        buf[n] = 0;
+    }
+    return static_cast<int64_t>(out.size());
 }
 
 void* bsp_get_stream(bsp_handle h) { return h ? static_cast<void*>(h->stream) : nullptr; }
@@ -259,6 +330,27 @@ int bsp_csr_download(bsp_handle h, const bsp_csr* m, int64_t* row_ptr, int32_t* 
         if (col_idx) d2h(h, col_idx, m->col_idx, m->nnz);
         if (values) d2h(h, values, m->values, m->nnz);
         sync(h);
+    });
+}
+
+int bsp_csr_download_async(bsp_handle h, const bsp_csr* m, int64_t* row_ptr, int32_t* col_idx,
+                           double* values) {
+    return guarded([&] {
+        check_csr(m, "bsp_csr_download_async");
+        if (row_ptr) d2h(h, row_ptr, m->row_ptr, m->nrows + 1);
+        if (col_idx) d2h(h, col_idx, m->col_idx, m->nnz);
+        if (values) d2h(h, values, m->values, m->nnz);
+    });
+}
+
+int bsp_stream_wait(bsp_handle waiter, bsp_handle signaler) {
+    return guarded([&] {
+        require(waiter && signaler, "bsp_stream_wait: null handle");
+        cudaEvent_t e;
+        BSP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        BSP_CUDA(cudaEventRecord(e, signaler->stream));
+        BSP_CUDA(cudaStreamWaitEvent(waiter->stream, e, 0));
+        BSP_CUDA(cudaEventDestroy(e));
     });
 }
 

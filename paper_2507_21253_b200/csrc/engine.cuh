@@ -13,6 +13,11 @@
 #error "This engine is written for sm_100a (B200) only."
 #endif
 
+struct bsp_prof_rec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+
 struct bsp_handle_s {
     int device = 0;
     int sm_count = 148;
@@ -20,6 +25,9 @@ struct bsp_handle_s {
     bool own_stream = false;
     int64_t launches = 0;
     bsp_exec_stats stats{};
+    bool prof = false;
+    std::vector<bsp_prof_rec> prof_recs;  // recorded launches (events owned)
+    std::vector<cudaEvent_t> prof_pool;   // recycled events
 };
 
 namespace bsp {
@@ -36,20 +44,27 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 // Every engine kernel launch goes through this so the handle can report how
 // many of OUR kernels ran (bench.py's gpu_launches).
-#define BSP_LAUNCH(h, kernel, grid, block, smem, ...)                                  \
+#define BSP_LAUNCH_AS(h, name, kernel, grid, block, smem, ...)                         \
     do {                                                                               \
         if ((grid) > 0) {                                                              \
+            const int prof_slot_ = ::bsp::prof_begin(h);                               \
             kernel<<<(grid), (block), (smem), (h)->stream>>>(__VA_ARGS__);             \
-            ::bsp::cuda_check(cudaGetLastError(), #kernel);                            \
+            ::bsp::cuda_check(cudaGetLastError(), name);                               \
+            ::bsp::prof_end((h), prof_slot_, name);                                    \
             ++(h)->launches;                                                           \
             ++(h)->stats.kernels_launched;                                             \
-            if (::bsp::trace_enabled()) ::bsp::trace_launch((h), #kernel, (grid));     \
+            if (::bsp::trace_enabled()) ::bsp::trace_launch((h), name, (grid));        \
         }                                                                              \
     } while (0)
+#define BSP_LAUNCH(h, kernel, grid, block, smem, ...) \
+    BSP_LAUNCH_AS(h, #kernel, kernel, grid, block, smem, __VA_ARGS__)
 
 // BSP_TRACE=1: synchronise and log every engine launch (debugging only).
 bool trace_enabled();
 void trace_launch(bsp_handle h, const char* name, long long grid);
+// Per-launch CUDA-event profiling (bsp_profile): -1 when disabled.
+int prof_begin(bsp_handle h);
+void prof_end(bsp_handle h, int slot, const char* name);
 
 // Stream-ordered device allocation from the device's default memory pool
 // (release threshold raised at handle creation so repeated calls reuse it).

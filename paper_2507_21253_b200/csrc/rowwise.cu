@@ -25,6 +25,7 @@
 //  Symbolic runs K3/K4 without values to get exact per-row counts (exact
 //  allocation as the reference), then an int64 scan gives row_ptr.
 #include "esc.cuh"
+#include "merge.cuh"
 
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
@@ -358,6 +359,164 @@ __global__ void __launch_bounds__(T) esc_tile_kernel(Mats m, const int32_t* __re
     }
 }
 
+// K3': merge-based exact numeric tile and hash-count symbolic tile
+// ---------------------------------------------------------------------------
+template <int T, int CAPM>
+__global__ void __launch_bounds__(T) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
+                                                      const Window* __restrict__ wins, OutCtx out) {
+    using S = MergeShared<T, CAPM>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S& s = *reinterpret_cast<S*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int32_t id = ids[blockIdx.x];
+    int32_t row, c0, c1, w = -1;
+    if (wins) {
+        w = id;
+        const Window wd = wins[w];
+        row = wd.row;
+        c0 = wd.c0;
+        c1 = wd.c1;
+    } else {
+        row = id;
+        c0 = 0;
+        c1 = m.ncols;
+    }
+    const int total = expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s);
+    const int b = merge_runs<T, CAPM>(s, total);
+    const uint32_t* K = s.key[b];
+    const uint16_t* X = s.idx[b];
+    // runs of equal columns: head = first position; ordered sums (k order)
+    constexpr int E_MAX = (CAPM + T - 1) / T;
+    const int E = (total + T - 1) / T;
+    const int o0 = min(total, tid * E), o1 = min(total, o0 + E);
+    int nh = 0;
+    for (int o = o0; o < o1; ++o) nh += (o == 0 || K[o] != K[o - 1]);
+    int hoff, tile_cnt;
+    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
+    double res[E_MAX];
+    uint32_t rk[E_MAX];
+    int r = 0;
+#pragma unroll
+    for (int q = 0; q < E_MAX; ++q) {
+        const int o = o0 + q;
+        if (o < o1 && (o == 0 || K[o] != K[o - 1])) {
+            const uint32_t key = K[o];
+            double acc = 0.0;
+            int e = o;
+            do {
+                acc = __dadd_rn(acc, s.val[X[e]]);
+                ++e;
+            } while (e < total && K[e] == key);
+            res[r] = acc;
+            rk[r] = key;
+            ++r;
+        }
+    }
+    __syncthreads();
+    // stage compacted output in key[b^1] / val (both free now)
+    uint32_t* KO = s.key[b ^ 1];
+#pragma unroll
+    for (int q = 0; q < E_MAX; ++q) {
+        if (q < r) {
+            KO[hoff + q] = rk[q] + static_cast<uint32_t>(c0);
+            s.val[hoff + q] = res[q];
+        }
+    }
+    __syncthreads();
+    int64_t base = out.crp[row - out.row_begin];
+    if (w >= 0) base += out.win_scan[w] - out.win_scan[wins[w].first];
+    for (int e = tid; e < tile_cnt; e += T) {
+        out.ccol[base + e] = static_cast<int32_t>(KO[e]);
+        out.cval[base + e] = s.val[e];
+    }
+}
+
+template <int T, int CAPM>
+struct HashShared {
+    int32_t table[2 * CAPM];
+    typename cub::BlockReduce<int32_t, T>::TempStorage red;
+    int64_t pstart[T];
+    int32_t plen[T];
+};
+
+// Distinct output columns of (row, [c0,c1)) with <= CAPM products.
+template <int T, int CAPM>
+__global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __restrict__ ids,
+                                                       const Window* __restrict__ wins,
+                                                       OutCtx out) {
+    using S = HashShared<T, CAPM>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S& s = *reinterpret_cast<S*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = T / 32;
+    constexpr int LG = 1 + 31 - __builtin_clz(static_cast<unsigned>(CAPM));  // 2*CAPM slots
+    const int32_t id = ids[blockIdx.x];
+    int32_t row, c0, c1, w = -1;
+    if (wins) {
+        w = id;
+        const Window wd = wins[w];
+        row = wd.row;
+        c0 = wd.c0;
+        c1 = wd.c1;
+    } else {
+        row = id;
+        c0 = 0;
+        c1 = m.ncols;
+    }
+    const bool full = wins == nullptr;
+    for (int e = tid; e < 2 * CAPM; e += T) s.table[e] = -1;
+    const int64_t rs = m.arp[row], re = m.arp[row + 1];
+    int cnt = 0;
+    for (int64_t pc = rs; pc < re; pc += T) {
+        const int64_t p = pc + tid;
+        int len = 0;
+        int64_t start = 0;
+        if (p < re) {
+            const int32_t k = __ldg(m.acol + p);
+            int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
+            if (!full) {
+                b0 = lower_bound_col(m.bcol, b0, b1, c0);
+                b1 = lower_bound_col(m.bcol, b0, b1, c1);
+            }
+            start = b0;
+            len = static_cast<int>(b1 - b0);
+        }
+        __syncthreads();
+        s.pstart[tid] = start;
+        s.plen[tid] = len;
+        __syncthreads();
+        const int nslots = static_cast<int>(::min(int64_t{T}, re - pc));
+        for (int slot = warp; slot < nslots; slot += NW) {
+            const int l = s.plen[slot];
+            const int64_t st = s.pstart[slot];
+            for (int q = lane; q < l; q += 32) {
+                const int32_t col = __ldg(m.bcol + st + q);
+                uint32_t hsl = col_hash(static_cast<uint32_t>(col), LG);
+                for (;;) {
+                    const int32_t prev = atomicCAS(&s.table[hsl], -1, col);
+                    if (prev == -1) {
+                        ++cnt;
+                        break;
+                    }
+                    if (prev == col) break;
+                    hsl = (hsl + 1) & (2 * CAPM - 1);
+                }
+            }
+        }
+    }
+    const int tot = cub::BlockReduce<int32_t, T>(s.red).Sum(cnt);
+    if (tid == 0) {
+        if (w >= 0) {
+            out.win_nnz[w] = tot;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&out.row_nnz[row - out.row_begin]),
+                      static_cast<unsigned long long>(tot));
+        } else {
+            out.row_nnz[row - out.row_begin] = tot;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
 // K4: dense window kernel (heavy windows, width <= WD, any product count)
 // ---------------------------------------------------------------------------
@@ -523,18 +682,41 @@ void launch_esc(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, cons
     if (n <= 0) return;
     using S = EscShared<T, I, NUMERIC>;
     auto k = esc_tile_kernel<T, I, NUMERIC>;
+    static const std::string nm = std::string(NUMERIC ? "esc_numeric<" : "esc_symbolic<") +
+                                  std::to_string(T) + "x" + std::to_string(I) + ">";
     set_smem(k, sizeof(S));
-    BSP_LAUNCH(h, k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
+    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
+}
+
+template <int T, int CAPM, bool NUMERIC>
+void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, const Window* wins,
+                 const OutCtx& out) {
+    if (n <= 0) return;
+    if (NUMERIC) {
+        using S = MergeShared<T, CAPM>;
+        auto k = esc_merge_kernel<T, CAPM>;
+        static const std::string nm = "esc_merge<" + std::to_string(T) + "," +
+                                      std::to_string(CAPM) + (wins ? ",win>" : ">");
+        set_smem(k, sizeof(S));
+        BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
+    } else {
+        using S = HashShared<T, CAPM>;
+        auto k = hash_count_kernel<T, CAPM>;
+        static const std::string nm = "hash_count<" + std::to_string(T) + "," +
+                                      std::to_string(CAPM) + (wins ? ",win>" : ">");
+        set_smem(k, sizeof(S));
+        BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
+    }
 }
 
 template <bool NUMERIC>
 void launch_light(bsp_handle h, int cls, const Mats& m, const int32_t* ids, int64_t n,
                   const OutCtx& out) {
     switch (cls) {
-        case 1: launch_esc<32, 4, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 2: launch_esc<64, 8, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 3: launch_esc<128, 16, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 4: launch_esc<256, 16, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 1: launch_tile<32, 128, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 2: launch_tile<64, 512, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 3: launch_tile<128, 2048, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 4: launch_tile<256, 4096, NUMERIC>(h, m, ids, n, nullptr, out); break;
         default: break;
     }
 }
@@ -545,7 +727,8 @@ void launch_dense(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, co
     if (n <= 0) return;
     auto k = dense_window_kernel<NUMERIC>;
     set_smem(k, sizeof(DenseShared));
-    BSP_LAUNCH(h, k, static_cast<unsigned>(n), DT, sizeof(DenseShared), m, ids, wins, out);
+    BSP_LAUNCH_AS(h, NUMERIC ? "dense_window_numeric" : "dense_window_symbolic", k,
+                  static_cast<unsigned>(n), DT, sizeof(DenseShared), m, ids, wins, out);
 }
 
 }  // namespace
@@ -634,7 +817,7 @@ template <bool NUMERIC>
 void run_plan(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx& out) {
     for (int c = 1; c < NCLS - 1; ++c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
-    launch_esc<256, 16, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse, plan.wins.p, out);
+    launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse, plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
 

@@ -256,8 +256,9 @@ void launch_topk(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, con
     if (n <= 0) return;
     using S = EscShared<T, I, true>;
     auto k = topk_tile_kernel<T, I>;
+    static const std::string nm = "topk_tile<" + std::to_string(T) + "x" + std::to_string(I) + ">";
     set_smem(k, sizeof(S));
-    BSP_LAUNCH(h, k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, topk, th, rj, rs, rn,
+    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, topk, th, rj, rs, rn,
                wj, ws, wn);
 }
 
