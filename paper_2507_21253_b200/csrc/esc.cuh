@@ -11,6 +11,11 @@ namespace bsp {
 
 constexpr int CAP = 4096;     // max products of one sparse tile (smem ESC)
 constexpr int CAPH = CAP / 2;
+// Window packing: bins with > CAPB products get their own window; runs of
+// smaller bins are cut where floor(prefix / CAPG) changes, so a window holds
+// < CAPG + CAPB = CAP products and averages ~CAPG.
+constexpr int CAPB = CAP / 4;
+constexpr int CAPG = CAP - CAPB;
 constexpr int WD = 4096;      // dense window width in columns
 constexpr int LOG_WD = 12;
 constexpr int MAXBINS = 4096; // planner histogram bins per heavy row
@@ -26,12 +31,16 @@ struct Mats {
     const int32_t* __restrict__ bcol;
     const double* __restrict__ bval;
     int32_t ncols;  // columns of B (= of C)
+    const int32_t* __restrict__ starts = nullptr;  // planner start tables (windows)
 };
 
 struct Window {
     int32_t row;    // absolute A row
     int32_t c0, c1; // column range [c0, c1)
     int32_t first;  // index of the row's first window
+    int32_t wi;     // index of this window within its row
+    int32_t pad_;
+    int64_t sofs;   // offset of the row's per-(window, segment) start table, or -1
 };
 
 struct OutCtx {
@@ -54,6 +63,23 @@ __device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ c
             hi = mid;
     }
     return lo;
+}
+
+// Segment [b0, b1) of B row k restricted to a window: from the planner's
+// start table when the row has one (no search), else by binary search.
+// b0/b1 hold the full segment on entry.
+__device__ __forceinline__ void window_bounds(const Mats& m, int64_t sofs, int wi, int64_t pl,
+                                              int64_t d, int32_t c0, int32_t c1, int64_t& b0,
+                                              int64_t& b1) {
+    if (sofs >= 0) {
+        const int32_t* st = m.starts + sofs;
+        const int64_t base = b0;
+        b1 = base + __ldg(st + int64_t{wi + 1} * d + pl);
+        b0 = base + __ldg(st + int64_t{wi} * d + pl);
+    } else {
+        b0 = lower_bound_col(m.bcol, b0, b1, c0);
+        b1 = lower_bound_col(m.bcol, b0, b1, c1);
+    }
 }
 
 __host__ __device__ __forceinline__ int bit_length(uint32_t x) {
@@ -90,7 +116,8 @@ struct EscShared {
 // Returns the product count.
 template <int T, int I, bool NUMERIC, typename S>
 __device__ __forceinline__ int expand_products(const Mats& m, int32_t row, int32_t c0, int32_t c1,
-                                               bool full, S& s) {
+                                               bool full, S& s, int64_t wsofs = -1,
+                                               int wwi = 0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = T / 32;
     const int64_t rs = m.arp[row], re = m.arp[row + 1];
@@ -103,10 +130,7 @@ __device__ __forceinline__ int expand_products(const Mats& m, int32_t row, int32
         if (p < re) {
             const int32_t k = __ldg(m.acol + p);
             int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            if (!full) {
-                b0 = lower_bound_col(m.bcol, b0, b1, c0);
-                b1 = lower_bound_col(m.bcol, b0, b1, c1);
-            }
+            if (!full) window_bounds(m, wsofs, wwi, p - rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
             if (NUMERIC) av = __ldg(m.aval + p);
@@ -146,6 +170,15 @@ struct RowwisePlan {
     int64_t nwin = 0, nsparse = 0, ndense = 0;
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
+    int64_t nhcur = 0;    // heavy rows walked by one CTA with cursors
+    DBuf<int32_t> hcur;   // ... sorted by products, descending
+    DBuf<int32_t> starts; // planner per-(window, segment) start tables
+    // Matrices as seen by the window kernels (start tables attached).
+    Mats with_starts(const Mats& m) const {
+        Mats r = m;
+        r.starts = starts.p;
+        return r;
+    }
 };
 
 Mats make_mats(const bsp_csr* A, const bsp_csr* B);

@@ -15,18 +15,39 @@
 
 #include "esc.cuh"
 
+#include <cub/block/block_radix_sort.cuh>
+
 namespace bsp {
+
+// Padded shared-memory index: one pad word per 32 keeps the per-thread
+// contiguous chunks of the merge (thread t owns [t*E, t*E+E)) on distinct
+// banks (ncu: 42% of shared wavefronts were bank conflicts without it).
+__device__ __forceinline__ int PADI(int i) { return i + (i >> 5); }
 
 template <int T, int CAPM>
 struct MergeShared {
-    uint32_t key[2][CAPM];
-    uint16_t idx[2][CAPM];
+    static constexpr int NP = CAPM + CAPM / 32 + 1;
+    using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, 6>;
+    // buffer 0 (also the radix-sort input/output)
+    uint32_t key0[NP];
+    uint16_t idx0[NP];
+    uint16_t ro0[CAPM + 2];  // run offsets (runs <= products <= CAPM)
     double val[CAPM];
-    uint16_t ro[2][CAPM + 2];  // run offsets (runs <= products <= CAPM)
+    // buffer 1 of the merge, aliased with the radix sort's temp storage
+    union U {
+        struct B1 {
+            uint32_t key1[NP];
+            uint16_t idx1[NP];
+            uint16_t ro1[CAPM + 2];
+        } m;
+        typename RSort::TempStorage sort;
+    } u;
+    __device__ __forceinline__ uint32_t* key(int b) { return b ? u.m.key1 : key0; }
+    __device__ __forceinline__ uint16_t* idx(int b) { return b ? u.m.idx1 : idx0; }
+    __device__ __forceinline__ uint16_t* ro(int b) { return b ? u.m.ro1 : ro0; }
     typename cub::BlockScan<int32_t, T>::TempStorage scan;
     int64_t pstart[T];
-    int32_t plen[T];
-    int32_t poff[T];
+    int32_t poff[T + 1];
     double pav[T];
     int nruns;
 };
@@ -35,7 +56,8 @@ struct MergeShared {
 // B-row segment becomes one sorted run.  Returns the product count.
 template <int T, int CAPM, bool VALUES>
 __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c0, int32_t c1,
-                                           bool full, MergeShared<T, CAPM>& s) {
+                                           bool full, MergeShared<T, CAPM>& s,
+                                           int64_t wsofs = -1, int wwi = 0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = T / 32;
     const int64_t rs = m.arp[row], re = m.arp[row + 1];
@@ -48,10 +70,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         if (p < re) {
             const int32_t k = __ldg(m.acol + p);
             int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            if (!full) {
-                b0 = lower_bound_col(m.bcol, b0, b1, c0);
-                b1 = lower_bound_col(m.bcol, b0, b1, c1);
-            }
+            if (!full) window_bounds(m, wsofs, wwi, p - rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
             if (VALUES) av = __ldg(m.aval + p);
@@ -60,32 +79,48 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         const int packed = len | ((len > 0) << 16);
         int off, agg;
         cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
-        const int o = total + (off & 0xffff);
-        if (len > 0) s.ro[0][nruns + (off >> 16)] = static_cast<uint16_t>(o);
-        s.pstart[tid] = start;
-        s.plen[tid] = len;
-        s.poff[tid] = o;
-        if (VALUES) s.pav[tid] = av;
+        // compact the non-empty segments of this chunk (run order = k order)
+        const int r = off >> 16;
+        if (len > 0) {
+            s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
+            s.pstart[r] = start;
+            s.poff[r] = off & 0xffff;
+            if (VALUES) s.pav[r] = av;
+        }
+        const int nr = agg >> 16, ct = agg & 0xffff;
+        if (tid == 0) s.poff[nr] = ct;
         __syncthreads();
-        const int nslots = static_cast<int>(::min(int64_t{T}, re - pc));
-        for (int slot = warp; slot < nslots; slot += NW) {
-            const int l = s.plen[slot];
-            const int64_t st = s.pstart[slot];
-            const int ob = s.poff[slot];
-            double a = 0.0;
-            if (VALUES) a = s.pav[slot];
-            for (int q = lane; q < l; q += 32) {
-                s.key[0][ob + q] = static_cast<uint32_t>(__ldg(m.bcol + st + q) - c0);
-                s.idx[0][ob + q] = static_cast<uint16_t>(ob + q);
-                if (VALUES) s.val[ob + q] = __dmul_rn(a, __ldg(m.bval + st + q));
+        // each thread copies a contiguous range of the chunk's products
+        const int E = (ct + T - 1) / T;
+        int e = min(ct, tid * E);
+        const int ee = min(ct, e + E);
+        if (e < ee) {
+            int lo = 0, hi = nr - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s.poff[mid] <= e) lo = mid; else hi = mid - 1;
+            }
+            int q = lo;
+            while (e < ee) {
+                while (s.poff[q + 1] <= e) ++q;
+                const int stop = min(ee, s.poff[q + 1]);
+                const int64_t base = s.pstart[q] - s.poff[q];
+                double a = 0.0;
+                if (VALUES) a = s.pav[q];
+                for (; e < stop; ++e) {
+                    const int g = total + e;
+                    s.key(0)[PADI(g)] = static_cast<uint32_t>(__ldg(m.bcol + base + e) - c0);
+                    s.idx(0)[PADI(g)] = static_cast<uint16_t>(g);
+                    if (VALUES) s.val[g] = __dmul_rn(a, __ldg(m.bval + base + e));
+                }
             }
         }
-        total += agg & 0xffff;
-        nruns += agg >> 16;
+        total += ct;
+        nruns += nr;
         __syncthreads();
     }
     if (tid == 0) {
-        s.ro[0][nruns] = static_cast<uint16_t>(total);
+        s.ro(0)[nruns] = static_cast<uint16_t>(total);
         s.nruns = nruns;
     }
     __syncthreads();
@@ -102,14 +137,14 @@ __device__ __forceinline__ int merge_runs(MergeShared<T, CAPM>& s, int total) {
     const int E = (total + T - 1) / T;
     while (R > 1) {
         const int Rn = (R + 1) >> 1;
-        const uint16_t* ro = s.ro[b];
-        uint16_t* rn = s.ro[b ^ 1];
+        const uint16_t* ro = s.ro(b);
+        uint16_t* rn = s.ro(b ^ 1);
         for (int i = tid; i <= Rn; i += T) rn[i] = (i < Rn) ? ro[2 * i] : static_cast<uint16_t>(total);
         __syncthreads();
-        const uint32_t* K = s.key[b];
-        const uint16_t* X = s.idx[b];
-        uint32_t* KO = s.key[b ^ 1];
-        uint16_t* XO = s.idx[b ^ 1];
+        const uint32_t* K = s.key(b);
+        const uint16_t* X = s.idx(b);
+        uint32_t* KO = s.key(b ^ 1);
+        uint16_t* XO = s.idx(b ^ 1);
         int o = min(total, tid * E);
         const int oe = min(total, o + E);
         while (o < oe) {
@@ -128,23 +163,23 @@ __device__ __forceinline__ int merge_runs(MergeShared<T, CAPM>& s, int total) {
             int a = max(0, k - (ye - xe)), a_hi = min(k, xe - xs);
             while (a < a_hi) {
                 const int mid = (a + a_hi) >> 1;
-                if (K[xs + mid] <= K[xe + k - 1 - mid]) a = mid + 1; else a_hi = mid;
+                if (K[PADI(xs + mid)] <= K[PADI(xe + k - 1 - mid)]) a = mid + 1; else a_hi = mid;
             }
             int xi = xs + a, yi = xe + (k - a);
-            uint32_t kx = xi < xe ? K[xi] : 0xffffffffu;
-            uint32_t ky = yi < ye ? K[yi] : 0xffffffffu;
+            uint32_t kx = xi < xe ? K[PADI(xi)] : 0xffffffffu;
+            uint32_t ky = yi < ye ? K[PADI(yi)] : 0xffffffffu;
             for (int t = k; t < kend; ++t) {
                 const bool takex = (yi >= ye) || (xi < xe && kx <= ky);
                 if (takex) {
-                    KO[xs + t] = kx;
-                    XO[xs + t] = X[xi];
+                    KO[PADI(xs + t)] = kx;
+                    XO[PADI(xs + t)] = X[PADI(xi)];
                     ++xi;
-                    kx = xi < xe ? K[xi] : 0xffffffffu;
+                    kx = xi < xe ? K[PADI(xi)] : 0xffffffffu;
                 } else {
-                    KO[xs + t] = ky;
-                    XO[xs + t] = X[yi];
+                    KO[PADI(xs + t)] = ky;
+                    XO[PADI(xs + t)] = X[PADI(yi)];
                     ++yi;
-                    ky = yi < ye ? K[yi] : 0xffffffffu;
+                    ky = yi < ye ? K[PADI(yi)] : 0xffffffffu;
                 }
             }
             o = xs + kend;
@@ -154,6 +189,107 @@ __device__ __forceinline__ int merge_runs(MergeShared<T, CAPM>& s, int total) {
         R = Rn;
     }
     return b;
+}
+
+// Stable block radix sort of the expanded tile by column (CUB, 6-bit digits);
+// chosen instead of merge_runs when the merge tree would need more levels
+// than the radix sort needs passes (windows of heavy rows carry hundreds of
+// short runs).  Result left in buffer 0.
+template <int T, int CAPM>
+__device__ __forceinline__ void radix_sort_tile(MergeShared<T, CAPM>& s, int total, int bits) {
+    constexpr int I = CAPM / T;
+    const int tid = threadIdx.x;
+    uint32_t k[I];
+    uint16_t v[I];
+    const uint32_t pad = (bits >= 32) ? 0xffffffffu : ((1u << bits) - 1u);
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = tid * I + i;
+        k[i] = e < total ? s.key0[PADI(e)] : pad;
+        v[i] = e < total ? s.idx0[PADI(e)] : static_cast<uint16_t>(0);
+    }
+    __syncthreads();
+    typename MergeShared<T, CAPM>::RSort(s.u.sort).Sort(k, v, 0, bits);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        s.key0[PADI(tid * I + i)] = k[i];
+        s.idx0[PADI(tid * I + i)] = v[i];
+    }
+    __syncthreads();
+}
+
+// Sort the expanded tile: merge of presorted runs, or radix when cheaper.
+template <int T, int CAPM>
+__device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width) {
+    const int R = s.nruns;
+    const int levels = R > 1 ? 32 - __clz(R - 1) : 0;
+    // pad key = 2^bits - 1 must exceed every key (< width)
+    const int bits = bit_length(width);
+    const int passes = (bits + 5) / 6;
+    if (levels > passes + 1) {  // measured: cfg4 (5 levels vs 4 passes) prefers merge
+        radix_sort_tile<T, CAPM>(s, total, bits);
+        return 0;
+    }
+    return merge_runs<T, CAPM>(s, total);
+}
+
+// After merge_runs: sum every run of equal columns left to right from 0.0
+// (ascending k), stage (column + kofs, sum) compactly in smem and write them
+// coalesced to ccol/cval.  Returns the number of distinct columns.
+template <int T, int CAPM>
+__device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, int total,
+                                                uint32_t kofs, int32_t* __restrict__ ccol,
+                                                double* __restrict__ cval) {
+    const int tid = threadIdx.x;
+    const uint32_t* K = s.key(b);
+    const uint16_t* X = s.idx(b);
+    constexpr int E_MAX = (CAPM + T - 1) / T;
+    const int E = (total + T - 1) / T;
+    const int o0 = min(total, tid * E), o1 = min(total, o0 + E);
+    int nh = 0;
+    for (int o = o0; o < o1; ++o) nh += (o == 0 || K[PADI(o)] != K[PADI(o - 1)]);
+    int hoff, tile_cnt;
+    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
+    double res[E_MAX];
+    bool hd[E_MAX];
+#pragma unroll
+    for (int q = 0; q < E_MAX; ++q) {
+        const int o = o0 + q;
+        hd[q] = o < o1 && (o == 0 || K[PADI(o)] != K[PADI(o - 1)]);
+        res[q] = 0.0;
+        if (hd[q]) {
+            const uint32_t key = K[PADI(o)];
+            double acc = 0.0;
+            int e = o;
+            do {
+                acc = __dadd_rn(acc, s.val[X[PADI(e)]]);
+                ++e;
+            } while (e < total && K[PADI(e)] == key);
+            res[q] = acc;
+        }
+    }
+    uint32_t kk[E_MAX];
+#pragma unroll
+    for (int q = 0; q < E_MAX; ++q) kk[q] = (o0 + q < o1) ? K[PADI(o0 + q)] : 0u;
+    __syncthreads();
+    uint32_t* KO = s.key(b ^ 1);
+    int r = hoff;
+#pragma unroll
+    for (int q = 0; q < E_MAX; ++q) {
+        if (hd[q]) {
+            KO[PADI(r)] = kk[q] + kofs;
+            s.val[r] = res[q];
+            ++r;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < tile_cnt; e += T) {
+        ccol[e] = static_cast<int32_t>(KO[PADI(e)]);
+        cval[e] = s.val[e];
+    }
+    __syncthreads();
+    return tile_cnt;
 }
 
 // Fibonacci hash of a column into a table of 2^lg slots.

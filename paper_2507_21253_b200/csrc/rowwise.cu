@@ -25,9 +25,11 @@
 //  Symbolic runs K3/K4 without values to get exact per-row counts (exact
 //  allocation as the reference), then an int64 scan gives row_ptr.
 #include "esc.cuh"
+#include "heavy.cuh"
 #include "merge.cuh"
 
 #include <cub/block/block_radix_sort.cuh>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -149,7 +151,9 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __r
                                                       int32_t* __restrict__ nwin,
                                                       const int64_t* __restrict__ win_off,
                                                       Window* __restrict__ wins,
-                                                      uint8_t* __restrict__ win_dense) {
+                                                      uint8_t* __restrict__ win_dense,
+                                                      const int64_t* __restrict__ start_off,
+                                                      int32_t* __restrict__ starts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PlanShared& s = *reinterpret_cast<PlanShared*>(smem_raw);
     const int32_t hrow = blockIdx.x;
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __r
         nstart[i] = 0;
         if (b >= nbins) continue;
         const int32_t pre = base + excl[i];
-        const bool big = cnt[i] > CAPH;
+        const bool big = cnt[i] > CAPB;
         if (big) {
             nstart[i] = cnt[i] > CAP ? sub : 1;
         } else {
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __r
             if (!start) {
                 const int32_t pc = s.hist[b - 1];
                 const int32_t ppre = pre - pc;
-                start = (pc > CAPH) || (ppre / CAPH != pre / CAPH);
+                start = (pc > CAPB) || (ppre / CAPG != pre / CAPG);
             }
             nstart[i] = start ? 1 : 0;
         }
@@ -222,8 +226,19 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __r
             }
         }
     }
+    // bin -> window (sub == 1: every bin lies in exactly one window)
+    {
+        int32_t run = wbase;
+        for (int i = 0; i < ITEMS; ++i) {
+            const int b = threadIdx.x * ITEMS + i;
+            run += nstart[i];
+            if (b < nbins) s.hist[b] = run - 1;  // hist no longer needed
+        }
+    }
     __syncthreads();
     const int64_t off = win_off[hrow];
+    const int64_t sofs = (starts != nullptr && start_off[hrow + 1] > start_off[hrow])
+                             ? start_off[hrow] : -1;
     for (int k = threadIdx.x; k < wtot; k += PLAN_T) {
         Window wd;
         wd.row = row;
@@ -232,8 +247,72 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __r
         if (s.wstart[k]) c1 = ::min(c1, int64_t{wd.c0} + WD);
         wd.c1 = static_cast<int32_t>(::min(c1, int64_t{m.ncols}));
         wd.first = static_cast<int32_t>(off);
+        wd.wi = k;
+        wd.sofs = sofs;
         wins[off + k] = wd;
         win_dense[off + k] = static_cast<uint8_t>(s.wstart[k]);
+    }
+    if (sofs < 0) return;
+    // Per-(window, segment) start offsets: starts[sofs + w*d + p] = number of
+    // elements of segment p lying in windows < w (streamed once per segment).
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t rs = m.arp[row];
+    const int d = static_cast<int>(m.arp[row + 1] - rs);
+    int32_t* st = starts + sofs;
+    for (int p = warp; p < d; p += PLAN_T / 32) {
+        const int32_t k = __ldg(m.acol + rs + p);
+        const int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
+        const int len = static_cast<int>(b1 - b0);
+        int carry = -1;  // window of the previous element
+        for (int q0 = 0; q0 < len; q0 += 32) {
+            const int q = q0 + lane;
+            const int wq = q < len ? s.hist[__ldg(m.bcol + b0 + q) >> log_binw] : wtot;
+            int wp = __shfl_up_sync(0xffffffffu, wq, 1);
+            if (lane == 0) wp = carry;
+            if (q < len)
+                for (int w2 = wp + 1; w2 <= wq; ++w2) st[int64_t{w2} * d + p] = q;
+            carry = __shfl_sync(0xffffffffu, wq, ::min(31, len - 1 - q0));
+        }
+        // windows after the last element start at len
+        const int wl = (len > 0) ? carry : -1;
+        for (int w2 = wl + 1 + lane; w2 <= wtot; w2 += 32) st[int64_t{w2} * d + p] = len;
+    }
+}
+
+// Size of each heavy row's start table ((windows+1) x A-row length), or 0
+// when it would exceed the per-row budget (those rows binary-search).
+__global__ void start_size_kernel(Mats m, const int32_t* __restrict__ heavy, int64_t nh,
+                                  const int32_t* __restrict__ nwin, int64_t per_row_cap,
+                                  int64_t* __restrict__ sz) {
+    const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (t > nh) return;
+    if (t == nh) {
+        sz[t] = 0;
+        return;
+    }
+    const int32_t row = heavy[t];
+    const int64_t d = m.arp[row + 1] - m.arp[row];
+    const int64_t e = (int64_t{nwin[t]} + 1) * d;
+    sz[t] = e <= per_row_cap ? e : 0;
+}
+
+// Split heavy rows: A-row length <= HDMAX -> cursor list (with products as
+// the LPT sort key), else -> mega list (planned windows).
+__global__ void split_heavy_kernel(Mats m, const int32_t* __restrict__ heavy, int64_t nh,
+                                   int64_t rb, const int64_t* __restrict__ prod,
+                                   int64_t* __restrict__ keys, int32_t* __restrict__ vals,
+                                   int32_t* __restrict__ mega,
+                                   unsigned long long* __restrict__ cnt, int64_t dmax) {
+    const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (t >= nh) return;
+    const int32_t row = heavy[t];
+    const int64_t d = m.arp[row + 1] - m.arp[row];
+    if (d <= dmax) {
+        const unsigned long long i = atomicAdd(&cnt[0], 1ull);
+        keys[i] = prod[row - rb];
+        vals[i] = row;
+    } else {
+        mega[atomicAdd(&cnt[1], 1ull)] = row;
     }
 }
 
@@ -268,19 +347,23 @@ __global__ void __launch_bounds__(T) esc_tile_kernel(Mats m, const int32_t* __re
     const int tid = threadIdx.x;
     const int32_t id = ids[blockIdx.x];
     int32_t row, c0, c1, w = -1;
+    int64_t wsofs = -1;
+    int wwi = 0;
     if (wins) {
         w = id;
         const Window wd = wins[w];
         row = wd.row;
         c0 = wd.c0;
         c1 = wd.c1;
+        wsofs = wd.sofs;
+        wwi = wd.wi;
     } else {
         row = id;
         c0 = 0;
         c1 = m.ncols;
     }
     const bool full = (wins == nullptr);
-    const int total = expand_products<T, I, NUMERIC>(m, row, c0, c1, full, s);
+    const int total = expand_products<T, I, NUMERIC>(m, row, c0, c1, full, s, wsofs, wwi);
 
     // Stable LSD radix sort of (column, position) pairs.
     const uint32_t width = static_cast<uint32_t>(c1 - c0);
@@ -370,73 +453,37 @@ __global__ void __launch_bounds__(T) esc_merge_kernel(Mats m, const int32_t* __r
     const int tid = threadIdx.x;
     const int32_t id = ids[blockIdx.x];
     int32_t row, c0, c1, w = -1;
+    int64_t wsofs = -1;
+    int wwi = 0;
     if (wins) {
         w = id;
         const Window wd = wins[w];
         row = wd.row;
         c0 = wd.c0;
         c1 = wd.c1;
+        wsofs = wd.sofs;
+        wwi = wd.wi;
     } else {
         row = id;
         c0 = 0;
         c1 = m.ncols;
     }
-    const int total = expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s);
-    const int b = merge_runs<T, CAPM>(s, total);
-    const uint32_t* K = s.key[b];
-    const uint16_t* X = s.idx[b];
-    // runs of equal columns: head = first position; ordered sums (k order)
-    constexpr int E_MAX = (CAPM + T - 1) / T;
-    const int E = (total + T - 1) / T;
-    const int o0 = min(total, tid * E), o1 = min(total, o0 + E);
-    int nh = 0;
-    for (int o = o0; o < o1; ++o) nh += (o == 0 || K[o] != K[o - 1]);
-    int hoff, tile_cnt;
-    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
-    double res[E_MAX];
-    uint32_t rk[E_MAX];
-    int r = 0;
-#pragma unroll
-    for (int q = 0; q < E_MAX; ++q) {
-        const int o = o0 + q;
-        if (o < o1 && (o == 0 || K[o] != K[o - 1])) {
-            const uint32_t key = K[o];
-            double acc = 0.0;
-            int e = o;
-            do {
-                acc = __dadd_rn(acc, s.val[X[e]]);
-                ++e;
-            } while (e < total && K[e] == key);
-            res[r] = acc;
-            rk[r] = key;
-            ++r;
-        }
-    }
-    __syncthreads();
-    // stage compacted output in key[b^1] / val (both free now)
-    uint32_t* KO = s.key[b ^ 1];
-#pragma unroll
-    for (int q = 0; q < E_MAX; ++q) {
-        if (q < r) {
-            KO[hoff + q] = rk[q] + static_cast<uint32_t>(c0);
-            s.val[hoff + q] = res[q];
-        }
-    }
-    __syncthreads();
+    const int total = expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s, wsofs, wwi);
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(c1 - c0));
+    (void)tid;
     int64_t base = out.crp[row - out.row_begin];
     if (w >= 0) base += out.win_scan[w] - out.win_scan[wins[w].first];
-    for (int e = tid; e < tile_cnt; e += T) {
-        out.ccol[base + e] = static_cast<int32_t>(KO[e]);
-        out.cval[base + e] = s.val[e];
-    }
+    reduce_and_write<T, CAPM>(s, b, total, static_cast<uint32_t>(c0), out.ccol + base,
+                              out.cval + base);
 }
 
 template <int T, int CAPM>
 struct HashShared {
     int32_t table[2 * CAPM];
     typename cub::BlockReduce<int32_t, T>::TempStorage red;
+    typename cub::BlockScan<int32_t, T>::TempStorage scan;
     int64_t pstart[T];
-    int32_t plen[T];
+    int32_t poff[T + 1];
 };
 
 // Distinct output columns of (row, [c0,c1)) with <= CAPM products.
@@ -452,12 +499,16 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
     constexpr int LG = 1 + 31 - __builtin_clz(static_cast<unsigned>(CAPM));  // 2*CAPM slots
     const int32_t id = ids[blockIdx.x];
     int32_t row, c0, c1, w = -1;
+    int64_t wsofs = -1;
+    int wwi = 0;
     if (wins) {
         w = id;
         const Window wd = wins[w];
         row = wd.row;
         c0 = wd.c0;
         c1 = wd.c1;
+        wsofs = wd.sofs;
+        wwi = wd.wi;
     } else {
         row = id;
         c0 = 0;
@@ -474,32 +525,49 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         if (p < re) {
             const int32_t k = __ldg(m.acol + p);
             int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            if (!full) {
-                b0 = lower_bound_col(m.bcol, b0, b1, c0);
-                b1 = lower_bound_col(m.bcol, b0, b1, c1);
-            }
+            if (!full) window_bounds(m, wsofs, wwi, p - rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
         }
+        // compact the chunk's non-empty segments, then each thread inserts a
+        // contiguous range of the chunk's products
+        const int packed = len | ((len > 0) << 16);
+        int off, agg;
         __syncthreads();
-        s.pstart[tid] = start;
-        s.plen[tid] = len;
+        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        if (len > 0) {
+            s.pstart[off >> 16] = start;
+            s.poff[off >> 16] = off & 0xffff;
+        }
+        const int nr = agg >> 16, ct = agg & 0xffff;
+        if (tid == 0) s.poff[nr] = ct;
         __syncthreads();
-        const int nslots = static_cast<int>(::min(int64_t{T}, re - pc));
-        for (int slot = warp; slot < nslots; slot += NW) {
-            const int l = s.plen[slot];
-            const int64_t st = s.pstart[slot];
-            for (int q = lane; q < l; q += 32) {
-                const int32_t col = __ldg(m.bcol + st + q);
-                uint32_t hsl = col_hash(static_cast<uint32_t>(col), LG);
-                for (;;) {
-                    const int32_t prev = atomicCAS(&s.table[hsl], -1, col);
-                    if (prev == -1) {
-                        ++cnt;
-                        break;
+        const int E = (ct + T - 1) / T;
+        int e = min(ct, tid * E);
+        const int ee = min(ct, e + E);
+        if (e < ee) {
+            int lo = 0, hi = nr - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s.poff[mid] <= e) lo = mid; else hi = mid - 1;
+            }
+            int q = lo;
+            while (e < ee) {
+                while (s.poff[q + 1] <= e) ++q;
+                const int stop = min(ee, s.poff[q + 1]);
+                const int64_t base = s.pstart[q] - s.poff[q];
+                for (; e < stop; ++e) {
+                    const int32_t col = __ldg(m.bcol + base + e);
+                    uint32_t hsl = col_hash(static_cast<uint32_t>(col), LG);
+                    for (;;) {
+                        const int32_t prev = atomicCAS(&s.table[hsl], -1, col);
+                        if (prev == -1) {
+                            ++cnt;
+                            break;
+                        }
+                        if (prev == col) break;
+                        hsl = (hsl + 1) & (2 * CAPM - 1);
                     }
-                    if (prev == col) break;
-                    hsl = (hsl + 1) & (2 * CAPM - 1);
                 }
             }
         }
@@ -565,8 +633,7 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
         if (p < re) {
             const int32_t k = __ldg(m.acol + p);
             int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            b0 = lower_bound_col(m.bcol, b0, b1, c0);
-            b1 = lower_bound_col(m.bcol, b0, b1, c1);
+            window_bounds(m, wd.sofs, wd.wi, p - rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
             if (NUMERIC) av = __ldg(m.aval + p);
@@ -733,6 +800,18 @@ void launch_dense(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, co
 
 }  // namespace
 
+// Heavy rows with A-row length <= this are walked by the cursor kernel;
+// BSP_HEAVY_CURSOR=<dmax> enables it (default 0: planned windows, measured
+// faster on cfg5 — see DESIGN.md).
+static int64_t heavy_cursor_dmax() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("BSP_HEAVY_CURSOR");
+        const long long x = e ? std::atoll(e) : 0;
+        return static_cast<int64_t>(std::min<long long>(std::max<long long>(x, 0), HDMAX));
+    }();
+    return v;
+}
+
 Mats make_mats(const bsp_csr* A, const bsp_csr* B) {
     return Mats{A->row_ptr, A->col_idx, A->values, B->row_ptr, B->col_idx, B->values,
                 static_cast<int32_t>(B->ncols)};
@@ -743,6 +822,11 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     const int64_t n = re - rb;
     plan.rb = rb;
     plan.n = n;
+    DBuf<int64_t> prod_tmp;
+    if (!prod_out) {
+        prod_tmp = DBuf<int64_t>(h, n);
+        prod_out = prod_tmp.p;
+    }
     DBuf<uint8_t> cls(h, n);
     DBuf<int64_t> counters(h, 2 * NCLS);
     BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * NCLS * sizeof(int64_t), h->stream));
@@ -772,10 +856,41 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         BSP_LAUNCH(h, bucket_kernel, static_cast<unsigned>(div_up(n, 256)), 256, 0, cls.p, rb, n,
                    cursor.p, plan.lists.p);
     }
-    // Heavy rows -> windows.
-    const int64_t nh = plan.class_count[NCLS - 1];
+    // Heavy rows: A-row length <= HDMAX -> one CTA walks the row with cursors
+    // (longest rows first); longer ("mega") rows -> planned column windows.
+    const int64_t nh_all = plan.class_count[NCLS - 1];
+    int64_t nh = 0;
+    DBuf<int32_t> mega;
+    if (nh_all > 0) {
+        const int32_t* heavy_all = plan.lists.p + plan.class_off[NCLS - 1];
+        DBuf<int64_t> keys(h, nh_all), keys2(h, nh_all);
+        DBuf<int32_t> vals(h, nh_all);
+        plan.hcur = DBuf<int32_t>(h, nh_all);
+        mega = DBuf<int32_t>(h, nh_all);
+        DBuf<unsigned long long> cnt(h, 2);
+        BSP_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), h->stream));
+        BSP_LAUNCH(h, split_heavy_kernel, static_cast<unsigned>(div_up(nh_all, 256)), 256, 0, m,
+                   heavy_all, nh_all, rb, prod_out, keys.p, vals.p, mega.p, cnt.p,
+                   heavy_cursor_dmax());
+        unsigned long long hcnt[2];
+        d2h(h, hcnt, cnt.p, 2);
+        sync(h);
+        plan.nhcur = static_cast<int64_t>(hcnt[0]);
+        nh = static_cast<int64_t>(hcnt[1]);
+        if (plan.nhcur > 0) {
+            size_t tmp = 0;
+            BSP_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, keys.p, keys2.p, vals.p,
+                                                               plan.hcur.p, plan.nhcur, 0, 64,
+                                                               h->stream));
+            DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+            BSP_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, keys.p, keys2.p, vals.p,
+                                                               plan.hcur.p, plan.nhcur, 0, 64,
+                                                               h->stream));
+            ++h->launches;
+        }
+    }
     if (nh > 0) {
-        const int32_t* heavy = plan.lists.p + plan.class_off[NCLS - 1];
+        const int32_t* heavy = mega.p;
         int log_binw = LOG_WD;
         while (div_up(m.ncols, int64_t{1} << log_binw) > MAXBINS) ++log_binw;
         const int32_t nbins = static_cast<int32_t>(div_up(m.ncols, int64_t{1} << log_binw));
@@ -788,14 +903,27 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         set_smem(k0, sizeof(PlanShared));
         set_smem(k1, sizeof(PlanShared));
         BSP_LAUNCH(h, k0, static_cast<unsigned>(nh), PLAN_T, sizeof(PlanShared), m, heavy, nbins,
-                   log_binw, nwin.p, nullptr, nullptr, nullptr);
+                   log_binw, nwin.p, nullptr, nullptr, nullptr, nullptr, nullptr);
         DBuf<int64_t> woff(h, nh + 1);
         exclusive_scan_i32_to_i64(h, nwin.p, woff.p, nh + 1);
-        plan.nwin = read_scalar(h, woff.p + nh);
+        // per-(window, segment) start tables, bounded per row and in total
+        DBuf<int64_t> ssz(h, nh + 1), soff(h, nh + 1);
+        BSP_LAUNCH(h, start_size_kernel, static_cast<unsigned>(div_up(nh + 1, 256)), 256, 0, m,
+                   heavy, nh, nwin.p, int64_t{1} << 24, ssz.p);
+        exclusive_scan_i64(h, ssz.p, soff.p, nh + 1);
+        int64_t hv[2];
+        d2h(h, &hv[0], woff.p + nh, 1);
+        d2h(h, &hv[1], soff.p + nh, 1);
+        sync(h);
+        plan.nwin = hv[0];
+        const int64_t nstart = hv[1];
+        const bool use_starts = nstart > 0 && nstart <= (int64_t{1} << 29);
+        if (use_starts) plan.starts = DBuf<int32_t>(h, nstart);
         plan.wins = DBuf<Window>(h, plan.nwin);
         DBuf<uint8_t> dense(h, plan.nwin);
         BSP_LAUNCH(h, k1, static_cast<unsigned>(nh), PLAN_T, sizeof(PlanShared), m, heavy, nbins,
-                   log_binw, nullptr, woff.p, plan.wins.p, dense.p);
+                   log_binw, nullptr, woff.p, plan.wins.p, dense.p,
+                   use_starts ? soff.p : nullptr, use_starts ? plan.starts.p : nullptr);
         plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
         plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
         DBuf<unsigned long long> cursor(h, 2);
@@ -809,13 +937,34 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         plan.ndense = static_cast<int64_t>(hcur[1]);
     }
     for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];
+    h->stats.units[5] = plan.nhcur;
     h->stats.units[6] = plan.nsparse;
     h->stats.units[7] = plan.ndense;
 }
 
 template <bool NUMERIC>
-void run_plan(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx& out) {
-    for (int c = 1; c < NCLS - 1; ++c)
+void launch_heavy(bsp_handle h, const Mats& m, const int32_t* rows, int64_t n, const OutCtx& out) {
+    if (n <= 0) return;
+    constexpr int T = 256, CAPM = 4096;
+    if (NUMERIC) {
+        auto k = heavy_numeric_kernel<T, CAPM>;
+        set_smem(k, sizeof(HeavyNumShared<T, CAPM>));
+        BSP_LAUNCH_AS(h, "heavy_numeric<256,4096>", k, static_cast<unsigned>(n), T,
+                      sizeof(HeavyNumShared<T, CAPM>), m, rows, out);
+    } else {
+        auto k = heavy_symbolic_kernel<T, CAPM>;
+        set_smem(k, sizeof(HeavySymShared<T, CAPM>));
+        BSP_LAUNCH_AS(h, "heavy_symbolic<256,4096>", k, static_cast<unsigned>(n), T,
+                      sizeof(HeavySymShared<T, CAPM>), m, rows, out);
+    }
+}
+
+template <bool NUMERIC>
+void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCtx& out) {
+    const Mats m = plan.with_starts(m0);
+    // longest work first: cursor-walked heavy rows, then the light classes
+    launch_heavy<NUMERIC>(h, m, plan.hcur.p, plan.nhcur, out);
+    for (int c = NCLS - 2; c >= 1; --c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
     launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse, plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);

@@ -83,19 +83,23 @@ __global__ void __launch_bounds__(T) topk_tile_kernel(Mats m, const int32_t* __r
     const int tid = threadIdx.x;
     const int32_t id = ids[blockIdx.x];
     int32_t row, c0, c1, w = -1;
+    int64_t wsofs = -1;
+    int wwi = 0;
     if (wins) {
         w = id;
         const Window wd = wins[w];
         row = wd.row;
         c0 = wd.c0;
         c1 = wd.c1;
+        wsofs = wd.sofs;
+        wwi = wd.wi;
     } else {
         row = id;
         c0 = 0;
         c1 = m.ncols;
     }
     if (tid == 0) s_nc = 0;
-    const int total = expand_products<T, I, false>(m, row, c0, c1, wins == nullptr, s);
+    const int total = expand_products<T, I, false>(m, row, c0, c1, wins == nullptr, s, wsofs, wwi);
     const uint32_t width = static_cast<uint32_t>(c1 - c0);
     const int bits = bit_length(width);
     uint32_t k[I], v[I];
@@ -451,8 +455,8 @@ __global__ void __launch_bounds__(TDT) topk_dense_kernel(Mats m, const int32_t* 
     for (int64_t p = m.arp[row] + warp; p < m.arp[row + 1]; p += TDT / 32) {
         const int32_t k = __ldg(m.acol + p);
         int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-        b0 = lower_bound_col(m.bcol, b0, b1, c0);
-        b1 = lower_bound_col(m.bcol, b0, b1, c1);
+        window_bounds(m, wd.sofs, wd.wi, p - m.arp[row], m.arp[row + 1] - m.arp[row], c0, c1, b0,
+                      b1);
         for (int64_t q = b0 + lane; q < b1; q += 32) atomicAdd(&s.cnt[__ldg(m.bcol + q) - c0], 1);
     }
     __syncthreads();
@@ -516,11 +520,12 @@ int bsp_spgemm_topk(bsp_handle h, const bsp_csr* A, const bsp_csr* At, int32_t t
         launch_topk<256, 16>(h, m, plan.lists.p + co[4], cc[4], nullptr, topk, jacc_th, rj.p, rs.p,
                              rn.p, wj.p, ws.p, wn.p);
         if (plan.nwin > 0) {
-            launch_topk<256, 16>(h, m, plan.sparse_ids.p, plan.nsparse, plan.wins.p, topk, jacc_th,
+            const Mats mw = plan.with_starts(m);
+            launch_topk<256, 16>(h, mw, plan.sparse_ids.p, plan.nsparse, plan.wins.p, topk, jacc_th,
                                  rj.p, rs.p, rn.p, wj.p, ws.p, wn.p);
             set_smem(topk_dense_kernel, sizeof(TopkDenseShared));
             BSP_LAUNCH(h, topk_dense_kernel, static_cast<unsigned>(plan.ndense), TDT,
-                       sizeof(TopkDenseShared), m,
+                       sizeof(TopkDenseShared), mw,
                        plan.dense_ids.p, plan.wins.p, topk, jacc_th, wj.p, ws.p, wn.p);
             DBuf<int64_t> woff(h, plan.nwin + 1);
             exclusive_scan_i32_to_i64(h, wn.p, woff.p, plan.nwin + 1);
