@@ -1,0 +1,87 @@
+"""CPU, world_size 2 over gloo: the multi-GPU plumbing of the row-sharded
+multiply — product-balanced row split, B replication by
+broadcast, per-rank shard multiply (oracle stands in for the GPU kernel on
+CPU), optional global C by all-gather — must reproduce the 1-rank C exactly.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import paper_2507_21253_b200 as B
+from paper_2507_21253_b200 import distributed as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if rank == 0:
+            a = B.make_config(5, 11)
+            meta = torch.tensor([a.nrows, a.nnz()], dtype=torch.int64)
+        else:
+            a = None
+            meta = torch.zeros(2, dtype=torch.int64)
+        dist.broadcast(meta, 0)
+        n, nnz = (int(x) for x in meta)
+        rp = torch.from_numpy(a.row_ptr) if rank == 0 else torch.zeros(n + 1, dtype=torch.int64)
+        ci = torch.from_numpy(a.col_idx) if rank == 0 else torch.zeros(nnz, dtype=torch.int32)
+        v = torch.from_numpy(a.values) if rank == 0 else torch.zeros(nnz, dtype=torch.float64)
+        D.broadcast_csr(rp, ci, v)
+        A = O.Csr(n, n, rp.numpy(), ci.numpy(), v.numpy())
+        blen = np.diff(A.row_ptr)
+        prods = np.array([blen[A.col_idx[A.row_ptr[i]:A.row_ptr[i + 1]]].sum() for i in range(n)])
+        bounds = D.product_split(prods, world)
+        r0, r1 = D.shard(bounds, rank)
+        sub = O.Csr(r1 - r0, n, A.row_ptr[r0:r1 + 1] - A.row_ptr[r0],
+                    A.col_idx[A.row_ptr[r0]:A.row_ptr[r1]], A.values[A.row_ptr[r0]:A.row_ptr[r1]])
+        c = O.spgemm_rowwise(sub, A)  # stands in for bsp_spgemm_rowwise_range
+        grp, gci, gv = D.allgather_csr(torch.from_numpy(c.row_ptr), torch.from_numpy(c.col_idx),
+                                       torch.from_numpy(c.values))
+        if rank == 0:
+            full = O.spgemm_rowwise(A, A)
+            ok = (np.array_equal(grp.numpy(), full.row_ptr) and np.array_equal(gci.numpy(), full.col_idx)
+                  and np.array_equal(gv.numpy().view(np.uint64), full.values.view(np.uint64)))
+            share = [int(prods[bounds[g]:bounds[g + 1]].sum()) for g in range(world)]
+            q.put((ok, share, int(prods.sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_multiply_equals_single_rank():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok, share, total = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok, "gathered shards differ from the single-rank product"
+    assert sum(share) == total and max(share) <= 0.75 * total  # products balanced
+
+
+def test_product_split_rule():
+    prods = np.array([5, 0, 0, 100, 1, 1, 1, 1, 50, 2], dtype=np.int64)
+    b = D.product_split(prods, 3)
+    assert b[0] == 0 and b[-1] == prods.size and np.all(np.diff(b) >= 0)
+    pre = np.concatenate([[0], np.cumsum(prods)])
+    for g in range(1, 3):  # first row whose exclusive prefix reaches total*g/3
+        assert pre[b[g]] >= prods.sum() * g // 3 and (b[g] == 0 or pre[b[g] - 1] < prods.sum() * g // 3)
