@@ -145,7 +145,7 @@ __global__ void cluster_to_csr_kernel(const int32_t* __restrict__ sizes,
 // ---------------------------------------------------------------------------
 // cluster products + routing
 // ---------------------------------------------------------------------------
-constexpr int NCC = 4;  // 0: row-wise, 1: <=512, 2: <=2048, 3: <=4096 products
+constexpr int NCC = 4;  // 0: row-wise bins, 1: <=512, 2: <=2048, 3: <=4096 products
 __constant__ int kClusterCap[NCC] = {0, 512, 2048, 4096};
 
 __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
@@ -157,14 +157,23 @@ __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
     for (int64_t c = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; c < ncl;
          c += int64_t{gridDim.x} * blockDim.x) {
         const int K = m.sizes[c];
-        int64_t P = 0;
+        int64_t P = 0, S = 0;
+        const int64_t MC = m.ccp[c + 1] - m.ccp[c];
         for (int64_t u = m.ccp[c]; u < m.ccp[c + 1]; ++u) {
             const int32_t k = m.ccol[u];
-            P += static_cast<int64_t>(__popc(m.mask[u])) * (m.brp[k + 1] - m.brp[k]);
+            const int64_t len = m.brp[k + 1] - m.brp[k];
+            P += static_cast<int64_t>(__popc(m.mask[u])) * len;
+            S += len;
         }
+        // staged cluster tile: B rows of the cluster fit the stage, every
+        // member fits one merge tile (otherwise the rows go to the row bins)
+        // composite-key radix tile (measured fastest of the three cluster tiles
+        // tried — see DESIGN.md §4): classes by the cluster's total products
         int cl = 0;
-        const bool fits = (bit_length(static_cast<uint32_t>(K)) + cbits) <= 31;
-        if (K >= 2 && fits && P > 0 && P <= kClusterCap[NCC - 1]) {
+        const bool keyfits = bit_length(static_cast<uint32_t>(K - 1)) + cbits <= 31;
+        (void)MC;
+        (void)S;
+        if (K >= 2 && K <= MAXK && keyfits && P > 0 && P <= kClusterCap[NCC - 1]) {
             cl = 1;
             while (P > kClusterCap[cl]) ++cl;
         }
@@ -175,6 +184,13 @@ __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
     }
     __syncthreads();
     if (threadIdx.x < NCC) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+__global__ void invert_mask_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                   int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; i < n;
+         i += int64_t{gridDim.x} * blockDim.x)
+        out[i] = in[i] ? 0 : 1;
 }
 
 __global__ void cluster_bucket_kernel(const uint8_t* __restrict__ ccls, int64_t ncl,
@@ -684,13 +700,22 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
                        cursor.p, lists.p);
         }
         const Mats m = make_mats(&acsr, B);
-        RowwisePlan plan;
+        RowwisePlan plan;  // rows outside cluster tiles (incl. heavy windows)
         build_plan(h, m, 0, n, skip.p, plan, nullptr);
         h->stats.units[5] = cnt[1] + cnt[2] + cnt[3];  // cluster tiles
         DBuf<int64_t> row_nnz(h, n + 1);
         BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
-        run_cluster_classes<false>(h, cm, lists.p, off, cnt, cbits, row_nnz.p, nullptr, nullptr,
-                                   nullptr);
+        // Symbolic: C's row structure does not depend on the clustering, so the
+        // cluster rows are counted by the (cheaper) row-wise hash tiles of a
+        // second plan restricted to them.
+        {
+            DBuf<uint8_t> only(h, n);
+            BSP_LAUNCH(h, invert_mask_kernel, grid_for(h, n, 256), 256, 0, skip.p, only.p, n);
+            RowwisePlan plan_c;
+            build_plan(h, m, 0, n, only.p, plan_c, nullptr);
+            DBuf<int64_t> wn_c;
+            plan_symbolic(h, m, plan_c, row_nnz.p, wn_c);
+        }
         DBuf<int64_t> win_nnz;
         plan_symbolic(h, m, plan, row_nnz.p, win_nnz);
         DBuf<int64_t> rp(h, n + 1);

@@ -130,12 +130,13 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
 // Bottom-up stable merge of the runs in key[0]/idx[0]; returns the buffer
 // holding the sorted result.
 template <int T, int CAPM>
-__device__ __forceinline__ int merge_runs(MergeShared<T, CAPM>& s, int total) {
+__device__ __forceinline__ int merge_runs(MergeShared<T, CAPM>& s, int total,
+                                          int max_levels = 64) {
     const int tid = threadIdx.x;
     int R = s.nruns;
     int b = 0;
     const int E = (total + T - 1) / T;
-    while (R > 1) {
+    for (int level = 0; R > 1 && level < max_levels; ++level) {
         const int Rn = (R + 1) >> 1;
         const uint16_t* ro = s.ro(b);
         uint16_t* rn = s.ro(b ^ 1);
@@ -238,9 +239,8 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
 // (ascending k), stage (column + kofs, sum) compactly in smem and write them
 // coalesced to ccol/cval.  Returns the number of distinct columns.
 template <int T, int CAPM>
-__device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, int total,
-                                                uint32_t kofs, int32_t* __restrict__ ccol,
-                                                double* __restrict__ cval) {
+__device__ __forceinline__ int reduce_stage(MergeShared<T, CAPM>& s, int b, int total,
+                                            uint32_t kofs) {
     const int tid = threadIdx.x;
     const uint32_t* K = s.key(b);
     const uint16_t* X = s.idx(b);
@@ -284,7 +284,16 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
         }
     }
     __syncthreads();
-    for (int e = tid; e < tile_cnt; e += T) {
+    return tile_cnt;  // staged: keys in s.key(b ^ 1) (padded), sums in s.val
+}
+
+template <int T, int CAPM>
+__device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, int total,
+                                                uint32_t kofs, int32_t* __restrict__ ccol,
+                                                double* __restrict__ cval) {
+    const int tile_cnt = reduce_stage<T, CAPM>(s, b, total, kofs);
+    const uint32_t* KO = s.key(b ^ 1);
+    for (int e = threadIdx.x; e < tile_cnt; e += T) {
         ccol[e] = static_cast<int32_t>(KO[PADI(e)]);
         cval[e] = s.val[e];
     }
