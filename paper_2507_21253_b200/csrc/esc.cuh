@@ -16,6 +16,7 @@ constexpr int CAPH = CAP / 2;
 // < CAPG + CAPB = CAP products and averages ~CAPG.
 constexpr int CAPB = CAP / 4;
 constexpr int CAPG = CAP - CAPB;
+constexpr int WSMALL = CAP / 2;  // sparse windows with <= WSMALL products run in half tiles
 constexpr int WD = 4096;      // dense window width in columns
 constexpr int LOG_WD = 12;
 constexpr int MAXBINS = 4096; // planner histogram bins per heavy row
@@ -39,7 +40,7 @@ struct Window {
     int32_t c0, c1; // column range [c0, c1)
     int32_t first;  // index of the row's first window
     int32_t wi;     // index of this window within its row
-    int32_t pad_;
+    int32_t nprod;  // products in the window (sparse windows)
     int64_t sofs;   // offset of the row's per-(window, segment) start table, or -1
 };
 
@@ -168,6 +169,7 @@ struct RowwisePlan {
     int64_t class_off[NCLS + 1]{};
     DBuf<int32_t> lists;  // all non-empty rows grouped by class
     int64_t nwin = 0, nsparse = 0, ndense = 0;
+    int64_t nsparse_large = 0;  // sparse_ids[0, nsparse_large): > WSMALL products
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
     int64_t nhcur = 0;    // heavy rows walked by one CTA with cursors

@@ -306,8 +306,9 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     // 1.3x faster tiles); skewed / duplicate-heavy tiles fall through.
     // (measured: small tiles only; cfg4/cfg5's larger tiles are slower with it)
     if (CAPM <= 512 && levels >= 2 && msd_sort_tile<T, CAPM>(s, total, width)) return 1;
-    // pad key = 2^bits - 1 must exceed every key (< width)
-    const int bits = bit_length(width);
+    // pad key = 2^bits - 1 >= every key (<= width-1); pads sit after `total`
+    // and the sort is stable, so real entries keep the first `total` slots.
+    const int bits = bit_length(width > 1 ? width - 1 : 1);
     const int passes = (bits + 5) / 6;
     if (levels > passes + 1) {  // measured: cfg4 (5 levels vs 4 passes) prefers merge
         radix_sort_tile<T, CAPM>(s, total, bits);

@@ -110,25 +110,90 @@ __global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64
 // K2: heavy-row planner
 // ---------------------------------------------------------------------------
 constexpr int PLAN_T = 256;
+constexpr int PLAN_U = 4;  // B-row chunks of 32 loaded ahead per warp
+constexpr uint32_t DENSE_BIT = 0x80000000u;
 
-struct PlanShared {
+struct PlanCountShared {
     int32_t hist[MAXBINS];
-    int32_t wstart[MAXBINS];  // per bin: first window index (or -1)
-    int32_t wc0[MAXBINS];     // window -> c0 (bounded by MAXBINS windows per row)
     typename cub::BlockScan<int32_t, PLAN_T>::TempStorage scan;
-    int32_t total;
 };
 
-// Histogram of a heavy row's products over `nbins` bins of width 1<<log_binw.
-__device__ void plan_histogram(const Mats& m, int32_t row, int log_binw, int32_t* hist) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = PLAN_T / 32;
-    for (int64_t p = m.arp[row] + warp; p < m.arp[row + 1]; p += nw) {
-        const int32_t k = __ldg(m.acol + p);
-        const int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-        for (int64_t q0 = b0; q0 < b1; q0 += 32) {
-            const int64_t q = q0 + lane;
-            const bool ok = q < b1;
-            const int32_t bin = ok ? (__ldg(m.bcol + q) >> log_binw) : 0x7fffffff;
+// Start tables of up to STAGE entries are built in smem and stored coalesced.
+constexpr int STAGE = 2 * MAXBINS;
+struct PlanWriteShared {
+    int32_t binwin[MAXBINS];  // bin -> window
+    union {
+        struct {
+            uint32_t wc0[MAXBINS + 1];  // window -> c0 | DENSE_BIT (+ sentinel ncols)
+            int32_t wpre[MAXBINS + 1];  // window -> product prefix at c0 (+ sentinel P)
+        } w;
+        int32_t stage[STAGE + 2];
+    } u;
+};
+
+// Walk the segments (A-row entries) of `row` one warp per segment, the
+// (b0, b1) bounds of 32 upcoming segments fetched at once by the warp's lanes
+// and PLAN_U chunks of 32 B columns loaded before they are consumed, so each
+// warp keeps several independent loads in flight.  f(p, q0, len, cols[U],
+// state) is called for each group of chunks (warp-uniform); cols[u] holds
+// the column of element q0 + 32u + lane or -1 past the end; `state` is an
+// int reset to -1 at the start of every segment.
+template <class F>
+__device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = PLAN_T / 32;
+    const int64_t rs = m.arp[row];
+    const int d = static_cast<int>(m.arp[row + 1] - rs);
+    for (int pb = warp; pb < d; pb += NW * 32) {
+        const int pl = pb + NW * lane;
+        int64_t mb0 = 0, mb1 = 0;
+        if (pl < d) {
+            const int32_t k = __ldg(m.acol + rs + pl);
+            mb0 = __ldg(m.brp + k);
+            mb1 = __ldg(m.brp + k + 1);
+        }
+        const int nseg = ::min(32, (d - pb + NW - 1) / NW);
+        for (int j = 0; j < nseg; ++j) {
+            const int64_t b0 = __shfl_sync(0xffffffffu, mb0, j);
+            const int len = static_cast<int>(__shfl_sync(0xffffffffu, mb1, j) - b0);
+            const int p = pb + NW * j;
+            int state = -1;
+            for (int q0 = 0; q0 < len; q0 += 32 * PLAN_U) {
+                int32_t cols[PLAN_U];
+#pragma unroll
+                for (int u = 0; u < PLAN_U; ++u) {
+                    const int q = q0 + 32 * u + lane;
+                    cols[u] = q < len ? __ldg(m.bcol + b0 + q) : -1;
+                }
+                f(p, q0, len, cols, state);
+            }
+        }
+    }
+}
+
+// K2a: per heavy row, a product histogram over `nbins` column bins, then the
+// window cut: a bin with > CAPB products gets its own window (dense when
+// > CAP), runs of smaller bins are cut where floor(prefix / CAPG) changes or
+// after a big bin.  Writes the window count and the descriptors
+// {c0 | DENSE_BIT, product prefix} (+ sentinel {ncols, P}) at desc[doff[h]].
+__global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
+                                                            const int32_t* __restrict__ heavy,
+                                                            int32_t nbins, int log_binw,
+                                                            int32_t* __restrict__ nwin,
+                                                            const int64_t* __restrict__ doff,
+                                                            uint2* __restrict__ desc) {
+    __shared__ PlanCountShared s;
+    const int32_t hrow = blockIdx.x;
+    const int32_t row = heavy[hrow];
+    const int lane = threadIdx.x & 31;
+    for (int b = threadIdx.x; b < nbins; b += PLAN_T) s.hist[b] = 0;
+    __syncthreads();
+    stream_segments(m, row, [&](int, int q0, int len, const int32_t* cols, int&) {
+#pragma unroll
+        for (int u = 0; u < PLAN_U; ++u) {
+            if (q0 + 32 * u >= len) break;
+            const bool ok = cols[u] >= 0;
+            const int32_t bin = ok ? (cols[u] >> log_binw) : 0x7fffffff;
             // columns are sorted within the B row, so equal bins form runs:
             // the last lane of each run adds the run length.
             const int32_t nxt = __shfl_down_sync(0xffffffffu, bin, 1);
@@ -137,37 +202,16 @@ __device__ void plan_histogram(const Mats& m, int32_t row, int log_binw, int32_t
             const unsigned heads = __ballot_sync(0xffffffffu, ok && (lane == 0 || prv != bin));
             if (tail) {
                 const unsigned below = heads & ((2u << lane) - 1u);
-                const int head_lane = 31 - __clz(below);
-                atomicAdd(&hist[bin], lane - head_lane + 1);
+                atomicAdd(&s.hist[bin], lane - (31 - __clz(below)) + 1);
             }
         }
-    }
-}
-
-// mode 0: count windows per heavy row; mode 1: write them.
-template <int MODE>
-__global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __restrict__ heavy,
-                                                      int32_t nbins, int log_binw,
-                                                      int32_t* __restrict__ nwin,
-                                                      const int64_t* __restrict__ win_off,
-                                                      Window* __restrict__ wins,
-                                                      uint8_t* __restrict__ win_dense,
-                                                      const int64_t* __restrict__ start_off,
-                                                      int32_t* __restrict__ starts) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    PlanShared& s = *reinterpret_cast<PlanShared*>(smem_raw);
-    const int32_t hrow = blockIdx.x;
-    const int32_t row = heavy[hrow];
-    for (int b = threadIdx.x; b < nbins; b += PLAN_T) s.hist[b] = 0;
+    });
     __syncthreads();
-    plan_histogram(m, row, log_binw, s.hist);
-    __syncthreads();
-    const int sub = 1 << (log_binw - LOG_WD);  // dense sub-windows per big bin
-    // Per-bin window-start counts, in blocked arrangement (ITEMS bins/thread).
+    // Per-bin counts in blocked arrangement (ITEMS bins per thread).
     constexpr int ITEMS = MAXBINS / PLAN_T;
-    int32_t excl[ITEMS];
-    int32_t cnt[ITEMS];
+    int32_t excl[ITEMS], cnt[ITEMS];
     int32_t local = 0;
+#pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int b = threadIdx.x * ITEMS + i;
         cnt[i] = b < nbins ? s.hist[b] : 0;
@@ -177,106 +221,138 @@ __global__ void __launch_bounds__(PLAN_T) plan_kernel(Mats m, const int32_t* __r
     int32_t base, tot;
     cub::BlockScan<int32_t, PLAN_T>(s.scan).ExclusiveSum(local, base, tot);
     __syncthreads();
-    // Bin b's exclusive product prefix: base + excl[i].  Window starts:
-    //   big bin (cnt > CAPH): 1 sparse window if cnt <= CAP, else `sub` dense
-    //   small bin: starts a window if first, after a big bin, or when
-    //   floor(prefix / CAPH) changes  (sum of such a run <= CAP).
-    int32_t nstart[ITEMS];
+    bool starts[ITEMS];
     int32_t mine = 0;
+#pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int b = threadIdx.x * ITEMS + i;
-        nstart[i] = 0;
-        if (b >= nbins) continue;
         const int32_t pre = base + excl[i];
-        const bool big = cnt[i] > CAPB;
-        if (big) {
-            nstart[i] = cnt[i] > CAP ? sub : 1;
-        } else {
-            bool start = (b == 0);
-            if (!start) {
+        bool st = false;
+        if (b < nbins) {
+            st = (b == 0) || cnt[i] > CAPB;
+            if (!st) {
                 const int32_t pc = s.hist[b - 1];
-                const int32_t ppre = pre - pc;
-                start = (pc > CAPB) || (ppre / CAPG != pre / CAPG);
+                st = (pc > CAPB) || ((pre - pc) / CAPG != pre / CAPG);
             }
-            nstart[i] = start ? 1 : 0;
         }
-        mine += nstart[i];
+        starts[i] = st;
+        mine += st;
     }
     int32_t wbase, wtot;
     cub::BlockScan<int32_t, PLAN_T>(s.scan).ExclusiveSum(mine, wbase, wtot);
-    if (MODE == 0) {
-        if (threadIdx.x == 0) nwin[hrow] = wtot;
-        return;
-    }
-    // MODE 1: record c0 of every window, then emit [c0, c1).
+    uint2* dd = desc + doff[hrow];
     int32_t w = wbase;
+#pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const int b = threadIdx.x * ITEMS + i;
-        if (b >= nbins || nstart[i] == 0) continue;
-        const int32_t c0 = b << log_binw;
-        if (nstart[i] == 1) {
-            s.wc0[w] = c0;
-            s.wstart[w] = (cnt[i] > CAP) ? 1 : 0;  // dense flag
-            ++w;
-        } else {
-            for (int j = 0; j < nstart[i]; ++j) {
-                s.wc0[w] = c0 + (j << LOG_WD);
-                s.wstart[w] = 1;
-                ++w;
-            }
-        }
+        if (!starts[i]) continue;
+        const uint32_t c0 = static_cast<uint32_t>((threadIdx.x * ITEMS + i) << log_binw);
+        dd[w++] = make_uint2(c0 | (cnt[i] > CAP ? DENSE_BIT : 0u),
+                             static_cast<uint32_t>(base + excl[i]));
     }
-    // bin -> window (sub == 1: every bin lies in exactly one window)
-    {
-        int32_t run = wbase;
-        for (int i = 0; i < ITEMS; ++i) {
-            const int b = threadIdx.x * ITEMS + i;
-            run += nstart[i];
-            if (b < nbins) s.hist[b] = run - 1;  // hist no longer needed
-        }
+    if (threadIdx.x == 0) {
+        nwin[hrow] = wtot;
+        dd[wtot] = make_uint2(static_cast<uint32_t>(m.ncols), static_cast<uint32_t>(tot));
+    }
+}
+
+// K2b: emit the Window records of each heavy row and its per-(window,
+// segment) start table: starts[sofs + w*d + p] = number of elements of
+// segment p lying in windows < w (one streaming pass over the row).
+__global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
+    Mats m, const int32_t* __restrict__ heavy, int32_t nbins, int log_binw,
+    const int32_t* __restrict__ nwin, const int64_t* __restrict__ doff,
+    const uint2* __restrict__ desc, const int64_t* __restrict__ win_off, Window* __restrict__ wins,
+    uint8_t* __restrict__ win_cat, const int64_t* __restrict__ start_off, int64_t start_budget,
+    int32_t* __restrict__ starts) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PlanWriteShared& s = *reinterpret_cast<PlanWriteShared*>(smem_raw);
+    const int32_t hrow = blockIdx.x;
+    const int32_t row = heavy[hrow];
+    const int wtot = nwin[hrow];
+    const uint2* dd = desc + doff[hrow];
+    for (int k = threadIdx.x; k <= wtot; k += PLAN_T) {
+        const uint2 v = dd[k];
+        s.u.w.wc0[k] = v.x;
+        s.u.w.wpre[k] = static_cast<int32_t>(v.y);
     }
     __syncthreads();
+    // bin -> window: the last window whose c0 <= the bin's first column
+    for (int b = threadIdx.x; b < nbins; b += PLAN_T) {
+        const uint32_t c = static_cast<uint32_t>(b) << log_binw;
+        int lo = 0, hi = wtot - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((s.u.w.wc0[mid] & ~DENSE_BIT) <= c) lo = mid; else hi = mid - 1;
+        }
+        s.binwin[b] = lo;
+    }
     const int64_t off = win_off[hrow];
-    const int64_t sofs = (starts != nullptr && start_off[hrow + 1] > start_off[hrow])
+    // rows past the table budget binary-search their segments instead
+    const int64_t sofs = (starts != nullptr && start_off[hrow + 1] > start_off[hrow] &&
+                          start_off[hrow + 1] <= start_budget)
                              ? start_off[hrow] : -1;
     for (int k = threadIdx.x; k < wtot; k += PLAN_T) {
         Window wd;
         wd.row = row;
-        wd.c0 = s.wc0[k];
-        int64_t c1 = (k + 1 < wtot) ? s.wc0[k + 1] : m.ncols;
-        if (s.wstart[k]) c1 = ::min(c1, int64_t{wd.c0} + WD);
+        const bool dense = (s.u.w.wc0[k] & DENSE_BIT) != 0;
+        wd.c0 = static_cast<int32_t>(s.u.w.wc0[k] & ~DENSE_BIT);
+        int64_t c1 = int64_t{s.u.w.wc0[k + 1] & ~DENSE_BIT};
+        if (dense) c1 = ::min(c1, int64_t{wd.c0} + WD);
         wd.c1 = static_cast<int32_t>(::min(c1, int64_t{m.ncols}));
         wd.first = static_cast<int32_t>(off);
         wd.wi = k;
+        wd.nprod = s.u.w.wpre[k + 1] - s.u.w.wpre[k];
         wd.sofs = sofs;
         wins[off + k] = wd;
-        win_dense[off + k] = static_cast<uint8_t>(s.wstart[k]);
+        // 0: sparse, 1: dense, 2: sparse with <= WSMALL products
+        win_cat[off + k] = static_cast<uint8_t>(dense ? 1 : (wd.nprod <= WSMALL ? 2 : 0));
     }
     if (sofs < 0) return;
-    // Per-(window, segment) start offsets: starts[sofs + w*d + p] = number of
-    // elements of segment p lying in windows < w (streamed once per segment).
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t rs = m.arp[row];
-    const int d = static_cast<int>(m.arp[row + 1] - rs);
-    int32_t* st = starts + sofs;
-    for (int p = warp; p < d; p += PLAN_T / 32) {
-        const int32_t k = __ldg(m.acol + rs + p);
-        const int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-        const int len = static_cast<int>(b1 - b0);
-        int carry = -1;  // window of the previous element
-        for (int q0 = 0; q0 < len; q0 += 32) {
-            const int q = q0 + lane;
-            const int wq = q < len ? s.hist[__ldg(m.bcol + b0 + q) >> log_binw] : wtot;
+    __syncthreads();  // wc0/wpre dead: the union becomes the staging area
+    const int lane = threadIdx.x & 31;
+    const int d = static_cast<int>(m.arp[row + 1] - m.arp[row]);
+    const int64_t tsz = int64_t{wtot + 1} * d;
+    const bool staged = tsz <= STAGE;
+    int32_t* tab = staged ? s.u.stage : starts + sofs;
+    stream_segments(m, row, [&](int p, int q0, int len, const int32_t* cols, int& carry) {
+        // carry: window of the element before this group (-1 at q0 == 0)
+#pragma unroll
+        for (int u = 0; u < PLAN_U; ++u) {
+            const int qb = q0 + 32 * u;
+            if (qb >= len) break;
+            const int q = qb + lane;
+            const int wq = cols[u] >= 0 ? s.binwin[cols[u] >> log_binw] : wtot;
             int wp = __shfl_up_sync(0xffffffffu, wq, 1);
             if (lane == 0) wp = carry;
             if (q < len)
-                for (int w2 = wp + 1; w2 <= wq; ++w2) st[int64_t{w2} * d + p] = q;
-            carry = __shfl_sync(0xffffffffu, wq, ::min(31, len - 1 - q0));
+                for (int w2 = wp + 1; w2 <= wq; ++w2) tab[w2 * int64_t{d} + p] = q;
+            carry = __shfl_sync(0xffffffffu, wq, ::min(31, len - 1 - qb));
         }
         // windows after the last element start at len
-        const int wl = (len > 0) ? carry : -1;
-        for (int w2 = wl + 1 + lane; w2 <= wtot; w2 += 32) st[int64_t{w2} * d + p] = len;
+        if (q0 + 32 * PLAN_U >= len)
+            for (int w2 = carry + 1 + lane; w2 <= wtot; w2 += 32) tab[w2 * int64_t{d} + p] = len;
+    });
+    if (staged) {
+        __syncthreads();
+        int32_t* st = starts + sofs;
+        for (int i = threadIdx.x; i < tsz; i += PLAN_T) st[i] = s.u.stage[i];
     }
+}
+
+// Upper bound on a heavy row's windows (+1 sentinel descriptor):
+// <= P/(CAPB+1) big bins, each may also start the run after it, and the
+// runs are cut at most P/CAPG times.
+__global__ void plan_bound_kernel(const int32_t* __restrict__ heavy, int64_t nh, int64_t rb,
+                                  const int64_t* __restrict__ prod, int32_t nbins,
+                                  int64_t* __restrict__ bound) {
+    const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (t > nh) return;
+    if (t == nh) {
+        bound[t] = 0;
+        return;
+    }
+    const int64_t P = prod[heavy[t] - rb];
+    bound[t] = ::min(2 * (P / (CAPB + 1)) + P / CAPG + 2, int64_t{nbins}) + 1;
 }
 
 // Size of each heavy row's start table ((windows+1) x A-row length), or 0
@@ -316,26 +392,27 @@ __global__ void split_heavy_kernel(Mats m, const int32_t* __restrict__ heavy, in
     }
 }
 
-// Split window ids into sparse / dense lists.
-__global__ void split_windows_kernel(const uint8_t* __restrict__ dense, int64_t nw,
+// Split window ids by category (0 sparse, 1 dense, 2 small sparse) into
+// out[category] lists.
+__global__ void split_windows_kernel(const uint8_t* __restrict__ cat, int64_t nw,
                                      unsigned long long* __restrict__ cursor,
-                                     int32_t* __restrict__ sparse_ids,
-                                     int32_t* __restrict__ dense_ids) {
-    __shared__ unsigned s_cnt[2];
-    __shared__ unsigned long long s_base[2];
-    if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
+                                     int32_t* __restrict__ out0, int32_t* __restrict__ out1,
+                                     int32_t* __restrict__ out2) {
+    __shared__ unsigned s_cnt[3];
+    __shared__ unsigned long long s_base[3];
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     const int64_t w = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
     int d = 0;
     unsigned rank = 0;
     if (w < nw) {
-        d = dense[w];
+        d = cat[w];
         rank = atomicAdd(&s_cnt[d], 1u);
     }
     __syncthreads();
-    if (threadIdx.x < 2) s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
+    if (threadIdx.x < 3) s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
     __syncthreads();
-    if (w < nw) (d ? dense_ids : sparse_ids)[s_base[d] + rank] = static_cast<int32_t>(w);
+    if (w < nw) (d == 0 ? out0 : d == 1 ? out1 : out2)[s_base[d] + rank] = static_cast<int32_t>(w);
 }
 
 template <int T, int I, bool NUMERIC>
@@ -898,12 +975,17 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                 "planner: heavy rows need ncols <= 16M (MAXBINS*WD) in this build");
         DBuf<int32_t> nwin(h, nh + 1);
         BSP_CUDA(cudaMemsetAsync(nwin.p, 0, (nh + 1) * sizeof(int32_t), h->stream));
-        auto k0 = plan_kernel<0>;
-        auto k1 = plan_kernel<1>;
-        set_smem(k0, sizeof(PlanShared));
-        set_smem(k1, sizeof(PlanShared));
-        BSP_LAUNCH(h, k0, static_cast<unsigned>(nh), PLAN_T, sizeof(PlanShared), m, heavy, nbins,
-                   log_binw, nwin.p, nullptr, nullptr, nullptr, nullptr, nullptr);
+        // window descriptors: per heavy row a slot sized by the window bound
+        DBuf<int64_t> dbound(h, nh + 1), doff(h, nh + 1);
+        BSP_LAUNCH(h, plan_bound_kernel, static_cast<unsigned>(div_up(nh + 1, 256)), 256, 0,
+                   heavy, nh, rb, prod_out, nbins, dbound.p);
+        exclusive_scan_i64(h, dbound.p, doff.p, nh + 1);
+        int64_t ndesc = 0;
+        d2h(h, &ndesc, doff.p + nh, 1);
+        sync(h);
+        DBuf<uint2> desc(h, ndesc);
+        BSP_LAUNCH(h, plan_count_kernel, static_cast<unsigned>(nh), PLAN_T, 0, m, heavy, nbins,
+                   log_binw, nwin.p, doff.p, desc.p);
         DBuf<int64_t> woff(h, nh + 1);
         exclusive_scan_i32_to_i64(h, nwin.p, woff.p, nh + 1);
         // per-(window, segment) start tables, bounded per row and in total
@@ -916,28 +998,41 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         d2h(h, &hv[1], soff.p + nh, 1);
         sync(h);
         plan.nwin = hv[0];
-        const int64_t nstart = hv[1];
-        const bool use_starts = nstart > 0 && nstart <= (int64_t{1} << 29);
-        if (use_starts) plan.starts = DBuf<int32_t>(h, nstart);
+        // Start-table budget: <= 2^30 entries (4 GB) and <= 1/8 of free HBM;
+        // the rows in scan order that fit get a table.
+        size_t free_b = 0, total_b = 0;
+        BSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const int64_t budget = std::min<int64_t>(
+            {hv[1], int64_t{1} << 30, static_cast<int64_t>(free_b / (8 * sizeof(int32_t)))});
+        const bool use_starts = budget > 0;
+        if (use_starts) plan.starts = DBuf<int32_t>(h, budget);
         plan.wins = DBuf<Window>(h, plan.nwin);
         DBuf<uint8_t> dense(h, plan.nwin);
-        BSP_LAUNCH(h, k1, static_cast<unsigned>(nh), PLAN_T, sizeof(PlanShared), m, heavy, nbins,
-                   log_binw, nullptr, woff.p, plan.wins.p, dense.p,
-                   use_starts ? soff.p : nullptr, use_starts ? plan.starts.p : nullptr);
+        set_smem(plan_write_kernel, sizeof(PlanWriteShared));
+        BSP_LAUNCH(h, plan_write_kernel, static_cast<unsigned>(nh), PLAN_T,
+                   sizeof(PlanWriteShared), m, heavy, nbins, log_binw, nwin.p, doff.p, desc.p,
+                   woff.p, plan.wins.p, dense.p, use_starts ? soff.p : nullptr, budget,
+                   use_starts ? plan.starts.p : nullptr);
         plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
         plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
-        DBuf<unsigned long long> cursor(h, 2);
-        BSP_CUDA(cudaMemsetAsync(cursor.p, 0, 2 * sizeof(unsigned long long), h->stream));
+        DBuf<int32_t> small(h, plan.nwin);
+        DBuf<unsigned long long> cursor(h, 3);
+        BSP_CUDA(cudaMemsetAsync(cursor.p, 0, 3 * sizeof(unsigned long long), h->stream));
         BSP_LAUNCH(h, split_windows_kernel, static_cast<unsigned>(div_up(plan.nwin, 256)), 256, 0,
-                   dense.p, plan.nwin, cursor.p, plan.sparse_ids.p, plan.dense_ids.p);
-        unsigned long long hcur[2];
-        d2h(h, hcur, cursor.p, 2);
+                   dense.p, plan.nwin, cursor.p, plan.sparse_ids.p, plan.dense_ids.p, small.p);
+        unsigned long long hcur[3];
+        d2h(h, hcur, cursor.p, 3);
         sync(h);
-        plan.nsparse = static_cast<int64_t>(hcur[0]);
+        // sparse list = large windows, then small ones (top-k walks it whole)
+        plan.nsparse_large = static_cast<int64_t>(hcur[0]);
+        plan.nsparse = static_cast<int64_t>(hcur[0] + hcur[2]);
         plan.ndense = static_cast<int64_t>(hcur[1]);
+        if (hcur[2] > 0)
+            BSP_CUDA(cudaMemcpyAsync(plan.sparse_ids.p + hcur[0], small.p,
+                                     hcur[2] * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                     h->stream));
     }
-    for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];
-    h->stats.units[5] = plan.nhcur;
+    for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];  // [5] = heavy rows
     h->stats.units[6] = plan.nsparse;
     h->stats.units[7] = plan.ndense;
 }
@@ -966,7 +1061,9 @@ void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCt
     launch_heavy<NUMERIC>(h, m, plan.hcur.p, plan.nhcur, out);
     for (int c = NCLS - 2; c >= 1; --c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
-    launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse, plan.wins.p, out);
+    launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
+    launch_tile<128, 2048, NUMERIC>(h, m, plan.sparse_ids.p + plan.nsparse_large,
+                                    plan.nsparse - plan.nsparse_large, plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
 
