@@ -53,14 +53,52 @@ struct MergeShared {
     int nruns;
 };
 
+// Largest power of two < n (0 for n <= 1): the first step of find_run.
+__device__ __forceinline__ int run_search_step(int n) {
+    return n > 1 ? 1 << (31 - __clz(n - 1)) : 0;
+}
+
+// Index q of the run holding element e: the largest q < n with poff[q] <= e
+// (poff[0] == 0).  Fixed trip count, so unrolled callers overlap their loads.
+__device__ __forceinline__ int find_run(const int32_t* poff, int n, int step, int e) {
+    int q = 0;
+    for (int st = step; st > 0; st >>= 1)
+        if (q + st < n && poff[q + st] <= e) q += st;
+    return q;
+}
+
 // Expand the products of (row, [c0, c1)) in (k, j) order; every non-empty
 // B-row segment becomes one sorted run.  Returns the product count.
+// Asynchronous global -> shared copies (sm_80+ LDGSTS), 4 and 8 bytes.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// Warp-contiguous split of `ct` flattened run elements over `nwarps` warps
+// (slices rounded to 32): this lane starts at element e (< we) inside run q.
+__device__ __forceinline__ void warp_slice_begin(const int32_t* poff, int nr, int ct, int nwarps,
+                                                 int& e, int& we, int& q) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ew = (((ct + nwarps - 1) / nwarps) + 31) & ~31;
+    const int wb = min(ct, warp * ew);
+    we = min(ct, wb + ew);
+    e = wb + lane;
+    q = e < we ? find_run(poff, nr, run_search_step(nr), e) : 0;
+}
+
 template <int T, int CAPM, bool VALUES>
 __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c0, int32_t c1,
                                            bool full, MergeShared<T, CAPM>& s,
                                            int64_t wsofs = -1, int wwi = 0) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = T / 32;
+    const int tid = threadIdx.x;
     const int64_t rs = m.arp[row], re = m.arp[row + 1];
     int total = 0, nruns = 0;
     for (int64_t pc = rs; pc < re; pc += T) {
@@ -91,30 +129,35 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         const int nr = agg >> 16, ct = agg & 0xffff;
         if (tid == 0) s.poff[nr] = ct;
         __syncthreads();
-        // each thread copies a contiguous range of the chunk's products
-        const int E = (ct + T - 1) / T;
-        int e = min(ct, tid * E);
-        const int ee = min(ct, e + E);
-        if (e < ee) {
-            int lo = 0, hi = nr - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s.poff[mid] <= e) lo = mid; else hi = mid - 1;
-            }
-            int q = lo;
-            while (e < ee) {
+        // Gather: warp w takes a contiguous slice of the chunk's products, its
+        // lanes consecutive ones (coalesced), and copies each product's B
+        // column and value straight into the tile with cp.async — no register
+        // round trip, so every load of the slice is in flight at once.  The
+        // run of each product is kept in the (idle) merge buffer for the
+        // fix-up pass.
+        uint16_t* rid = s.idx(1);
+        {
+            int e, we, q;
+            warp_slice_begin(s.poff, nr, ct, T / 32, e, we, q);
+            for (; e < we; e += 32) {
                 while (s.poff[q + 1] <= e) ++q;
-                const int stop = min(ee, s.poff[q + 1]);
-                const int64_t base = s.pstart[q] - s.poff[q];
-                double a = 0.0;
-                if (VALUES) a = s.pav[q];
-                for (; e < stop; ++e) {
-                    const int g = total + e;
-                    s.key(0)[PADI(g)] = static_cast<uint32_t>(__ldg(m.bcol + base + e) - c0);
-                    s.idx(0)[PADI(g)] = static_cast<uint16_t>(g);
-                    if (VALUES) s.val[g] = __dmul_rn(a, __ldg(m.bval + base + e));
+                const int64_t src = s.pstart[q] + (e - s.poff[q]);
+                const int g = total + e;
+                cp_async4(&s.key(0)[PADI(g)], m.bcol + src);
+                if (VALUES) {
+                    cp_async8(&s.val[g], m.bval + src);
+                    rid[g] = static_cast<uint16_t>(q);
                 }
             }
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        // fix-up: window-relative key, position, product a_ik * b_kj
+        for (int e = tid; e < ct; e += T) {
+            const int g = total + e;
+            s.key(0)[PADI(g)] -= static_cast<uint32_t>(c0);
+            s.idx(0)[PADI(g)] = static_cast<uint16_t>(g);
+            if (VALUES) s.val[g] = __dmul_rn(s.pav[rid[g]], s.val[g]);
         }
         total += ct;
         nruns += nr;

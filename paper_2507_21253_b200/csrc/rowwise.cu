@@ -619,16 +619,13 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         const int nr = agg >> 16, ct = agg & 0xffff;
         if (tid == 0) s.poff[nr] = ct;
         __syncthreads();
+        // each thread inserts a contiguous range of the chunk's products
+        // (measured faster here than warp-strided slices: no per-element walk)
         const int E = (ct + T - 1) / T;
         int e = min(ct, tid * E);
         const int ee = min(ct, e + E);
         if (e < ee) {
-            int lo = 0, hi = nr - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s.poff[mid] <= e) lo = mid; else hi = mid - 1;
-            }
-            int q = lo;
+            int q = find_run(s.poff, nr, run_search_step(nr), e);
             while (e < ee) {
                 while (s.poff[q + 1] <= e) ++q;
                 const int stop = min(ee, s.poff[q + 1]);
