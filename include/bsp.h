@@ -48,7 +48,9 @@ typedef struct {
     int64_t* row_ptr; /* device, nrows+1 */
     int32_t* col_idx; /* device, nnz */
     double* values;   /* device, nnz */
-    int32_t owned;    /* 1: allocated by the library, released by bsp_csr_free */
+    int32_t owned;    /* 0: caller's arrays; 1: library-allocated (released by
+                         bsp_csr_free); 2: library-allocated, col_idx shares the
+                         values block (results of a multiply) */
 } bsp_csr;
 
 /* Host CSR (library- or caller-owned host memory). */

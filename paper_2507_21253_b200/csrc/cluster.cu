@@ -457,25 +457,25 @@ void build_cluster_device(bsp_handle h, const bsp_csr* A, int64_t ncl, int64_t* 
     const int g = grid_for(h, ncl * 32, 256);
     BSP_LAUNCH(h, build_cluster_kernel<0>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl, mptr,
                rows, ucount.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
-    DBuf<int64_t> ccp(h, ncl + 1);
+    DBuf<int64_t> ccp(h, ncl + 1, Pool::out);
     exclusive_scan_i64(h, ucount.p, ccp.p, ncl + 1);
     DBuf<int64_t> slots(h, ncl + 1);
-    DBuf<int32_t> sizes(h, ncl);
+    DBuf<int32_t> sizes(h, ncl, Pool::out);
     BSP_CUDA(cudaMemsetAsync(slots.p + ncl, 0, sizeof(int64_t), h->stream));
     BSP_LAUNCH(h, value_ptr_kernel, grid_for(h, ncl, 256), 256, 0, ucount.p, mptr, ncl, slots.p,
                sizes.p);
-    DBuf<int64_t> vptr(h, ncl + 1);
+    DBuf<int64_t> vptr(h, ncl + 1, Pool::out);
     exclusive_scan_i64(h, slots.p, vptr.p, ncl + 1);
     int64_t tot[2];
     d2h(h, &tot[0], ccp.p + ncl, 1);
     d2h(h, &tot[1], vptr.p + ncl, 1);
     sync(h);
     const int64_t ncolslots = tot[0], nslots = tot[1];
-    DBuf<int32_t> ocol(h, ncolslots);
-    DBuf<uint32_t> omask(h, ncolslots);
-    DBuf<double> oval(h, nslots);
+    DBuf<int32_t> ocol(h, ncolslots, Pool::out);
+    DBuf<uint32_t> omask(h, ncolslots, Pool::out);
+    DBuf<double> oval(h, nslots, Pool::out);
     const int64_t nwords = (nslots + 63) / 64;
-    DBuf<uint64_t> valid(h, nwords);
+    DBuf<uint64_t> valid(h, nwords, Pool::out);
     BSP_CUDA(cudaMemsetAsync(oval.p, 0, std::max<int64_t>(nslots, 1) * sizeof(double), h->stream));
     BSP_CUDA(cudaMemsetAsync(valid.p, 0, std::max<int64_t>(nwords, 1) * sizeof(uint64_t), h->stream));
     BSP_LAUNCH(h, build_cluster_kernel<1>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl, mptr,
@@ -499,9 +499,9 @@ void build_cluster_device(bsp_handle h, const bsp_csr* A, int64_t ncl, int64_t* 
     out->csr_col_idx = nullptr;
     out->csr_values = nullptr;
     if (keep_csr) {
-        DBuf<int64_t> rp(h, A->nrows + 1);
-        DBuf<int32_t> ci(h, A->nnz);
-        DBuf<double> v(h, A->nnz);
+        DBuf<int64_t> rp(h, A->nrows + 1, Pool::out);
+        DBuf<int32_t> ci(h, A->nnz, Pool::out);
+        DBuf<double> v(h, A->nnz, Pool::out);
         BSP_CUDA(cudaMemcpyAsync(rp.p, A->row_ptr, (A->nrows + 1) * sizeof(int64_t),
                                  cudaMemcpyDeviceToDevice, h->stream));
         BSP_CUDA(cudaMemcpyAsync(ci.p, A->col_idx, A->nnz * sizeof(int32_t),
@@ -523,11 +523,11 @@ void cluster_to_csr_device(bsp_handle h, const bsp_csr_cluster* m, bsp_csr* out)
     BSP_LAUNCH(h, cluster_to_csr_kernel<0>, g, 256, 0, m->cluster_sizes, m->member_ptr,
                m->cluster_col_ptr, m->col_idx, m->value_ptr, m->values, m->member_mask,
                m->row_map, m->nclusters, cnt.p, nullptr, nullptr, nullptr);
-    DBuf<int64_t> rp(h, n + 1);
+    DBuf<int64_t> rp(h, n + 1, Pool::out);
     exclusive_scan_i64(h, cnt.p, rp.p, n + 1);
     const int64_t nnz = read_scalar(h, rp.p + n);
-    DBuf<int32_t> ci(h, nnz);
-    DBuf<double> v(h, nnz);
+    DBuf<int32_t> ci(h, nnz, Pool::out);
+    DBuf<double> v(h, nnz, Pool::out);
     BSP_LAUNCH(h, cluster_to_csr_kernel<1>, g, 256, 0, m->cluster_sizes, m->member_ptr,
                m->cluster_col_ptr, m->col_idx, m->value_ptr, m->values, m->member_mask,
                m->row_map, m->nclusters, nullptr, rp.p, ci.p, v.p);
@@ -582,8 +582,8 @@ int bsp_csr_cluster_build(bsp_handle h, const bsp_csr* A, int64_t nclusters,
         for (int64_t i = 0; i < n; ++i)
             require(seen[i], "cluster assignment: row " + std::to_string(i) + " not covered");
         const int64_t total = nclusters > 0 ? cluster_ptr[nclusters] : 0;
-        DBuf<int64_t> mptr(h, nclusters + 1);
-        DBuf<int32_t> drows(h, total);
+        DBuf<int64_t> mptr(h, nclusters + 1, Pool::out);
+        DBuf<int32_t> drows(h, total, Pool::out);
         if (nclusters > 0) {
             h2d(h, mptr.p, cluster_ptr, nclusters + 1);
             h2d(h, drows.p, rows, total);
@@ -719,23 +719,23 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         }
         DBuf<int64_t> win_nnz;
         plan_symbolic(h, m, plan, row_nnz.p, win_nnz);
-        DBuf<int64_t> rp(h, n + 1);
+        DBuf<int64_t> rp(h, n + 1, Pool::out);
         exclusive_scan_i64(h, row_nnz.p, rp.p, n + 1);
         DBuf<int64_t> win_scan(h, plan.nwin + 1);
         if (plan.nwin > 0) exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
         const int64_t nnz = read_scalar(h, rp.p + n);
         h->stats.nnz_out = nnz;
-        DBuf<int32_t> ccol(h, nnz);
-        DBuf<double> cval(h, nnz);
-        run_cluster_classes<true>(h, cm, lists.p, off, cnt, cbits, nullptr, rp.p, ccol.p, cval.p);
-        plan_numeric(h, m, plan, rp.p, win_scan.p, ccol.p, cval.p);
+        ResultPayload pay(h, nnz);
+        run_cluster_classes<true>(h, cm, lists.p, off, cnt, cbits, nullptr, rp.p, pay.col_idx(),
+                                  pay.values());
+        plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values());
         C->nrows = n;
         C->ncols = B->ncols;
         C->nnz = nnz;
         C->row_ptr = rp.release();
-        C->col_idx = ccol.release();
-        C->values = cval.release();
-        C->owned = 1;
+        C->col_idx = pay.col_idx();
+        C->values = pay.block.release();
+        C->owned = 2;
         if (tmp_csr.owned) {
             dfree(h, tmp_csr.row_ptr);
             dfree(h, tmp_csr.col_idx);
@@ -744,8 +744,8 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         if (C_cluster) {
             // C's cluster form = build_csr_cluster(C, A's assignment)
             // (same sizes/row_map; union of members' output columns).
-            DBuf<int64_t> mptr(h, ncl + 1);
-            DBuf<int32_t> rows(h, n);
+            DBuf<int64_t> mptr(h, ncl + 1, Pool::out);
+            DBuf<int32_t> rows(h, n, Pool::out);
             BSP_CUDA(cudaMemcpyAsync(mptr.p, A->member_ptr, (ncl + 1) * sizeof(int64_t),
                                      cudaMemcpyDeviceToDevice, h->stream));
             BSP_CUDA(cudaMemcpyAsync(rows.p, A->row_map, n * sizeof(int32_t),

@@ -153,6 +153,18 @@ __global__ void sort_rows_kernel(const int64_t* __restrict__ rp, int64_t nrows,
 
 }  // namespace
 
+size_t available_bytes(bsp_handle h) {
+    size_t free_b = 0, total_b = 0;
+    BSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    for (cudaMemPool_t pool : {h->scratch_pool, h->out_pool}) {
+        uint64_t reserved = 0, used = 0;
+        BSP_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+        BSP_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+        free_b += static_cast<size_t>(reserved - used);
+    }
+    return free_b;
+}
+
 }  // namespace bsp
 
 using namespace bsp;
@@ -176,10 +188,15 @@ int bsp_create(int device, bsp_handle* out) {
         h->sm_count = prop.multiProcessorCount;
         BSP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         h->own_stream = true;
-        cudaMemPool_t pool;
-        BSP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-        uint64_t thr = UINT64_MAX;
-        BSP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        for (cudaMemPool_t* pool : {&h->scratch_pool, &h->out_pool}) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = device;
+            BSP_CUDA(cudaMemPoolCreate(pool, &props));
+            uint64_t thr = UINT64_MAX;  // keep freed blocks mapped for reuse
+            BSP_CUDA(cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         *out = h;
     });
 }
@@ -189,6 +206,10 @@ int bsp_destroy(bsp_handle h) {
         if (!h) return;
         cudaStreamSynchronize(h->stream);
         if (h->own_stream) cudaStreamDestroy(h->stream);
+        // pools with live allocations (results still held by the caller) are
+        // released by the driver once those are freed
+        if (h->scratch_pool) cudaMemPoolDestroy(h->scratch_pool);
+        if (h->out_pool) cudaMemPoolDestroy(h->out_pool);
         delete h;
     });
 }
@@ -274,9 +295,9 @@ int bsp_csr_upload(bsp_handle h, int64_t nrows, int64_t ncols, const int64_t* ro
         BSP_CUDA(cudaSetDevice(h->device));
         const int64_t nnz = row_ptr[nrows];
         require(row_ptr[0] == 0 && nnz >= 0, "bsp_csr_upload: bad row_ptr");
-        DBuf<int64_t> rp(h, nrows + 1);
-        DBuf<int32_t> ci(h, nnz);
-        DBuf<double> v(h, nnz);
+        DBuf<int64_t> rp(h, nrows + 1, Pool::out);
+        DBuf<int32_t> ci(h, nnz, Pool::out);
+        DBuf<double> v(h, nnz, Pool::out);
         h2d(h, rp.p, row_ptr, nrows + 1);
         h2d(h, ci.p, col_idx, nnz);
         if (values) {
@@ -359,7 +380,7 @@ int bsp_csr_free(bsp_handle h, bsp_csr* m) {
         if (!m) return;
         if (m->owned) {
             dfree(h, m->row_ptr);
-            dfree(h, m->col_idx);
+            if (m->owned != 2) dfree(h, m->col_idx);  // 2: col_idx inside the values block
             dfree(h, m->values);
         }
         m->row_ptr = nullptr;
@@ -388,13 +409,13 @@ int bsp_transpose(bsp_handle h, const bsp_csr* A, bsp_csr* out) {
         const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(nnz, 1), 256),
                                                             h->sm_count * 16));
         BSP_LAUNCH(h, col_count_kernel, grid, 256, 0, A->col_idx, nnz, cnt.p);
-        DBuf<int64_t> rp(h, n + 1);
+        DBuf<int64_t> rp(h, n + 1, Pool::out);
         exclusive_scan_i32_to_i64(h, cnt.p, rp.p, n + 1);
         DBuf<int64_t> cursor(h, n + 1);
         BSP_CUDA(cudaMemcpyAsync(cursor.p, rp.p, (n + 1) * sizeof(int64_t),
                                  cudaMemcpyDeviceToDevice, h->stream));
-        DBuf<int32_t> tc(h, nnz);
-        DBuf<double> tv(h, nnz);
+        DBuf<int32_t> tc(h, nnz, Pool::out);
+        DBuf<double> tv(h, nnz, Pool::out);
         const int rgrid = static_cast<int>(
             std::min<int64_t>(div_up(std::max<int64_t>(A->nrows, 1), 256), h->sm_count * 16));
         BSP_LAUNCH(h, transpose_scatter_kernel, rgrid, 256, 0, A->row_ptr, A->col_idx, A->values,

@@ -28,6 +28,12 @@ struct bsp_handle_s {
     bool prof = false;
     std::vector<bsp_prof_rec> prof_recs;  // recorded launches (events owned)
     std::vector<cudaEvent_t> prof_pool;   // recycled events
+    // Stream-ordered pools: plan/scratch buffers and arrays handed to the
+    // caller (results, uploads) live apart, so scratch never splits the block
+    // a freed result leaves behind and the next result of the same size
+    // reuses it without remapping (cfg5: C is 138 GB of the 178 GB HBM).
+    cudaMemPool_t scratch_pool = nullptr;
+    cudaMemPool_t out_pool = nullptr;
 };
 
 namespace bsp {
@@ -66,19 +72,26 @@ void trace_launch(bsp_handle h, const char* name, long long grid);
 int prof_begin(bsp_handle h);
 void prof_end(bsp_handle h, int slot, const char* name);
 
-// Stream-ordered device allocation from the device's default memory pool
-// (release threshold raised at handle creation so repeated calls reuse it).
+// Stream-ordered device allocation from one of the handle's pools.
+enum class Pool { scratch, out };
+
 template <typename T>
-T* dalloc(bsp_handle h, int64_t n) {
+T* dalloc(bsp_handle h, int64_t n, Pool pool = Pool::scratch) {
     void* p = nullptr;
     const size_t bytes = static_cast<size_t>(n > 0 ? n : 1) * sizeof(T);
-    cuda_check(cudaMallocAsync(&p, bytes, h->stream), "cudaMallocAsync");
+    cuda_check(cudaMallocFromPoolAsync(&p, bytes, pool == Pool::out ? h->out_pool : h->scratch_pool,
+                                       h->stream),
+               "cudaMallocFromPoolAsync");
     return static_cast<T*>(p);
 }
 
 inline void dfree(bsp_handle h, void* p) {
     if (p) cudaFreeAsync(p, h->stream);
 }
+
+// Device bytes available to a new allocation: free HBM plus what the
+// handle's pools hold cached but unused.
+size_t available_bytes(bsp_handle h);
 
 // RAII device buffer bound to a handle's stream.
 template <typename T>
@@ -87,7 +100,8 @@ struct DBuf {
     T* p = nullptr;
     int64_t n = 0;
     DBuf() = default;
-    DBuf(bsp_handle hh, int64_t nn) : h(hh), p(dalloc<T>(hh, nn)), n(nn) {}
+    DBuf(bsp_handle hh, int64_t nn, Pool pool = Pool::scratch)
+        : h(hh), p(dalloc<T>(hh, nn, pool)), n(nn) {}
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     DBuf(DBuf&& o) noexcept : h(o.h), p(o.p), n(o.n) { o.p = nullptr; }
@@ -152,5 +166,15 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
                       int64_t* row_nnz_out /*nullable, device*/);
 
 inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// A multiply result's payload: nnz values followed by nnz column indices in
+// one output-pool block (bsp_csr.owned == 2).
+struct ResultPayload {
+    DBuf<double> block;
+    int64_t nnz = 0;
+    ResultPayload(bsp_handle h, int64_t n) : block(h, n + (n + 1) / 2, Pool::out), nnz(n) {}
+    double* values() const { return block.p; }
+    int32_t* col_idx() const { return reinterpret_cast<int32_t*>(block.p + nnz); }
+};
 
 }  // namespace bsp

@@ -27,7 +27,10 @@ __device__ __forceinline__ int PADI(int i) { return i + (i >> 5); }
 template <int T, int CAPM>
 struct MergeShared {
     static constexpr int NP = CAPM + CAPM / 32 + 1;
-    using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, 6>;
+    // radix digit width: CUB's rank storage is T x 2^RB / 2 words, so 512-thread
+    // tiles use 5-bit digits to keep it at 32 KB
+    static constexpr int RB = T >= 512 ? 5 : 6;
+    using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, RB>;
     // buffer 0 (also the radix-sort input/output)
     uint32_t key0[NP];
     uint16_t idx0[NP];
@@ -352,7 +355,8 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     // pad key = 2^bits - 1 >= every key (<= width-1); pads sit after `total`
     // and the sort is stable, so real entries keep the first `total` slots.
     const int bits = bit_length(width > 1 ? width - 1 : 1);
-    const int passes = (bits + 5) / 6;
+    constexpr int RB = MergeShared<T, CAPM>::RB;
+    const int passes = (bits + RB - 1) / RB;
     if (levels > passes + 1) {  // measured: cfg4 (5 levels vs 4 passes) prefers merge
         radix_sort_tile<T, CAPM>(s, total, bits);
         return 0;

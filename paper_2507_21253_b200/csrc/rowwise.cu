@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(T) esc_tile_kernel(Mats m, const int32_t* __re
 // K3': merge-based exact numeric tile and hash-count symbolic tile
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
-__global__ void __launch_bounds__(T) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(T, T >= 256 ? 2 : 4) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
                                                       const Window* __restrict__ wins, OutCtx out) {
     using S = MergeShared<T, CAPM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -836,15 +836,21 @@ void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, con
     if (NUMERIC) {
         using S = MergeShared<T, CAPM>;
         auto k = esc_merge_kernel<T, CAPM>;
-        static const std::string nm = "esc_merge<" + std::to_string(T) + "," +
-                                      std::to_string(CAPM) + (wins ? ",win>" : ">");
+        static const std::string nm_row = "esc_merge<" + std::to_string(T) + "," +
+                                          std::to_string(CAPM) + ">";
+        static const std::string nm_win = "esc_merge<" + std::to_string(T) + "," +
+                                          std::to_string(CAPM) + ",win>";
+        const std::string& nm = wins ? nm_win : nm_row;
         set_smem(k, sizeof(S));
         BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
     } else {
         using S = HashShared<T, CAPM>;
         auto k = hash_count_kernel<T, CAPM>;
-        static const std::string nm = "hash_count<" + std::to_string(T) + "," +
-                                      std::to_string(CAPM) + (wins ? ",win>" : ">");
+        static const std::string nm_row = "hash_count<" + std::to_string(T) + "," +
+                                          std::to_string(CAPM) + ">";
+        static const std::string nm_win = "hash_count<" + std::to_string(T) + "," +
+                                          std::to_string(CAPM) + ",win>";
+        const std::string& nm = wins ? nm_win : nm_row;
         set_smem(k, sizeof(S));
         BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
     }
@@ -997,10 +1003,9 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         plan.nwin = hv[0];
         // Start-table budget: <= 2^30 entries (4 GB) and <= 1/8 of free HBM;
         // the rows in scan order that fit get a table.
-        size_t free_b = 0, total_b = 0;
-        BSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
         const int64_t budget = std::min<int64_t>(
-            {hv[1], int64_t{1} << 30, static_cast<int64_t>(free_b / (8 * sizeof(int32_t)))});
+            {hv[1], int64_t{1} << 30,
+             static_cast<int64_t>(available_bytes(h) / (8 * sizeof(int32_t)))});
         const bool use_starts = budget > 0;
         if (use_starts) plan.starts = DBuf<int32_t>(h, budget);
         plan.wins = DBuf<Window>(h, plan.nwin);
@@ -1058,7 +1063,10 @@ void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCt
     launch_heavy<NUMERIC>(h, m, plan.hcur.p, plan.nhcur, out);
     for (int c = NCLS - 2; c >= 1; --c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
-    launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
+    if (NUMERIC && std::getenv("BSP_T512"))
+        launch_tile<512, 4096, true>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
+    else
+        launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
     launch_tile<128, 2048, NUMERIC>(h, m, plan.sparse_ids.p + plan.nsparse_large,
                                     plan.nsparse - plan.nsparse_large, plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
@@ -1110,22 +1118,21 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     if (row_nnz_out)
         BSP_CUDA(cudaMemcpyAsync(row_nnz_out, crp.p, n * sizeof(int64_t),
                                  cudaMemcpyDeviceToDevice, h->stream));
-    DBuf<int64_t> rp(h, n + 1);
+    DBuf<int64_t> rp(h, n + 1, Pool::out);
     exclusive_scan_i64(h, crp.p, rp.p, n + 1);
     DBuf<int64_t> win_scan(h, plan.nwin + 1);
     if (plan.nwin > 0) exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
     const int64_t nnz = read_scalar(h, rp.p + n);
     h->stats.nnz_out = nnz;
-    DBuf<int32_t> ccol(h, nnz);
-    DBuf<double> cval(h, nnz);
-    plan_numeric(h, m, plan, rp.p, win_scan.p, ccol.p, cval.p);
+    ResultPayload pay(h, nnz);
+    plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values());
     C->nrows = n;
     C->ncols = B->ncols;
     C->nnz = nnz;
     C->row_ptr = rp.release();
-    C->col_idx = ccol.release();
-    C->values = cval.release();
-    C->owned = 1;
+    C->col_idx = pay.col_idx();
+    C->values = pay.block.release();
+    C->owned = 2;
 }
 
 }  // namespace bsp
