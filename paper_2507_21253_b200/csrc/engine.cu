@@ -153,6 +153,31 @@ __global__ void sort_rows_kernel(const int64_t* __restrict__ rp, int64_t nrows,
 
 }  // namespace
 
+namespace {
+__global__ void readback_kernel(const unsigned char* __restrict__ src,
+                                unsigned char* __restrict__ dst, size_t bytes) {
+    const bool w4 = ((reinterpret_cast<uintptr_t>(src) | bytes) & 3) == 0;
+    if (w4) {
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+        uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+        for (size_t i = threadIdx.x; i < bytes / 4; i += blockDim.x) d4[i] = s4[i];
+    } else {
+        for (size_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+    }
+}
+}  // namespace
+
+void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes) {
+    if (!h->rb_host) {
+        BSP_CUDA(cudaHostAlloc(&h->rb_host, kReadbackBytes, cudaHostAllocMapped));
+        BSP_CUDA(cudaHostGetDevicePointer(&h->rb_dev, h->rb_host, 0));
+    }
+    BSP_LAUNCH(h, readback_kernel, 1, 256, 0, static_cast<const unsigned char*>(src),
+               static_cast<unsigned char*>(h->rb_dev), bytes);
+    BSP_CUDA(cudaStreamSynchronize(h->stream));
+    std::memcpy(dst, h->rb_host, bytes);
+}
+
 size_t available_bytes(bsp_handle h) {
     size_t free_b = 0, total_b = 0;
     BSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -196,6 +221,11 @@ int bsp_create(int device, bsp_handle* out) {
             BSP_CUDA(cudaMemPoolCreate(pool, &props));
             uint64_t thr = UINT64_MAX;  // keep freed blocks mapped for reuse
             BSP_CUDA(cudaMemPoolSetAttribute(*pool, cudaMemPoolAttrReleaseThreshold, &thr));
+            // Never make an allocation wait on another stream's pending free:
+            // a result freed on a copy stream after its download must not
+            // serialise the next multiply behind that download.
+            int no = 0;
+            BSP_CUDA(cudaMemPoolSetAttribute(*pool, cudaMemPoolReuseAllowInternalDependencies, &no));
         }
         *out = h;
     });
@@ -208,6 +238,7 @@ int bsp_destroy(bsp_handle h) {
         if (h->own_stream) cudaStreamDestroy(h->stream);
         // pools with live allocations (results still held by the caller) are
         // released by the driver once those are freed
+        if (h->rb_host) cudaFreeHost(h->rb_host);
         if (h->scratch_pool) cudaMemPoolDestroy(h->scratch_pool);
         if (h->out_pool) cudaMemPoolDestroy(h->out_pool);
         delete h;

@@ -34,6 +34,9 @@ struct bsp_handle_s {
     // reuses it without remapping (cfg5: C is 138 GB of the 178 GB HBM).
     cudaMemPool_t scratch_pool = nullptr;
     cudaMemPool_t out_pool = nullptr;
+    // Mapped pinned buffer for small synchronous readbacks (see d2h).
+    void* rb_host = nullptr;
+    void* rb_dev = nullptr;
 };
 
 namespace bsp {
@@ -125,10 +128,22 @@ struct DBuf {
     }
 };
 
+// Small device -> host reads (plan counters, scalars) are written by a
+// one-block kernel into mapped pinned memory and complete synchronously:
+// they never queue on a copy engine behind a multi-GB result download
+// running on another stream.  Larger reads are ordinary async copies.
+constexpr size_t kReadbackBytes = 64 << 10;
+void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes);
+
 template <typename T>
 void d2h(bsp_handle h, T* dst, const T* src, int64_t n) {
     if (n <= 0) return;
-    BSP_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, h->stream));
+    const size_t bytes = static_cast<size_t>(n) * sizeof(T);
+    if (bytes <= kReadbackBytes) {
+        small_readback(h, dst, src, bytes);
+        return;
+    }
+    BSP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
 }
 template <typename T>
 void h2d(bsp_handle h, T* dst, const T* src, int64_t n) {
