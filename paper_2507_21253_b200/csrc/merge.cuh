@@ -364,67 +364,55 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     return merge_runs<T, CAPM>(s, total);
 }
 
-// After merge_runs: sum every run of equal columns left to right from 0.0
-// (ascending k), stage (column + kofs, sum) compactly in smem and write them
-// coalesced to ccol/cval.  Returns the number of distinct columns.
-template <int T, int CAPM>
-__device__ __forceinline__ int reduce_stage(MergeShared<T, CAPM>& s, int b, int total,
-                                            uint32_t kofs) {
-    const int tid = threadIdx.x;
-    const uint32_t* K = s.key(b);
-    const uint16_t* X = s.idx(b);
-    constexpr int E_MAX = (CAPM + T - 1) / T;
-    const int E = (total + T - 1) / T;
-    const int o0 = min(total, tid * E), o1 = min(total, o0 + E);
-    int nh = 0;
-    for (int o = o0; o < o1; ++o) nh += (o == 0 || K[PADI(o)] != K[PADI(o - 1)]);
-    int hoff, tile_cnt;
-    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
-    double res[E_MAX];
-    bool hd[E_MAX];
-#pragma unroll
-    for (int q = 0; q < E_MAX; ++q) {
-        const int o = o0 + q;
-        hd[q] = o < o1 && (o == 0 || K[PADI(o)] != K[PADI(o - 1)]);
-        res[q] = 0.0;
-        if (hd[q]) {
-            const uint32_t key = K[PADI(o)];
-            double acc = 0.0;
-            int e = o;
-            do {
-                acc = __dadd_rn(acc, s.val[X[PADI(e)]]);
-                ++e;
-            } while (e < total && K[PADI(e)] == key);
-            res[q] = acc;
-        }
-    }
-    uint32_t kk[E_MAX];
-#pragma unroll
-    for (int q = 0; q < E_MAX; ++q) kk[q] = (o0 + q < o1) ? K[PADI(o0 + q)] : 0u;
-    __syncthreads();
-    uint32_t* KO = s.key(b ^ 1);
-    int r = hoff;
-#pragma unroll
-    for (int q = 0; q < E_MAX; ++q) {
-        if (hd[q]) {
-            KO[PADI(r)] = kk[q] + kofs;
-            s.val[r] = res[q];
-            ++r;
-        }
-    }
-    __syncthreads();
-    return tile_cnt;  // staged: keys in s.key(b ^ 1) (padded), sums in s.val
-}
-
+// After the sort: sum every run of equal columns left to right from 0.0
+// (ascending k — the reference's order, spgemm.hpp:92-97) and write
+// (column + kofs, sum) to ccol/cval.  Element-strided: lane l of warp w owns
+// sorted element o = r*T + 32w + l of row r, so head detection reads smem
+// conflict-free, a head's output rank is a ballot prefix plus a scan over the
+// (row, warp) head counts, and consecutive lanes store consecutive entries of
+// C (coalesced, no staging).  Returns the number of distinct columns.
 template <int T, int CAPM>
 __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, int total,
                                                 uint32_t kofs, int32_t* __restrict__ ccol,
                                                 double* __restrict__ cval) {
-    const int tile_cnt = reduce_stage<T, CAPM>(s, b, total, kofs);
-    const uint32_t* KO = s.key(b ^ 1);
-    for (int e = threadIdx.x; e < tile_cnt; e += T) {
-        ccol[e] = static_cast<int32_t>(KO[PADI(e)]);
-        cval[e] = s.val[e];
+    constexpr int NW = T / 32;
+    constexpr int R = (CAPM + T - 1) / T;
+    static_assert(R * NW <= T && R * NW <= CAPM / 2, "row/warp counters");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t* K = s.key(b);
+    const uint16_t* X = s.idx(b);
+    int* cnt = reinterpret_cast<int*>(s.hist);  // [row][warp] head counts, then offsets
+    const int nrows = (total + T - 1) / T;
+    unsigned hm[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int o = r * T + threadIdx.x;
+        const bool h = o < total && (o == 0 || K[PADI(o)] != K[PADI(o - 1)]);
+        hm[r] = __ballot_sync(0xffffffffu, h);
+        if (lane == 0 && r < nrows) cnt[r * NW + warp] = __popc(hm[r]);
+    }
+    __syncthreads();
+    const int v = threadIdx.x < nrows * NW ? cnt[threadIdx.x] : 0;
+    int pre, tile_cnt;
+    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(v, pre, tile_cnt);
+    __syncthreads();
+    if (threadIdx.x < nrows * NW) cnt[threadIdx.x] = pre;
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (!((hm[r] >> lane) & 1u)) continue;
+        const int o = r * T + threadIdx.x;
+        const int rank = cnt[r * NW + warp] + __popc(hm[r] & below);
+        const uint32_t key = K[PADI(o)];
+        double acc = 0.0;
+        int e = o;
+        do {
+            acc = __dadd_rn(acc, s.val[X[PADI(e)]]);
+            ++e;
+        } while (e < total && K[PADI(e)] == key);
+        ccol[rank] = static_cast<int32_t>(key + kofs);
+        cval[rank] = acc;
     }
     __syncthreads();
     return tile_cnt;
