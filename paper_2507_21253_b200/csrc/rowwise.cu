@@ -110,7 +110,7 @@ __global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64
 // K2: heavy-row planner
 // ---------------------------------------------------------------------------
 constexpr int PLAN_T = 256;
-constexpr int PLAN_U = 4;  // B-row chunks of 32 loaded ahead per warp
+constexpr int PLAN_U = 8;  // B-row chunks of 32 loaded ahead per warp
 constexpr uint32_t DENSE_BIT = 0x80000000u;
 
 struct PlanCountShared {
@@ -554,9 +554,10 @@ __global__ void __launch_bounds__(T, T >= 256 ? 2 : 4) esc_merge_kernel(Mats m, 
                               out.cval + base);
 }
 
-template <int T, int CAPM>
+template <int T, int CAPM, bool STAGED = true>
 struct HashShared {
     int32_t table[2 * CAPM];
+    int32_t stage[STAGED ? CAPM : 1];  // gathered columns of the current chunk
     typename cub::BlockReduce<int32_t, T>::TempStorage red;
     typename cub::BlockScan<int32_t, T>::TempStorage scan;
     int64_t pstart[T];
@@ -564,11 +565,13 @@ struct HashShared {
 };
 
 // Distinct output columns of (row, [c0,c1)) with <= CAPM products.
-template <int T, int CAPM>
+// STAGED: the chunk's columns are first gathered into smem with cp.async
+// (warp-contiguous, all loads in flight), then hashed from smem.
+template <int T, int CAPM, bool STAGED>
 __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __restrict__ ids,
                                                        const Window* __restrict__ wins,
                                                        OutCtx out) {
-    using S = HashShared<T, CAPM>;
+    using S = HashShared<T, CAPM, STAGED>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S& s = *reinterpret_cast<S*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -619,29 +622,40 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         const int nr = agg >> 16, ct = agg & 0xffff;
         if (tid == 0) s.poff[nr] = ct;
         __syncthreads();
-        // each thread inserts a contiguous range of the chunk's products
-        // (measured faster here than warp-strided slices: no per-element walk)
-        const int E = (ct + T - 1) / T;
-        int e = min(ct, tid * E);
-        const int ee = min(ct, e + E);
-        if (e < ee) {
-            int q = find_run(s.poff, nr, run_search_step(nr), e);
-            while (e < ee) {
+        auto insert = [&](int32_t col) {
+            uint32_t hsl = col_hash(static_cast<uint32_t>(col), LG);
+            for (;;) {
+                const int32_t prev = atomicCAS(&s.table[hsl], -1, col);
+                if (prev == -1) {
+                    ++cnt;
+                    break;
+                }
+                if (prev == col) break;
+                hsl = (hsl + 1) & (2 * CAPM - 1);
+            }
+        };
+        if constexpr (STAGED) {
+            int e, we, q;
+            warp_slice_begin(s.poff, nr, ct, NW, e, we, q);
+            for (; e < we; e += 32) {
                 while (s.poff[q + 1] <= e) ++q;
-                const int stop = min(ee, s.poff[q + 1]);
-                const int64_t base = s.pstart[q] - s.poff[q];
-                for (; e < stop; ++e) {
-                    const int32_t col = __ldg(m.bcol + base + e);
-                    uint32_t hsl = col_hash(static_cast<uint32_t>(col), LG);
-                    for (;;) {
-                        const int32_t prev = atomicCAS(&s.table[hsl], -1, col);
-                        if (prev == -1) {
-                            ++cnt;
-                            break;
-                        }
-                        if (prev == col) break;
-                        hsl = (hsl + 1) & (2 * CAPM - 1);
-                    }
+                cp_async4(&s.stage[e], m.bcol + s.pstart[q] + (e - s.poff[q]));
+            }
+            cp_async_wait_all();
+            __syncthreads();
+            for (int e2 = tid; e2 < ct; e2 += T) insert(s.stage[e2]);
+        } else {
+            // each thread inserts a contiguous range of the chunk's products
+            const int E = (ct + T - 1) / T;
+            int e = min(ct, tid * E);
+            const int ee = min(ct, e + E);
+            if (e < ee) {
+                int q = find_run(s.poff, nr, run_search_step(nr), e);
+                while (e < ee) {
+                    while (s.poff[q + 1] <= e) ++q;
+                    const int stop = min(ee, s.poff[q + 1]);
+                    const int64_t base = s.pstart[q] - s.poff[q];
+                    for (; e < stop; ++e) insert(__ldg(m.bcol + base + e));
                 }
             }
         }
@@ -844,15 +858,28 @@ void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, con
         set_smem(k, sizeof(S));
         BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
     } else {
-        using S = HashShared<T, CAPM>;
-        auto k = hash_count_kernel<T, CAPM>;
+        static const bool staged = [] {
+            const char* e = std::getenv("BSP_HASH_STAGE");
+            return !(e && e[0] == '0');
+        }();
         static const std::string nm_row = "hash_count<" + std::to_string(T) + "," +
                                           std::to_string(CAPM) + ">";
         static const std::string nm_win = "hash_count<" + std::to_string(T) + "," +
                                           std::to_string(CAPM) + ",win>";
         const std::string& nm = wins ? nm_win : nm_row;
-        set_smem(k, sizeof(S));
-        BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
+        if (staged) {
+            using S = HashShared<T, CAPM, true>;
+            auto k = hash_count_kernel<T, CAPM, true>;
+            set_smem(k, sizeof(S));
+            BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins,
+                          out);
+        } else {
+            using S = HashShared<T, CAPM, false>;
+            auto k = hash_count_kernel<T, CAPM, false>;
+            set_smem(k, sizeof(S));
+            BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins,
+                          out);
+        }
     }
 }
 
