@@ -223,6 +223,14 @@ int bsp_rowwise_access_stats(bsp_handle h, const bsp_csr* A, const bsp_csr* B,
 /* ------------------------------------------------------------------ */
 /* Device transpose (rows of the result sorted).  reference: transpose, csr.hpp:115-135 */
 int bsp_transpose(bsp_handle h, const bsp_csr* A, bsp_csr* out);
+/* Tall-skinny frontier operands by batched BFS on the device.  reference:
+ * generate_frontiers, frontier.hpp:20-77 (identical matrices: sources = sorted
+ * prefix of reorder_random(n, seed), frontier t = {(v, s): depth_s(v) == t}).
+ * `out` must hold num_frontiers entries; *count receives how many were made
+ * (fewer when every search exhausts its component).  Each is n x min(batch, n),
+ * library-owned (bsp_csr_free). */
+int bsp_generate_frontiers(bsp_handle h, const bsp_csr* A, int64_t num_frontiers, int64_t batch,
+                           uint64_t seed, bsp_csr* out, int64_t* count);
 /* reference: spgemm_topk, spgemm.hpp:144-206 (element-for-element identical
  * output list, scores bitwise).  Results in library-malloc'ed host memory
  * (free with bsp_host_free_plain). a/a_t patterns only (values ignored). */

@@ -122,6 +122,8 @@ def ref() -> C.CDLL:
         l.ref_permute_symmetric.argtypes = [i64, i64, vp, vp, vp, vp, P(P(i64)), P(P(i32)),
                                             P(P(dbl))]
         l.ref_jaccard.argtypes = [i64, i64, vp, vp, i64, i64, P(dbl)]
+        l.ref_generate_frontiers.argtypes = [i64, i64, vp, vp, i64, i64, u64, P(i64), P(i64),
+                                             P(P(i64)), P(P(i64)), P(P(i32))]
         l.ref_free.argtypes = [vp]
         _ref = l
     return _ref
@@ -375,3 +377,103 @@ def ref_jaccard(a, i, j) -> float:
     out = dbl()
     _ref_check(ref().ref_jaccard(a.nrows, a.ncols, _p(arp), _p(aci), i, j, C.byref(out)))
     return float(out.value)
+
+
+def ref_generate_frontiers(a, num_frontiers: int, batch: int, seed: int) -> list:
+    """The reference's generate_frontiers (frontier.hpp:20-77) on host CSR `a`."""
+    arp, aci, _ = _csr_args(a)
+    cnt, width = i64(), i64()
+    rps, coff, cis = P(i64)(), P(i64)(), P(i32)()
+    _ref_check(ref().ref_generate_frontiers(a.nrows, a.ncols, _p(arp), _p(aci), num_frontiers,
+                                            batch, seed, C.byref(cnt), C.byref(width),
+                                            C.byref(rps), C.byref(coff), C.byref(cis)))
+    f = ref().ref_free
+    n, k = a.nrows, cnt.value
+    rp = _arr(rps, k * (n + 1), np.int64, f).reshape(k, n + 1) if k else np.zeros((0, n + 1), np.int64)
+    off = _arr(coff, k + 1, np.int64, f)
+    ci = _arr(cis, int(off[-1]), np.int32, f)
+    return [Csr(n, width.value, rp[t].copy(), ci[off[t]:off[t + 1]].copy(),
+                np.ones(off[t + 1] - off[t], np.float64)) for t in range(k)]
+
+
+# ---------------------------------------------------------------------------
+# Frontier generation (restatement of frontier.hpp:20-77, pure Python: small
+# inputs only).  std::mt19937_64 per the C++ standard [rand.eng.mers] and the
+# reference's multiply-shift `bounded` (types.hpp:36-39).
+# ---------------------------------------------------------------------------
+_M64 = (1 << 64) - 1
+
+
+class _MT19937_64:
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & _M64
+        for i in range(1, 312):
+            prev = self.mt[i - 1]
+            self.mt[i] = (6364136223846793005 * (prev ^ (prev >> 62)) + i) & _M64
+        self.i = 312
+
+    def __call__(self) -> int:
+        if self.i >= 312:
+            mt = self.mt
+            for k in range(312):
+                x = (mt[k] & 0xFFFFFFFF80000000) | (mt[(k + 1) % 312] & 0x7FFFFFFF)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                mt[k] = mt[(k + 156) % 312] ^ xa
+            self.i = 0
+        x = self.mt[self.i]
+        self.i += 1
+        x ^= (x >> 29) & 0x5555555555555555
+        x ^= (x << 17) & 0x71D67FFFEDA60000
+        x ^= (x << 37) & 0xFFF7EEE000000000
+        x ^= x >> 43
+        return x & _M64
+
+
+def random_permutation(n: int, seed: int) -> np.ndarray:
+    """reorder_random (reorder.hpp:20-30): Fisher-Yates, j = (rng() * (i+1)) >> 64."""
+    rng = _MT19937_64(seed)
+    perm = list(range(n))
+    for i in range(n - 1, 0, -1):
+        j = (rng() * (i + 1)) >> 64
+        perm[i], perm[j] = perm[j], perm[i]
+    return np.array(perm, np.int32)
+
+
+def generate_frontiers(a, num_frontiers: int, batch: int, seed: int) -> list:
+    """frontier.hpp:20-77: `width = min(batch, n)` sorted sources from the first
+    entries of a seeded shuffle (:37-46); one BFS per source over a's rows as
+    out-neighbour lists (:48-63); frontier t = {(v, s): depth_s(v) == t}
+    (:65-76), at most num_frontiers of them, fewer when every search ends."""
+    if a.nrows != a.ncols or num_frontiers < 1 or batch < 1:
+        raise ValueError("generate_frontiers: contract")
+    n = a.nrows
+    if n == 0:
+        return []
+    width = min(batch, n)
+    sources = np.sort(random_permutation(n, seed)[:width])
+    rp, ci = np.asarray(a.row_ptr, np.int64), np.asarray(a.col_idx, np.int32)
+    depth = np.full((width, n), -1, np.int64)
+    max_depth = 0
+    for s in range(width):
+        d = depth[s]
+        q = [int(sources[s])]
+        d[q[0]] = 0
+        h = 0
+        while h < len(q):
+            v = q[h]
+            h += 1
+            for w in ci[rp[v]:rp[v + 1]]:
+                if d[w] < 0:
+                    d[w] = d[v] + 1
+                    q.append(int(w))
+        max_depth = max(max_depth, int(d[q[-1]]))
+    out = []
+    for t in range(min(num_frontiers, max_depth + 1)):
+        vv, ss = np.nonzero(depth.T == t)  # row-major over (v, s): rows sorted, cols ascending
+        cnt = np.bincount(vv, minlength=n)
+        rpt = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+        out.append(Csr(n, width, rpt, ss.astype(np.int32), np.ones(len(ss), np.float64)))
+    return out

@@ -265,4 +265,28 @@ int ref_jaccard(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* 
     });
 }
 
+// generate_frontiers (frontier.hpp:20-77): the t-th frontier's row_ptr is
+// rps[t*(n+1) .. ], its columns cis[coff[t] .. coff[t+1]).
+int ref_generate_frontiers(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
+                           int64_t num_frontiers, int64_t batch, uint64_t seed, int64_t* count,
+                           int64_t* width, int64_t** rps, int64_t** coff, int32_t** cis) {
+    return guard([&] {
+        const CsrMatrix a = make(nrows, ncols, rp, ci, nullptr);
+        const std::vector<CsrMatrix> fs = generate_frontiers(
+            a, static_cast<index_t>(num_frontiers), static_cast<index_t>(batch), seed);
+        *count = static_cast<int64_t>(fs.size());
+        *width = fs.empty() ? 0 : fs[0].ncols;
+        std::vector<int64_t> r, o(1, 0);
+        std::vector<int32_t> c;
+        for (const CsrMatrix& f : fs) {
+            for (index_t x : f.row_ptr) r.push_back(x);
+            c.insert(c.end(), f.col_idx.begin(), f.col_idx.end());
+            o.push_back(static_cast<int64_t>(c.size()));
+        }
+        *rps = dup(r);
+        *coff = dup(o);
+        *cis = dup(c);
+    });
+}
+
 }  // extern "C"

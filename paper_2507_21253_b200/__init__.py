@@ -32,7 +32,8 @@ __all__ = [
     "build_csr_cluster", "cluster_to_csr", "spgemm_clusterwise", "spgemm_clusterwise_instrumented",
     "rowwise_access_stats", "fixed_length_clusters", "variable_length_clusters",
     "hierarchical_clusters", "merge_candidates", "assignment_to_permutation", "reorder_random",
-    "reorder_degree", "reorder_rcm", "bandwidth", "transpose", "binarize", "permute_symmetric",
+    "reorder_degree", "reorder_rcm", "bandwidth", "transpose", "generate_frontiers", "binarize",
+    "permute_symmetric",
     "permute_rows", "coo_to_csr", "csr_equal_canonical", "gen_er", "gen_hidden_clusters",
     "gen_rmat", "gen_stencil27", "make_config", "CONFIGS",
 ]
@@ -521,6 +522,16 @@ class Engine:
         _check(self.lib.bsp_transpose(self.h, C.byref(A.s), C.byref(s)))
         return DeviceCsr(self, s)
 
+    def generate_frontiers(self, A: DeviceCsr, num_frontiers: int = 10, batch: int = 64,
+                           seed: int = 0) -> list:
+        """Frontier operands of the tall-skinny workload (frontier.hpp:20-77) as
+        device CSRs, built by a batched BFS on the device."""
+        arr = (L.bsp_csr * max(int(num_frontiers), 1))()
+        cnt = C.c_int64()
+        _check(self.lib.bsp_generate_frontiers(self.h, C.byref(A.s), num_frontiers, batch, seed,
+                                               arr, C.byref(cnt)))
+        return [DeviceCsr(self, arr[t]) for t in range(cnt.value)]
+
     # -- cluster-wise --------------------------------------------------------
     def build_csr_cluster(self, A: DeviceCsr, asg: ClusterAssignment) -> DeviceCsrCluster:
         s = L.bsp_csr_cluster()
@@ -759,6 +770,22 @@ def bandwidth(a: CsrMatrix) -> int:
     ha = a._host()
     _check(L.load().bsp_bandwidth(C.byref(ha), C.byref(out)))
     return int(out.value)
+
+
+def generate_frontiers(a: CsrMatrix, num_frontiers: int = 10, batch: int = 64,
+                       seed: int = 0) -> list:
+    """reference frontier.hpp:20-77 (host CSR in, host CSRs out; BFS on the GPU)."""
+    e = default_engine()
+    A = e.upload(a)
+    try:
+        fs = e.generate_frontiers(A, num_frontiers, batch, seed)
+        out = []
+        for f in fs:
+            out.append(f.download())
+            f.free()
+        return out
+    finally:
+        A.free()
 
 
 def transpose(a: CsrMatrix) -> CsrMatrix:

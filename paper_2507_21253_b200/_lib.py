@@ -102,6 +102,8 @@ SIGNATURES = {
                                            P(bsp_access_stats)]),
     "bsp_rowwise_access_stats": (C.c_int, [vp, P(bsp_csr), P(bsp_csr), P(bsp_access_stats)]),
     "bsp_transpose": (C.c_int, [vp, P(bsp_csr), P(bsp_csr)]),
+    "bsp_generate_frontiers": (C.c_int, [vp, P(bsp_csr), C.c_int64, C.c_int64, C.c_uint64,
+                                         P(bsp_csr), P(C.c_int64)]),
     "bsp_spgemm_topk": (C.c_int, [vp, P(bsp_csr), P(bsp_csr), i32, dbl, P(P(bsp_candidate)),
                                   P(i64)]),
     "bsp_minhash_candidates": (C.c_int, [vp, P(bsp_csr), i32, i32, u64, i32, dbl,

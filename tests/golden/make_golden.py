@@ -18,6 +18,9 @@ import oracle as O  # noqa: E402
 import paper_2507_21253_b200 as B  # noqa: E402
 
 SMALL = {1: 256, 2: 32, 3: 8, 4: 6, 5: 9}
+# (cfg, num_frontiers, batch, seed): R-MAT, directed hidden-cluster rows,
+# batch > n, a single frontier
+FRONTIER_CASES = [(5, 10, 16, 0), (2, 10, 64, 3), (1, 4, 100, 1), (4, 1, 8, 5)]
 
 
 def main():
@@ -43,6 +46,16 @@ def main():
         if a.nrows == a.ncols:
             out[p + "rcm"] = O.ref_reorder_rcm(a)
             out[p + "degree"] = O.ref_reorder_degree(a)
+    # tall-skinny frontier operands (frontier.hpp:20-77) on the fixtures' A
+    for cfg, nf, bt, sd in FRONTIER_CASES:
+        p = f"cfg{cfg}_"
+        a = O.Csr(len(out[p + "A_rp"]) - 1, len(out[p + "A_rp"]) - 1, out[p + "A_rp"],
+                  out[p + "A_ci"], out[p + "A_v"])
+        fs = O.ref_generate_frontiers(a, nf, bt, sd)
+        q = f"fr_{cfg}_{nf}_{bt}_{sd}_"
+        out[q + "count"] = np.array([len(fs)], np.int64)
+        for t, f in enumerate(fs):
+            out[q + f"{t}_rp"], out[q + f"{t}_ci"] = f.row_ptr, f.col_idx
     for n, seed in [(1, 7), (5, 3), (100, 42), (4096, 4)]:
         out[f"perm_{n}_{seed}"] = O.ref_reorder_random(n, seed)
     path = Path(__file__).with_name("golden.npz")
