@@ -177,6 +177,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--workload", default="a2", choices=["a2", "ts"],
+                    help="a2: C = A*A (headline); ts: A x 10 BFS frontiers of 64 sources "
+                         "(square x tall-skinny, SURVEY 8(f)-1)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -195,6 +198,10 @@ def main():
     import torch
 
     torch.cuda.set_device(local)
+    if args.workload == "ts":
+        if rank == 0:
+            run_tall_skinny(B, args)
+        return
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -343,6 +350,95 @@ def main():
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_tall_skinny(B, args, num_frontiers=10, batch=64, seed=0):
+    """Square x tall-skinny (bench.hpp:129-193 with Workload::tall_skinny):
+    B_t = the BFS frontiers of A (generate_frontiers, frontier.hpp:20-77; 10 x
+    64 sources, seed 0, original order), one step = C_t = A * B_t for every
+    t (time_rowwise / time_clusterwise, bench.hpp:172-193), A clustered once
+    (hierarchical) and reused — the paper's amortisation scenario."""
+    import torch
+
+    a = B.make_config(CFG, args.scale)
+    eng = B.Engine(0)
+    stream = torch.cuda.Stream()
+    eng.set_stream(stream.cuda_stream)
+    A = eng.upload(a)
+    fs = eng.generate_frontiers(A, num_frontiers, batch, seed)
+    products = sum(eng.spgemm_products(A, f) for f in fs)
+    asg = eng.hierarchical_clusters(a)
+    Ac = eng.build_csr_cluster(A, asg)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            for f in fs:
+                fn(f).free()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = eng.kernel_launches()
+        e0.record(stream)
+        for _ in range(args.steps):
+            for f in fs:
+                fn(f).free()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps, eng.kernel_launches() - l0
+
+    with ClockSampler(0) as clk:
+        ms_row, launches = timed(lambda f: eng.spgemm_rowwise(A, f))
+        ms_cl, _ = timed(lambda f: eng.spgemm_clusterwise(Ac, f))
+    nnz_c = 0
+    for f in fs:
+        C = eng.spgemm_rowwise(A, f)
+        nnz_c += C.nnz()
+        C.free()
+    peak, peak_kind = hbm_peak()
+    bal = sum(bytes_alg(a.nnz(), f.nnz(), 0, a.nrows, f.nrows, a.nrows) for f in fs) + 12 * nnz_c
+    line = {
+        "metric": "A·B SpGEMM GFLOP/s (2×products/s)",
+        "value": 2.0 * products / (ms_row * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_row,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded R-MAT, BASELINE cfg5; frontiers by device BFS)",
+        "config": {"workload": f"cfg5_rmat22_x_{len(fs)}_frontiers_b{batch}_rowwise",
+                   "n": a.nrows, "nnz_a": a.nnz(), "frontiers": len(fs), "batch": batch,
+                   "nnz_b": [f.nnz() for f in fs], "products": products, "nnz_c": nnz_c,
+                   "parallelism": "x1"},
+        "clusterwise": {"value": 2.0 * products / (ms_cl * 1e-3) / 1e9, "ms_per_step": ms_cl,
+                        "clusters": asg.nclusters},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": bal / (ms_row * 1e-3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": bal / (ms_row * 1e-3) / 1e9 / peak,
+                     "traffic": None, "bytes_alg_per_step": bal, "peak_source": peak_kind,
+                     "unit_of_work": "all frontier multiplies of one step"},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu:
+        import oracle as O
+
+        if O.have_ref():
+            stride = args.cpu_stride
+            rows = np.arange(0, a.nrows, stride, dtype=np.int64)
+            lens = np.diff(a.row_ptr)[rows]
+            rp = np.zeros(rows.size + 1, np.int64)
+            rp[1:] = np.cumsum(lens)
+            idx = np.concatenate([np.arange(a.row_ptr[r], a.row_ptr[r + 1]) for r in rows])
+            sub = O.Csr(rows.size, a.ncols, rp, a.col_idx[idx], a.values[idx])
+            secs, prods = 0.0, 0
+            for f in fs:
+                fh = f.download()
+                prods += int(np.diff(fh.row_ptr)[sub.col_idx].sum())
+                t0 = time.perf_counter()
+                O.ref_spgemm_rowwise(sub, O.Csr(fh.nrows, fh.ncols, fh.row_ptr, fh.col_idx,
+                                                fh.values), threads=os.cpu_count() or 1)
+                secs += time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": 2.0 * prods / secs / 1e9, "unit": "GFLOP/s",
+                                    "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"rows i = 0 mod {stride} of A x every frontier"}
+    for f in fs:
+        f.free()
+    print(json.dumps(line))
 
 
 def run_e2e(B, eng, a, args, total_products):

@@ -135,9 +135,10 @@ struct PlanWriteShared {
 // (b0, b1) bounds of 32 upcoming segments fetched at once by the warp's lanes
 // and PLAN_U chunks of 32 B columns loaded before they are consumed, so each
 // warp keeps several independent loads in flight.  f(p, q0, len, cols[U],
-// state) is called for each group of chunks (warp-uniform); cols[u] holds
-// the column of element q0 + 32u + lane or -1 past the end; `state` is an
-// int reset to -1 at the start of every segment.
+// state) is called for each group of chunks (warp-uniform; once with q0 = 0
+// for an empty segment); cols[u] holds the column of element q0 + 32u + lane
+// or -1 past the end; `state` is an int reset to -1 at the start of every
+// segment.
 template <class F>
 __device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& f) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -158,7 +159,9 @@ __device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& 
             const int len = static_cast<int>(__shfl_sync(0xffffffffu, mb1, j) - b0);
             const int p = pb + NW * j;
             int state = -1;
-            for (int q0 = 0; q0 < len; q0 += 32 * PLAN_U) {
+            // an empty segment still gets one call (all columns -1): the
+            // start-table pass must fill its entries too
+            for (int q0 = 0; q0 < ::max(len, 1); q0 += 32 * PLAN_U) {
                 int32_t cols[PLAN_U];
 #pragma unroll
                 for (int u = 0; u < PLAN_U; ++u) {

@@ -136,3 +136,40 @@ def test_host_buffer_entry_point(engine):
     a = B.make_config(2, 1024)
     c = B.spgemm_rowwise(a, a)
     assert_csr_identical(c, O.spgemm_rowwise(a, a), "host entry")
+
+
+def test_heavy_rows_over_empty_b_rows(engine):
+    """Heavy rows (windowed) whose segments include empty B rows — the shape
+    of A x frontier operands: every start-table entry must still be filled."""
+    rng = np.random.default_rng(5)
+    n, m = 600, 3000
+    r, c = [], []
+    for i in range(n):
+        d = 1500 if i % 50 == 0 else int(rng.integers(1, 12))
+        cols = np.sort(rng.choice(n, size=min(d, n), replace=False))
+        r += [i] * cols.size
+        c += cols.tolist()
+    a = B.coo_to_csr(n, n, np.array(r), np.array(c), rng.random(len(r)))
+    br, bc = [], []
+    for k in range(n):
+        if k % 3 == 0:
+            continue  # empty B row
+        cols = np.sort(rng.choice(m, size=int(rng.integers(5, 40)), replace=False))
+        br += [k] * cols.size
+        bc += cols.tolist()
+    b = B.coo_to_csr(n, m, np.array(br), np.array(bc), rng.random(len(br)))
+    A, Bd = engine.upload(a), engine.upload(b)
+    c = engine.spgemm_rowwise(A, Bd).download()
+    assert engine.exec_stats()["units"][5] > 0, "no heavy rows"
+    assert_csr_identical(c, O.spgemm_rowwise(a, b), "heavy rows over empty B rows")
+    # tall-skinny: every heavy row's window is one dense 64-column window
+    r64, c64 = [], []
+    for k in range(n):
+        if k % 3:
+            cols = np.sort(rng.choice(64, size=int(rng.integers(1, 20)), replace=False))
+            r64 += [k] * cols.size
+            c64 += cols.tolist()
+    b64 = B.coo_to_csr(n, 64, np.array(r64), np.array(c64), np.ones(len(r64)))
+    B64 = engine.upload(b64)
+    assert_csr_identical(engine.spgemm_rowwise(A, B64).download(), O.spgemm_rowwise(a, b64),
+                         "dense windows over empty B rows")
