@@ -170,6 +170,7 @@ struct RowwisePlan {
     DBuf<int32_t> lists;  // all non-empty rows grouped by class
     int64_t nwin = 0, nsparse = 0, ndense = 0;
     int64_t nsparse_large = 0;  // sparse_ids[0, nsparse_large): > WSMALL products
+    int64_t nsparse_mid = 0;    // ... then this many with 512 < products <= WSMALL
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
     int64_t nhcur = 0;    // heavy rows walked by one CTA with cursors

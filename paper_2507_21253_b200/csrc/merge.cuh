@@ -27,9 +27,7 @@ __device__ __forceinline__ int PADI(int i) { return i + (i >> 5); }
 template <int T, int CAPM>
 struct MergeShared {
     static constexpr int NP = CAPM + CAPM / 32 + 1;
-    // radix digit width: CUB's rank storage is T x 2^RB / 2 words, so 512-thread
-    // tiles use 5-bit digits to keep it at 32 KB
-    static constexpr int RB = T >= 512 ? 5 : 6;
+    static constexpr int RB = 6;  // radix digit bits (CUB rank storage T x 2^RB / 2 words)
     using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, RB>;
     // buffer 0 (also the radix-sort input/output)
     uint32_t key0[NP];

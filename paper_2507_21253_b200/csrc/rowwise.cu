@@ -175,8 +175,8 @@ __device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& 
 }
 
 // K2a: per heavy row, a product histogram over `nbins` column bins, then the
-// window cut: a bin with > CAPB products gets its own window (dense when
-// > CAP), runs of smaller bins are cut where floor(prefix / CAPG) changes or
+// window cut: a bin with > capb products gets its own window (dense when
+// > CAP), runs of smaller bins are cut where floor(prefix / capg) changes or
 // after a big bin.  Writes the window count and the descriptors
 // {c0 | DENSE_BIT, product prefix} (+ sentinel {ncols, P}) at desc[doff[h]].
 __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
                                                             int32_t nbins, int log_binw,
                                                             int32_t* __restrict__ nwin,
                                                             const int64_t* __restrict__ doff,
-                                                            uint2* __restrict__ desc) {
+                                                            uint2* __restrict__ desc,
+                                                            int32_t capb, int32_t capg) {
     __shared__ PlanCountShared s;
     const int32_t hrow = blockIdx.x;
     const int32_t row = heavy[hrow];
@@ -232,10 +233,10 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
         const int32_t pre = base + excl[i];
         bool st = false;
         if (b < nbins) {
-            st = (b == 0) || cnt[i] > CAPB;
+            st = (b == 0) || cnt[i] > capb;
             if (!st) {
                 const int32_t pc = s.hist[b - 1];
-                st = (pc > CAPB) || ((pre - pc) / CAPG != pre / CAPG);
+                st = (pc > capb) || ((pre - pc) / capg != pre / capg);
             }
         }
         starts[i] = st;
@@ -307,8 +308,9 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
         wd.nprod = s.u.w.wpre[k + 1] - s.u.w.wpre[k];
         wd.sofs = sofs;
         wins[off + k] = wd;
-        // 0: sparse, 1: dense, 2: sparse with <= WSMALL products
-        win_cat[off + k] = static_cast<uint8_t>(dense ? 1 : (wd.nprod <= WSMALL ? 2 : 0));
+        // 0: sparse > 2048 products, 1: dense, 2: sparse <= 2048, 3: sparse <= 512
+        win_cat[off + k] = static_cast<uint8_t>(
+            dense ? 1 : (wd.nprod <= 512 ? 3 : (wd.nprod <= WSMALL ? 2 : 0)));
     }
     if (sofs < 0) return;
     __syncthreads();  // wc0/wpre dead: the union becomes the staging area
@@ -343,11 +345,11 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
 }
 
 // Upper bound on a heavy row's windows (+1 sentinel descriptor):
-// <= P/(CAPB+1) big bins, each may also start the run after it, and the
-// runs are cut at most P/CAPG times.
+// <= P/(capb+1) big bins, each may also start the run after it, and the
+// runs are cut at most P/capg times.
 __global__ void plan_bound_kernel(const int32_t* __restrict__ heavy, int64_t nh, int64_t rb,
                                   const int64_t* __restrict__ prod, int32_t nbins,
-                                  int64_t* __restrict__ bound) {
+                                  int32_t capb, int32_t capg, int64_t* __restrict__ bound) {
     const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
     if (t > nh) return;
     if (t == nh) {
@@ -355,7 +357,7 @@ __global__ void plan_bound_kernel(const int32_t* __restrict__ heavy, int64_t nh,
         return;
     }
     const int64_t P = prod[heavy[t] - rb];
-    bound[t] = ::min(2 * (P / (CAPB + 1)) + P / CAPG + 2, int64_t{nbins}) + 1;
+    bound[t] = ::min(2 * (P / (capb + 1)) + P / capg + 2, int64_t{nbins}) + 1;
 }
 
 // Size of each heavy row's start table ((windows+1) x A-row length), or 0
@@ -395,15 +397,15 @@ __global__ void split_heavy_kernel(Mats m, const int32_t* __restrict__ heavy, in
     }
 }
 
-// Split window ids by category (0 sparse, 1 dense, 2 small sparse) into
-// out[category] lists.
+// Split window ids by category (0 sparse, 1 dense, 2 / 3 smaller sparse)
+// into out[category] lists.
 __global__ void split_windows_kernel(const uint8_t* __restrict__ cat, int64_t nw,
                                      unsigned long long* __restrict__ cursor,
                                      int32_t* __restrict__ out0, int32_t* __restrict__ out1,
-                                     int32_t* __restrict__ out2) {
-    __shared__ unsigned s_cnt[3];
-    __shared__ unsigned long long s_base[3];
-    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+                                     int32_t* __restrict__ out2, int32_t* __restrict__ out3) {
+    __shared__ unsigned s_cnt[4];
+    __shared__ unsigned long long s_base[4];
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     const int64_t w = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
     int d = 0;
@@ -413,9 +415,20 @@ __global__ void split_windows_kernel(const uint8_t* __restrict__ cat, int64_t nw
         rank = atomicAdd(&s_cnt[d], 1u);
     }
     __syncthreads();
-    if (threadIdx.x < 3) s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
+    if (threadIdx.x < 4) s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
     __syncthreads();
-    if (w < nw) (d == 0 ? out0 : d == 1 ? out1 : out2)[s_base[d] + rank] = static_cast<int32_t>(w);
+    if (w < nw) {
+        int32_t* o = d == 0 ? out0 : d == 1 ? out1 : d == 2 ? out2 : out3;
+        o[s_base[d] + rank] = static_cast<int32_t>(w);
+    }
+}
+
+// Sort key of a window list: its first column (windows launched in column
+// order share B's column slices in L2 across heavy rows).
+__global__ void window_c0_kernel(const Window* __restrict__ wins, const int32_t* __restrict__ ids,
+                                 int64_t n, uint32_t* __restrict__ keys) {
+    const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (i < n) keys[i] = static_cast<uint32_t>(wins[ids[i]].c0);
 }
 
 template <int T, int I, bool NUMERIC>
@@ -1008,17 +1021,25 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                 "planner: heavy rows need ncols <= 16M (MAXBINS*WD) in this build");
         DBuf<int32_t> nwin(h, nh + 1);
         BSP_CUDA(cudaMemsetAsync(nwin.p, 0, (nh + 1) * sizeof(int32_t), h->stream));
+        // window packing target (products): runs of small bins are cut every
+        // capg products, bins above capb stand alone (BSP_WTARGET to tune)
+        static const int32_t capg = [] {
+            const char* e = std::getenv("BSP_WTARGET");
+            const int v = e ? std::atoi(e) : CAPG;
+            return std::max(64, std::min(v, CAPG));
+        }();
+        const int32_t capb = std::min(CAPB, capg / 3);
         // window descriptors: per heavy row a slot sized by the window bound
         DBuf<int64_t> dbound(h, nh + 1), doff(h, nh + 1);
         BSP_LAUNCH(h, plan_bound_kernel, static_cast<unsigned>(div_up(nh + 1, 256)), 256, 0,
-                   heavy, nh, rb, prod_out, nbins, dbound.p);
+                   heavy, nh, rb, prod_out, nbins, capb, capg, dbound.p);
         exclusive_scan_i64(h, dbound.p, doff.p, nh + 1);
         int64_t ndesc = 0;
         d2h(h, &ndesc, doff.p + nh, 1);
         sync(h);
         DBuf<uint2> desc(h, ndesc);
         BSP_LAUNCH(h, plan_count_kernel, static_cast<unsigned>(nh), PLAN_T, 0, m, heavy, nbins,
-                   log_binw, nwin.p, doff.p, desc.p);
+                   log_binw, nwin.p, doff.p, desc.p, capb, capg);
         DBuf<int64_t> woff(h, nh + 1);
         exclusive_scan_i32_to_i64(h, nwin.p, woff.p, nh + 1);
         // per-(window, segment) start tables, bounded per row and in total
@@ -1031,11 +1052,14 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         d2h(h, &hv[1], soff.p + nh, 1);
         sync(h);
         plan.nwin = hv[0];
-        // Start-table budget: <= 2^30 entries (4 GB) and <= 1/8 of free HBM;
-        // the rows in scan order that fit get a table.
-        const int64_t budget = std::min<int64_t>(
-            {hv[1], int64_t{1} << 30,
-             static_cast<int64_t>(available_bytes(h) / (8 * sizeof(int32_t)))});
+        // Start-table budget: what HBM holds beyond an upper bound of C
+        // (12 B x products) and a 2 GB margin, at most 2^32 entries (16 GB);
+        // the rows in scan order that fit get a table, the rest binary-search.
+        const int64_t spare = static_cast<int64_t>(available_bytes(h)) -
+                              12 * h->stats.products - (int64_t{2} << 30);
+        const int64_t budget = std::max<int64_t>(
+            0, std::min<int64_t>({hv[1], int64_t{1} << 32,
+                                  spare / static_cast<int64_t>(sizeof(int32_t))}));
         const bool use_starts = budget > 0;
         if (use_starts) plan.starts = DBuf<int32_t>(h, budget);
         plan.wins = DBuf<Window>(h, plan.nwin);
@@ -1047,22 +1071,60 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                    use_starts ? plan.starts.p : nullptr);
         plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
         plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
-        DBuf<int32_t> small(h, plan.nwin);
-        DBuf<unsigned long long> cursor(h, 3);
-        BSP_CUDA(cudaMemsetAsync(cursor.p, 0, 3 * sizeof(unsigned long long), h->stream));
+        DBuf<int32_t> mid(h, plan.nwin), small(h, plan.nwin);
+        DBuf<unsigned long long> cursor(h, 4);
+        BSP_CUDA(cudaMemsetAsync(cursor.p, 0, 4 * sizeof(unsigned long long), h->stream));
         BSP_LAUNCH(h, split_windows_kernel, static_cast<unsigned>(div_up(plan.nwin, 256)), 256, 0,
-                   dense.p, plan.nwin, cursor.p, plan.sparse_ids.p, plan.dense_ids.p, small.p);
-        unsigned long long hcur[3];
-        d2h(h, hcur, cursor.p, 3);
+                   dense.p, plan.nwin, cursor.p, plan.sparse_ids.p, plan.dense_ids.p, mid.p,
+                   small.p);
+        unsigned long long hcur[4];
+        d2h(h, hcur, cursor.p, 4);
         sync(h);
-        // sparse list = large windows, then small ones (top-k walks it whole)
+        // sparse list = large windows, then <= 2048, then <= 512 products
+        // (top-k walks it whole)
         plan.nsparse_large = static_cast<int64_t>(hcur[0]);
-        plan.nsparse = static_cast<int64_t>(hcur[0] + hcur[2]);
+        plan.nsparse_mid = static_cast<int64_t>(hcur[2]);
+        plan.nsparse = static_cast<int64_t>(hcur[0] + hcur[2] + hcur[3]);
         plan.ndense = static_cast<int64_t>(hcur[1]);
         if (hcur[2] > 0)
-            BSP_CUDA(cudaMemcpyAsync(plan.sparse_ids.p + hcur[0], small.p,
-                                     hcur[2] * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+            BSP_CUDA(cudaMemcpyAsync(plan.sparse_ids.p + hcur[0], mid.p, hcur[2] * sizeof(int32_t),
+                                     cudaMemcpyDeviceToDevice, h->stream));
+        if (hcur[3] > 0)
+            BSP_CUDA(cudaMemcpyAsync(plan.sparse_ids.p + hcur[0] + hcur[2], small.p,
+                                     hcur[3] * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                                      h->stream));
+        // BSP_WINDOW_ORDER=col: each list in column order (stable) so that
+        // concurrent windows share B's column slices in L2 — measured slower
+        // on cfg5 (545 vs 524 ms: A rows and start tables lose their reuse),
+        // so row order is the default.
+        static const bool by_col = [] {
+            const char* e = std::getenv("BSP_WINDOW_ORDER");
+            return e && std::string(e) == "col";
+        }();
+        if (by_col) {
+            const int cbits = bit_length(static_cast<uint32_t>(std::max<int64_t>(m.ncols, 1)));
+            auto sort_list = [&](int32_t* ids, int64_t n) {
+                if (n <= 1) return;
+                DBuf<uint32_t> k0(h, n), k1(h, n);
+                DBuf<int32_t> v1(h, n);
+                BSP_LAUNCH(h, window_c0_kernel, static_cast<unsigned>(div_up(n, 256)), 256, 0,
+                           plan.wins.p, ids, n, k0.p);
+                size_t tmp = 0;
+                BSP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0.p, k1.p, ids, v1.p, n, 0,
+                                                         cbits, h->stream));
+                DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+                BSP_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, k0.p, k1.p, ids, v1.p, n, 0,
+                                                         cbits, h->stream));
+                ++h->launches;
+                BSP_CUDA(cudaMemcpyAsync(ids, v1.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                         h->stream));
+            };
+            sort_list(plan.sparse_ids.p, plan.nsparse_large);
+            sort_list(plan.sparse_ids.p + plan.nsparse_large, plan.nsparse_mid);
+            sort_list(plan.sparse_ids.p + plan.nsparse_large + plan.nsparse_mid,
+                      plan.nsparse - plan.nsparse_large - plan.nsparse_mid);
+            sort_list(plan.dense_ids.p, plan.ndense);
+        }
     }
     for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];  // [5] = heavy rows
     h->stats.units[6] = plan.nsparse;
@@ -1093,12 +1155,12 @@ void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCt
     launch_heavy<NUMERIC>(h, m, plan.hcur.p, plan.nhcur, out);
     for (int c = NCLS - 2; c >= 1; --c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
-    if (NUMERIC && std::getenv("BSP_T512"))
-        launch_tile<512, 4096, true>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
-    else
-        launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
+    launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
     launch_tile<128, 2048, NUMERIC>(h, m, plan.sparse_ids.p + plan.nsparse_large,
-                                    plan.nsparse - plan.nsparse_large, plan.wins.p, out);
+                                    plan.nsparse_mid, plan.wins.p, out);
+    launch_tile<64, 512, NUMERIC>(h, m, plan.sparse_ids.p + plan.nsparse_large + plan.nsparse_mid,
+                                  plan.nsparse - plan.nsparse_large - plan.nsparse_mid,
+                                  plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
 
