@@ -16,7 +16,10 @@ constexpr int CAPH = CAP / 2;
 // < CAPG + CAPB = CAP products and averages ~CAPG.
 constexpr int CAPB = CAP / 4;
 constexpr int CAPG = CAP - CAPB;
-constexpr int WSMALL = CAP / 2;  // sparse windows with <= WSMALL products run in half tiles
+// Sparse-window tile classes (descending): a window runs in the smallest
+// tile that holds its products (CUB's block sort always sorts the full tile).
+// (A 192-thread 3072 class was measured slower: 2 CTAs x 6 warps per SM.)
+constexpr int NWCLS = 3;
 constexpr int WD = 4096;      // dense window width in columns
 constexpr int LOG_WD = 12;
 constexpr int MAXBINS = 4096; // planner histogram bins per heavy row
@@ -169,8 +172,8 @@ struct RowwisePlan {
     int64_t class_off[NCLS + 1]{};
     DBuf<int32_t> lists;  // all non-empty rows grouped by class
     int64_t nwin = 0, nsparse = 0, ndense = 0;
-    int64_t nsparse_large = 0;  // sparse_ids[0, nsparse_large): > WSMALL products
-    int64_t nsparse_mid = 0;    // ... then this many with 512 < products <= WSMALL
+    // sparse_ids[wcls_off[k], wcls_off[k+1]): windows of tile class k (kWinCap)
+    int64_t wcls_off[NWCLS + 1]{};
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
     int64_t nhcur = 0;    // heavy rows walked by one CTA with cursors

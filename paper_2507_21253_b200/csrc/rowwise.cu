@@ -110,6 +110,7 @@ __global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64
 // K2: heavy-row planner
 // ---------------------------------------------------------------------------
 constexpr int PLAN_T = 256;
+__constant__ int kWinCapDev[NWCLS] = {4096, 2048, 512};
 constexpr int PLAN_U = 8;  // B-row chunks of 32 loaded ahead per warp
 constexpr uint32_t DENSE_BIT = 0x80000000u;
 
@@ -308,9 +309,13 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
         wd.nprod = s.u.w.wpre[k + 1] - s.u.w.wpre[k];
         wd.sofs = sofs;
         wins[off + k] = wd;
-        // 0: sparse > 2048 products, 1: dense, 2: sparse <= 2048, 3: sparse <= 512
-        win_cat[off + k] = static_cast<uint8_t>(
-            dense ? 1 : (wd.nprod <= 512 ? 3 : (wd.nprod <= WSMALL ? 2 : 0)));
+        // sparse: the smallest tile class that holds the window; dense: NWCLS
+        int cat = NWCLS;
+        if (!dense) {
+            cat = 0;
+            while (cat + 1 < NWCLS && wd.nprod <= kWinCapDev[cat + 1]) ++cat;
+        }
+        win_cat[off + k] = static_cast<uint8_t>(cat);
     }
     if (sofs < 0) return;
     __syncthreads();  // wc0/wpre dead: the union becomes the staging area
@@ -397,15 +402,27 @@ __global__ void split_heavy_kernel(Mats m, const int32_t* __restrict__ heavy, in
     }
 }
 
-// Split window ids by category (0 sparse, 1 dense, 2 / 3 smaller sparse)
-// into out[category] lists.
+// Window ids by category (sparse tile class 0..NWCLS-1, dense NWCLS):
+// counts, then a scatter from per-category cursors (block-aggregated).
+__global__ void window_cat_count_kernel(const uint8_t* __restrict__ cat, int64_t nw,
+                                        unsigned long long* __restrict__ cnt) {
+    __shared__ unsigned s_cnt[NWCLS + 1];
+    if (threadIdx.x <= NWCLS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t w = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (w < nw) atomicAdd(&s_cnt[cat[w]], 1u);
+    __syncthreads();
+    if (threadIdx.x <= NWCLS && s_cnt[threadIdx.x])
+        atomicAdd(&cnt[threadIdx.x], static_cast<unsigned long long>(s_cnt[threadIdx.x]));
+}
+
 __global__ void split_windows_kernel(const uint8_t* __restrict__ cat, int64_t nw,
                                      unsigned long long* __restrict__ cursor,
-                                     int32_t* __restrict__ out0, int32_t* __restrict__ out1,
-                                     int32_t* __restrict__ out2, int32_t* __restrict__ out3) {
-    __shared__ unsigned s_cnt[4];
-    __shared__ unsigned long long s_base[4];
-    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+                                     int32_t* __restrict__ sparse_ids,
+                                     int32_t* __restrict__ dense_ids) {
+    __shared__ unsigned s_cnt[NWCLS + 1];
+    __shared__ unsigned long long s_base[NWCLS + 1];
+    if (threadIdx.x <= NWCLS) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     const int64_t w = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
     int d = 0;
@@ -415,12 +432,9 @@ __global__ void split_windows_kernel(const uint8_t* __restrict__ cat, int64_t nw
         rank = atomicAdd(&s_cnt[d], 1u);
     }
     __syncthreads();
-    if (threadIdx.x < 4) s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
+    if (threadIdx.x <= NWCLS) s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
     __syncthreads();
-    if (w < nw) {
-        int32_t* o = d == 0 ? out0 : d == 1 ? out1 : d == 2 ? out2 : out3;
-        o[s_base[d] + rank] = static_cast<int32_t>(w);
-    }
+    if (w < nw) (d == NWCLS ? dense_ids : sparse_ids)[s_base[d] + rank] = static_cast<int32_t>(w);
 }
 
 // Sort key of a window list: its first column (windows launched in column
@@ -570,9 +584,12 @@ __global__ void __launch_bounds__(T, T >= 256 ? 2 : 4) esc_merge_kernel(Mats m, 
                               out.cval + base);
 }
 
+constexpr int pow2_ceil(int x) { return x <= 1 ? 1 : 2 * pow2_ceil((x + 1) / 2); }
+
 template <int T, int CAPM, bool STAGED = true>
 struct HashShared {
-    int32_t table[2 * CAPM];
+    static constexpr int TS = pow2_ceil(2 * CAPM);  // open-addressing slots (power of two)
+    int32_t table[TS];
     int32_t stage[STAGED ? CAPM : 1];  // gathered columns of the current chunk
     typename cub::BlockReduce<int32_t, T>::TempStorage red;
     typename cub::BlockScan<int32_t, T>::TempStorage scan;
@@ -592,7 +609,8 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
     S& s = *reinterpret_cast<S*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = T / 32;
-    constexpr int LG = 1 + 31 - __builtin_clz(static_cast<unsigned>(CAPM));  // 2*CAPM slots
+    constexpr int TS = S::TS;
+    constexpr int LG = 31 - __builtin_clz(static_cast<unsigned>(TS));
     const int32_t id = ids[blockIdx.x];
     int32_t row, c0, c1, w = -1;
     int64_t wsofs = -1;
@@ -611,7 +629,7 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         c1 = m.ncols;
     }
     const bool full = wins == nullptr;
-    for (int e = tid; e < 2 * CAPM; e += T) s.table[e] = -1;
+    for (int e = tid; e < TS; e += T) s.table[e] = -1;
     const int64_t rs = m.arp[row], re = m.arp[row + 1];
     int cnt = 0;
     for (int64_t pc = rs; pc < re; pc += T) {
@@ -647,7 +665,7 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
                     break;
                 }
                 if (prev == col) break;
-                hsl = (hsl + 1) & (2 * CAPM - 1);
+                hsl = (hsl + 1) & (TS - 1);
             }
         };
         if constexpr (STAGED) {
@@ -1071,28 +1089,25 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                    use_starts ? plan.starts.p : nullptr);
         plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
         plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
-        DBuf<int32_t> mid(h, plan.nwin), small(h, plan.nwin);
-        DBuf<unsigned long long> cursor(h, 4);
-        BSP_CUDA(cudaMemsetAsync(cursor.p, 0, 4 * sizeof(unsigned long long), h->stream));
+        DBuf<unsigned long long> cnt(h, NWCLS + 1);
+        BSP_CUDA(cudaMemsetAsync(cnt.p, 0, (NWCLS + 1) * sizeof(unsigned long long), h->stream));
+        BSP_LAUNCH(h, window_cat_count_kernel, static_cast<unsigned>(div_up(plan.nwin, 256)), 256,
+                   0, dense.p, plan.nwin, cnt.p);
+        unsigned long long hc[NWCLS + 1];
+        d2h(h, hc, cnt.p, NWCLS + 1);
+        // sparse list = tile classes in descending size (top-k walks it whole)
+        unsigned long long cur[NWCLS + 1];
+        plan.wcls_off[0] = 0;
+        for (int k = 0; k < NWCLS; ++k) {
+            cur[k] = static_cast<unsigned long long>(plan.wcls_off[k]);
+            plan.wcls_off[k + 1] = plan.wcls_off[k] + static_cast<int64_t>(hc[k]);
+        }
+        cur[NWCLS] = 0;
+        plan.nsparse = plan.wcls_off[NWCLS];
+        plan.ndense = static_cast<int64_t>(hc[NWCLS]);
+        h2d(h, cnt.p, cur, NWCLS + 1);
         BSP_LAUNCH(h, split_windows_kernel, static_cast<unsigned>(div_up(plan.nwin, 256)), 256, 0,
-                   dense.p, plan.nwin, cursor.p, plan.sparse_ids.p, plan.dense_ids.p, mid.p,
-                   small.p);
-        unsigned long long hcur[4];
-        d2h(h, hcur, cursor.p, 4);
-        sync(h);
-        // sparse list = large windows, then <= 2048, then <= 512 products
-        // (top-k walks it whole)
-        plan.nsparse_large = static_cast<int64_t>(hcur[0]);
-        plan.nsparse_mid = static_cast<int64_t>(hcur[2]);
-        plan.nsparse = static_cast<int64_t>(hcur[0] + hcur[2] + hcur[3]);
-        plan.ndense = static_cast<int64_t>(hcur[1]);
-        if (hcur[2] > 0)
-            BSP_CUDA(cudaMemcpyAsync(plan.sparse_ids.p + hcur[0], mid.p, hcur[2] * sizeof(int32_t),
-                                     cudaMemcpyDeviceToDevice, h->stream));
-        if (hcur[3] > 0)
-            BSP_CUDA(cudaMemcpyAsync(plan.sparse_ids.p + hcur[0] + hcur[2], small.p,
-                                     hcur[3] * sizeof(int32_t), cudaMemcpyDeviceToDevice,
-                                     h->stream));
+                   dense.p, plan.nwin, cnt.p, plan.sparse_ids.p, plan.dense_ids.p);
         // BSP_WINDOW_ORDER=col: each list in column order (stable) so that
         // concurrent windows share B's column slices in L2 — measured slower
         // on cfg5 (545 vs 524 ms: A rows and start tables lose their reuse),
@@ -1119,10 +1134,9 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                 BSP_CUDA(cudaMemcpyAsync(ids, v1.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                                          h->stream));
             };
-            sort_list(plan.sparse_ids.p, plan.nsparse_large);
-            sort_list(plan.sparse_ids.p + plan.nsparse_large, plan.nsparse_mid);
-            sort_list(plan.sparse_ids.p + plan.nsparse_large + plan.nsparse_mid,
-                      plan.nsparse - plan.nsparse_large - plan.nsparse_mid);
+            for (int k = 0; k < NWCLS; ++k)
+                sort_list(plan.sparse_ids.p + plan.wcls_off[k],
+                          plan.wcls_off[k + 1] - plan.wcls_off[k]);
             sort_list(plan.dense_ids.p, plan.ndense);
         }
     }
@@ -1155,12 +1169,12 @@ void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCt
     launch_heavy<NUMERIC>(h, m, plan.hcur.p, plan.nhcur, out);
     for (int c = NCLS - 2; c >= 1; --c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
-    launch_tile<256, 4096, NUMERIC>(h, m, plan.sparse_ids.p, plan.nsparse_large, plan.wins.p, out);
-    launch_tile<128, 2048, NUMERIC>(h, m, plan.sparse_ids.p + plan.nsparse_large,
-                                    plan.nsparse_mid, plan.wins.p, out);
-    launch_tile<64, 512, NUMERIC>(h, m, plan.sparse_ids.p + plan.nsparse_large + plan.nsparse_mid,
-                                  plan.nsparse - plan.nsparse_large - plan.nsparse_mid,
-                                  plan.wins.p, out);
+    auto wl = [&](int k) { return plan.sparse_ids.p + plan.wcls_off[k]; };
+    auto wn = [&](int k) { return plan.wcls_off[k + 1] - plan.wcls_off[k]; };
+    static_assert(NWCLS == 3, "one launch per window tile class");
+    launch_tile<256, 4096, NUMERIC>(h, m, wl(0), wn(0), plan.wins.p, out);
+    launch_tile<128, 2048, NUMERIC>(h, m, wl(1), wn(1), plan.wins.p, out);
+    launch_tile<64, 512, NUMERIC>(h, m, wl(2), wn(2), plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
 
