@@ -18,8 +18,9 @@ constexpr int CAPB = CAP / 4;
 constexpr int CAPG = CAP - CAPB;
 // Sparse-window tile classes (descending): a window runs in the smallest
 // tile that holds its products (CUB's block sort always sorts the full tile).
-// (A 192-thread 3072 class was measured slower: 2 CTAs x 6 warps per SM.)
-constexpr int NWCLS = 3;
+// The 3072 class keeps 256 threads and is sized (≈73 KB smem, 85 registers)
+// for 3 CTAs/SM; a 192-thread 3072 tile (2 CTAs x 6 warps) measured slower.
+constexpr int NWCLS = 4;
 constexpr int WD = 4096;      // dense window width in columns
 constexpr int LOG_WD = 12;
 constexpr int MAXBINS = 4096; // planner histogram bins per heavy row
@@ -176,8 +177,6 @@ struct RowwisePlan {
     int64_t wcls_off[NWCLS + 1]{};
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
-    int64_t nhcur = 0;    // heavy rows walked by one CTA with cursors
-    DBuf<int32_t> hcur;   // ... sorted by products, descending
     DBuf<int32_t> starts; // planner per-(window, segment) start tables
     // Matrices as seen by the window kernels (start tables attached).
     Mats with_starts(const Mats& m) const {

@@ -27,23 +27,30 @@ __device__ __forceinline__ int PADI(int i) { return i + (i >> 5); }
 template <int T, int CAPM>
 struct MergeShared {
     static constexpr int NP = CAPM + CAPM / 32 + 1;
-    static constexpr int RB = 6;  // radix digit bits (CUB rank storage T x 2^RB / 2 words)
+    // radix digit bits: CUB's rank storage is T x 2^RB / 2 words whatever the
+    // tile size, so the 3072-product tile (sized for 3 CTAs/SM) uses 5-bit
+    // digits (16 KB) and the power-of-two tiles 6-bit digits
+    static constexpr int RB = (CAPM & (CAPM - 1)) == 0 ? 6 : 5;
     using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, RB>;
+    // run offsets: tiles with more runs than this use the radix sort
+    static constexpr int MAXRUNS = CAPM < 1024 ? CAPM : 1024;
+    // counters: MSD buckets (small tiles) or the reduction's (row, warp) heads
+    static constexpr int NHIST = CAPM <= 512 ? CAPM / 2 : ((CAPM + T - 1) / T) * (T / 32);
     // buffer 0 (also the radix-sort input/output)
     uint32_t key0[NP];
     uint16_t idx0[NP];
-    uint16_t ro0[CAPM + 2];  // run offsets (runs <= products <= CAPM)
+    uint16_t ro0[MAXRUNS + 2];
     double val[CAPM];
     // buffer 1 of the merge, aliased with the radix sort's temp storage
     union U {
         struct B1 {
             uint32_t key1[NP];
             uint16_t idx1[NP];
-            uint16_t ro1[CAPM + 2];
+            uint16_t ro1[MAXRUNS + 2];
         } m;
         typename RSort::TempStorage sort;
     } u;
-    uint32_t hist[CAPM / 2];  // MSD bucket counters / cursors
+    uint32_t hist[NHIST];
     __device__ __forceinline__ uint32_t* key(int b) { return b ? u.m.key1 : key0; }
     __device__ __forceinline__ uint16_t* idx(int b) { return b ? u.m.idx1 : idx0; }
     __device__ __forceinline__ uint16_t* ro(int b) { return b ? u.m.ro1 : ro0; }
@@ -122,7 +129,8 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         // compact the non-empty segments of this chunk (run order = k order)
         const int r = off >> 16;
         if (len > 0) {
-            s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
+            if (nruns + r < MergeShared<T, CAPM>::MAXRUNS)
+                s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
             s.pstart[r] = start;
             s.poff[r] = off & 0xffff;
             if (VALUES) s.pav[r] = av;
@@ -165,7 +173,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         __syncthreads();
     }
     if (tid == 0) {
-        s.ro(0)[nruns] = static_cast<uint16_t>(total);
+        if (nruns <= MergeShared<T, CAPM>::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
         s.nruns = nruns;
     }
     __syncthreads();
@@ -349,13 +357,15 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     // MSD counting sort when the columns spread evenly over the buckets (cfg2:
     // 1.3x faster tiles); skewed / duplicate-heavy tiles fall through.
     // (measured: small tiles only; cfg4/cfg5's larger tiles are slower with it)
-    if (CAPM <= 512 && levels >= 2 && msd_sort_tile<T, CAPM>(s, total, width)) return 1;
+    if constexpr (CAPM <= 512)
+        if (levels >= 2 && msd_sort_tile<T, CAPM>(s, total, width)) return 1;
     // pad key = 2^bits - 1 >= every key (<= width-1); pads sit after `total`
     // and the sort is stable, so real entries keep the first `total` slots.
     const int bits = bit_length(width > 1 ? width - 1 : 1);
     constexpr int RB = MergeShared<T, CAPM>::RB;
     const int passes = (bits + RB - 1) / RB;
-    if (levels > passes + 1) {  // measured: cfg4 (5 levels vs 4 passes) prefers merge
+    // measured: cfg4 (5 levels vs 4 passes) prefers merge
+    if (levels > passes + 1 || R > MergeShared<T, CAPM>::MAXRUNS) {
         radix_sort_tile<T, CAPM>(s, total, bits);
         return 0;
     }
@@ -375,7 +385,7 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
                                                 double* __restrict__ cval) {
     constexpr int NW = T / 32;
     constexpr int R = (CAPM + T - 1) / T;
-    static_assert(R * NW <= T && R * NW <= CAPM / 2, "row/warp counters");
+    static_assert(R * NW <= T && R * NW <= MergeShared<T, CAPM>::NHIST, "row/warp counters");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t* K = s.key(b);
     const uint16_t* X = s.idx(b);

@@ -25,7 +25,6 @@
 //  Symbolic runs K3/K4 without values to get exact per-row counts (exact
 //  allocation as the reference), then an int64 scan gives row_ptr.
 #include "esc.cuh"
-#include "heavy.cuh"
 #include "merge.cuh"
 
 #include <cub/block/block_radix_sort.cuh>
@@ -110,7 +109,7 @@ __global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64
 // K2: heavy-row planner
 // ---------------------------------------------------------------------------
 constexpr int PLAN_T = 256;
-__constant__ int kWinCapDev[NWCLS] = {4096, 2048, 512};
+__constant__ int kWinCapDev[NWCLS] = {4096, 3072, 2048, 512};
 constexpr int PLAN_U = 8;  // B-row chunks of 32 loaded ahead per warp
 constexpr uint32_t DENSE_BIT = 0x80000000u;
 
@@ -382,26 +381,6 @@ __global__ void start_size_kernel(Mats m, const int32_t* __restrict__ heavy, int
     sz[t] = e <= per_row_cap ? e : 0;
 }
 
-// Split heavy rows: A-row length <= HDMAX -> cursor list (with products as
-// the LPT sort key), else -> mega list (planned windows).
-__global__ void split_heavy_kernel(Mats m, const int32_t* __restrict__ heavy, int64_t nh,
-                                   int64_t rb, const int64_t* __restrict__ prod,
-                                   int64_t* __restrict__ keys, int32_t* __restrict__ vals,
-                                   int32_t* __restrict__ mega,
-                                   unsigned long long* __restrict__ cnt, int64_t dmax) {
-    const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
-    if (t >= nh) return;
-    const int32_t row = heavy[t];
-    const int64_t d = m.arp[row + 1] - m.arp[row];
-    if (d <= dmax) {
-        const unsigned long long i = atomicAdd(&cnt[0], 1ull);
-        keys[i] = prod[row - rb];
-        vals[i] = row;
-    } else {
-        mega[atomicAdd(&cnt[1], 1ull)] = row;
-    }
-}
-
 // Window ids by category (sparse tile class 0..NWCLS-1, dense NWCLS):
 // counts, then a scatter from per-category cursors (block-aggregated).
 __global__ void window_cat_count_kernel(const uint8_t* __restrict__ cat, int64_t nw,
@@ -552,7 +531,7 @@ __global__ void __launch_bounds__(T) esc_tile_kernel(Mats m, const int32_t* __re
 // K3': merge-based exact numeric tile and hash-count symbolic tile
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
-__global__ void __launch_bounds__(T, T >= 256 ? 2 : 4) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? 2 : 4)) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
                                                       const Window* __restrict__ wins, OutCtx out) {
     using S = MergeShared<T, CAPM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -941,18 +920,6 @@ void launch_dense(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, co
 
 }  // namespace
 
-// Heavy rows with A-row length <= this are walked by the cursor kernel;
-// BSP_HEAVY_CURSOR=<dmax> enables it (default 0: planned windows, measured
-// faster on cfg5 — see DESIGN.md).
-static int64_t heavy_cursor_dmax() {
-    static const int64_t v = [] {
-        const char* e = std::getenv("BSP_HEAVY_CURSOR");
-        const long long x = e ? std::atoll(e) : 0;
-        return static_cast<int64_t>(std::min<long long>(std::max<long long>(x, 0), HDMAX));
-    }();
-    return v;
-}
-
 Mats make_mats(const bsp_csr* A, const bsp_csr* B) {
     return Mats{A->row_ptr, A->col_idx, A->values, B->row_ptr, B->col_idx, B->values,
                 static_cast<int32_t>(B->ncols)};
@@ -997,41 +964,10 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         BSP_LAUNCH(h, bucket_kernel, static_cast<unsigned>(div_up(n, 256)), 256, 0, cls.p, rb, n,
                    cursor.p, plan.lists.p);
     }
-    // Heavy rows: A-row length <= HDMAX -> one CTA walks the row with cursors
-    // (longest rows first); longer ("mega") rows -> planned column windows.
-    const int64_t nh_all = plan.class_count[NCLS - 1];
-    int64_t nh = 0;
-    DBuf<int32_t> mega;
-    if (nh_all > 0) {
-        const int32_t* heavy_all = plan.lists.p + plan.class_off[NCLS - 1];
-        DBuf<int64_t> keys(h, nh_all), keys2(h, nh_all);
-        DBuf<int32_t> vals(h, nh_all);
-        plan.hcur = DBuf<int32_t>(h, nh_all);
-        mega = DBuf<int32_t>(h, nh_all);
-        DBuf<unsigned long long> cnt(h, 2);
-        BSP_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * sizeof(unsigned long long), h->stream));
-        BSP_LAUNCH(h, split_heavy_kernel, static_cast<unsigned>(div_up(nh_all, 256)), 256, 0, m,
-                   heavy_all, nh_all, rb, prod_out, keys.p, vals.p, mega.p, cnt.p,
-                   heavy_cursor_dmax());
-        unsigned long long hcnt[2];
-        d2h(h, hcnt, cnt.p, 2);
-        sync(h);
-        plan.nhcur = static_cast<int64_t>(hcnt[0]);
-        nh = static_cast<int64_t>(hcnt[1]);
-        if (plan.nhcur > 0) {
-            size_t tmp = 0;
-            BSP_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, keys.p, keys2.p, vals.p,
-                                                               plan.hcur.p, plan.nhcur, 0, 64,
-                                                               h->stream));
-            DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
-            BSP_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.p, tmp, keys.p, keys2.p, vals.p,
-                                                               plan.hcur.p, plan.nhcur, 0, 64,
-                                                               h->stream));
-            ++h->launches;
-        }
-    }
+    // Heavy rows: planned column windows.
+    const int64_t nh = plan.class_count[NCLS - 1];
     if (nh > 0) {
-        const int32_t* heavy = mega.p;
+        const int32_t* heavy = plan.lists.p + plan.class_off[NCLS - 1];
         int log_binw = LOG_WD;
         while (div_up(m.ncols, int64_t{1} << log_binw) > MAXBINS) ++log_binw;
         const int32_t nbins = static_cast<int32_t>(div_up(m.ncols, int64_t{1} << log_binw));
@@ -1146,35 +1082,18 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
 }
 
 template <bool NUMERIC>
-void launch_heavy(bsp_handle h, const Mats& m, const int32_t* rows, int64_t n, const OutCtx& out) {
-    if (n <= 0) return;
-    constexpr int T = 256, CAPM = 4096;
-    if (NUMERIC) {
-        auto k = heavy_numeric_kernel<T, CAPM>;
-        set_smem(k, sizeof(HeavyNumShared<T, CAPM>));
-        BSP_LAUNCH_AS(h, "heavy_numeric<256,4096>", k, static_cast<unsigned>(n), T,
-                      sizeof(HeavyNumShared<T, CAPM>), m, rows, out);
-    } else {
-        auto k = heavy_symbolic_kernel<T, CAPM>;
-        set_smem(k, sizeof(HeavySymShared<T, CAPM>));
-        BSP_LAUNCH_AS(h, "heavy_symbolic<256,4096>", k, static_cast<unsigned>(n), T,
-                      sizeof(HeavySymShared<T, CAPM>), m, rows, out);
-    }
-}
-
-template <bool NUMERIC>
 void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCtx& out) {
     const Mats m = plan.with_starts(m0);
-    // longest work first: cursor-walked heavy rows, then the light classes
-    launch_heavy<NUMERIC>(h, m, plan.hcur.p, plan.nhcur, out);
+    // longest work first: the light classes from the largest, then windows
     for (int c = NCLS - 2; c >= 1; --c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
     auto wl = [&](int k) { return plan.sparse_ids.p + plan.wcls_off[k]; };
     auto wn = [&](int k) { return plan.wcls_off[k + 1] - plan.wcls_off[k]; };
-    static_assert(NWCLS == 3, "one launch per window tile class");
+    static_assert(NWCLS == 4, "one launch per window tile class");
     launch_tile<256, 4096, NUMERIC>(h, m, wl(0), wn(0), plan.wins.p, out);
-    launch_tile<128, 2048, NUMERIC>(h, m, wl(1), wn(1), plan.wins.p, out);
-    launch_tile<64, 512, NUMERIC>(h, m, wl(2), wn(2), plan.wins.p, out);
+    launch_tile<256, 3072, NUMERIC>(h, m, wl(1), wn(1), plan.wins.p, out);
+    launch_tile<128, 2048, NUMERIC>(h, m, wl(2), wn(2), plan.wins.p, out);
+    launch_tile<64, 512, NUMERIC>(h, m, wl(3), wn(3), plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
 
