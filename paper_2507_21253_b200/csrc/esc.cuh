@@ -11,11 +11,6 @@ namespace bsp {
 
 constexpr int CAP = 4096;     // max products of one sparse tile (smem ESC)
 constexpr int CAPH = CAP / 2;
-// Window packing: bins with > CAPB products get their own window; runs of
-// smaller bins are cut where floor(prefix / CAPG) changes, so a window holds
-// < CAPG + CAPB = CAP products and averages ~CAPG.
-constexpr int CAPB = CAP / 4;
-constexpr int CAPG = CAP - CAPB;
 // Sparse-window tile classes (descending): a window runs in the smallest
 // tile that holds its products (CUB's block sort always sorts the full tile).
 // The 3072 class keeps 256 threads and is sized (≈73 KB smem, 85 registers)

@@ -175,9 +175,7 @@ __device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& 
 }
 
 // K2a: per heavy row, a product histogram over `nbins` column bins, then the
-// window cut: a bin with > capb products gets its own window (dense when
-// > CAP), runs of smaller bins are cut where floor(prefix / capg) changes or
-// after a big bin.  Writes the window count and the descriptors
+// greedy window cut (below).  Writes the window count and the descriptors
 // {c0 | DENSE_BIT, product prefix} (+ sentinel {ncols, P}) at desc[doff[h]].
 __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
                                                             const int32_t* __restrict__ heavy,
@@ -185,7 +183,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
                                                             int32_t* __restrict__ nwin,
                                                             const int64_t* __restrict__ doff,
                                                             uint2* __restrict__ desc,
-                                                            int32_t capb, int32_t capg) {
+                                                            int32_t capg) {
     __shared__ PlanCountShared s;
     const int32_t hrow = blockIdx.x;
     const int32_t row = heavy[hrow];
@@ -211,51 +209,28 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
         }
     });
     __syncthreads();
-    // Per-bin counts in blocked arrangement (ITEMS bins per thread).
-    constexpr int ITEMS = MAXBINS / PLAN_T;
-    int32_t excl[ITEMS], cnt[ITEMS];
-    int32_t local = 0;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int b = threadIdx.x * ITEMS + i;
-        cnt[i] = b < nbins ? s.hist[b] : 0;
-        excl[i] = local;
-        local += cnt[i];
-    }
-    int32_t base, tot;
-    cub::BlockScan<int32_t, PLAN_T>(s.scan).ExclusiveSum(local, base, tot);
-    __syncthreads();
-    bool starts[ITEMS];
-    int32_t mine = 0;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int b = threadIdx.x * ITEMS + i;
-        const int32_t pre = base + excl[i];
-        bool st = false;
-        if (b < nbins) {
-            st = (b == 0) || cnt[i] > capb;
-            if (!st) {
-                const int32_t pc = s.hist[b - 1];
-                st = (pc > capb) || ((pre - pc) / capg != pre / capg);
-            }
-        }
-        starts[i] = st;
-        mine += st;
-    }
-    int32_t wbase, wtot;
-    cub::BlockScan<int32_t, PLAN_T>(s.scan).ExclusiveSum(mine, wbase, wtot);
-    uint2* dd = desc + doff[hrow];
-    int32_t w = wbase;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        if (!starts[i]) continue;
-        const uint32_t c0 = static_cast<uint32_t>((threadIdx.x * ITEMS + i) << log_binw);
-        dd[w++] = make_uint2(c0 | (cnt[i] > CAP ? DENSE_BIT : 0u),
-                             static_cast<uint32_t>(base + excl[i]));
-    }
+    // Greedy cut over the bins (one thread; ~1024 bins): a window grows while
+    // it holds <= capg products; a bin above capg stands alone (dense above
+    // CAP), and the bin after it starts a new window.  Every packed window
+    // thus fits the capg-product tile.
     if (threadIdx.x == 0) {
-        nwin[hrow] = wtot;
-        dd[wtot] = make_uint2(static_cast<uint32_t>(m.ncols), static_cast<uint32_t>(tot));
+        uint2* dd = desc + doff[hrow];
+        int32_t nw = 0, acc = 0, pre = 0;
+        bool prev_big = false;
+        for (int b = 0; b < nbins; ++b) {
+            const int32_t c = s.hist[b];
+            if (b == 0 || prev_big || c > capg || acc + c > capg) {
+                dd[nw++] = make_uint2(static_cast<uint32_t>(b << log_binw) | (c > CAP ? DENSE_BIT : 0u),
+                                      static_cast<uint32_t>(pre));
+                acc = c;
+            } else {
+                acc += c;
+            }
+            prev_big = c > capg;
+            pre += c;
+        }
+        nwin[hrow] = nw;
+        dd[nw] = make_uint2(static_cast<uint32_t>(m.ncols), static_cast<uint32_t>(pre));
     }
 }
 
@@ -348,12 +323,12 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
     }
 }
 
-// Upper bound on a heavy row's windows (+1 sentinel descriptor):
-// <= P/(capb+1) big bins, each may also start the run after it, and the
-// runs are cut at most P/capg times.
+// Upper bound on a heavy row's windows (+1 sentinel descriptor): any two
+// consecutive greedy windows hold > capg products together, so
+// nwin < 2P/capg + 2.
 __global__ void plan_bound_kernel(const int32_t* __restrict__ heavy, int64_t nh, int64_t rb,
                                   const int64_t* __restrict__ prod, int32_t nbins,
-                                  int32_t capb, int32_t capg, int64_t* __restrict__ bound) {
+                                  int32_t capg, int64_t* __restrict__ bound) {
     const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
     if (t > nh) return;
     if (t == nh) {
@@ -361,7 +336,7 @@ __global__ void plan_bound_kernel(const int32_t* __restrict__ heavy, int64_t nh,
         return;
     }
     const int64_t P = prod[heavy[t] - rb];
-    bound[t] = ::min(2 * (P / (capb + 1)) + P / capg + 2, int64_t{nbins}) + 1;
+    bound[t] = ::min(2 * (P / capg) + 3, int64_t{nbins}) + 1;
 }
 
 // Size of each heavy row's start table ((windows+1) x A-row length), or 0
@@ -975,25 +950,24 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                 "planner: heavy rows need ncols <= 16M (MAXBINS*WD) in this build");
         DBuf<int32_t> nwin(h, nh + 1);
         BSP_CUDA(cudaMemsetAsync(nwin.p, 0, (nh + 1) * sizeof(int32_t), h->stream));
-        // window packing target (products): runs of small bins are cut every
-        // capg products, bins above capb stand alone (BSP_WTARGET to tune)
+        // window packing capacity (products; BSP_WTARGET to tune): the 3072
+        // tile runs 3 CTAs/SM
         static const int32_t capg = [] {
             const char* e = std::getenv("BSP_WTARGET");
-            const int v = e ? std::atoi(e) : CAPG;
-            return std::max(64, std::min(v, CAPG));
+            const int v = e ? std::atoi(e) : 3072;
+            return std::max(64, std::min(v, CAP));
         }();
-        const int32_t capb = std::min(CAPB, capg / 3);
         // window descriptors: per heavy row a slot sized by the window bound
         DBuf<int64_t> dbound(h, nh + 1), doff(h, nh + 1);
         BSP_LAUNCH(h, plan_bound_kernel, static_cast<unsigned>(div_up(nh + 1, 256)), 256, 0,
-                   heavy, nh, rb, prod_out, nbins, capb, capg, dbound.p);
+                   heavy, nh, rb, prod_out, nbins, capg, dbound.p);
         exclusive_scan_i64(h, dbound.p, doff.p, nh + 1);
         int64_t ndesc = 0;
         d2h(h, &ndesc, doff.p + nh, 1);
         sync(h);
         DBuf<uint2> desc(h, ndesc);
         BSP_LAUNCH(h, plan_count_kernel, static_cast<unsigned>(nh), PLAN_T, 0, m, heavy, nbins,
-                   log_binw, nwin.p, doff.p, desc.p, capb, capg);
+                   log_binw, nwin.p, doff.p, desc.p, capg);
         DBuf<int64_t> woff(h, nh + 1);
         exclusive_scan_i32_to_i64(h, nwin.p, woff.p, nh + 1);
         // per-(window, segment) start tables, bounded per row and in total
