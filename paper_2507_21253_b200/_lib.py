@@ -59,7 +59,7 @@ class bsp_candidate(C.Structure):
 
 
 class bsp_exec_stats(C.Structure):
-    _fields_ = [("products", i64), ("nnz_out", i64), ("units", i64 * 8),
+    _fields_ = [("products", i64), ("nnz_out", i64), ("units", i64 * 16),
                 ("kernels_launched", i32), ("chunks", i32)]
 
 

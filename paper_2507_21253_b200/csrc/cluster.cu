@@ -703,7 +703,7 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         const Mats m = make_mats(&acsr, B);
         RowwisePlan plan;  // rows outside cluster tiles (incl. heavy windows)
         build_plan(h, m, 0, n, skip.p, plan, nullptr);
-        h->stats.units[5] = cnt[1] + cnt[2] + cnt[3];  // cluster tiles
+        h->stats.units[10] = cnt[1] + cnt[2] + cnt[3];  // cluster tiles
         DBuf<int64_t> row_nnz(h, n + 1);
         BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
         // Symbolic: C's row structure does not depend on the clustering, so the

@@ -878,7 +878,8 @@ void launch_light(bsp_handle h, int cls, const Mats& m, const int32_t* ids, int6
         case 1: launch_tile<32, 128, NUMERIC>(h, m, ids, n, nullptr, out); break;
         case 2: launch_tile<64, 512, NUMERIC>(h, m, ids, n, nullptr, out); break;
         case 3: launch_tile<128, 2048, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 4: launch_tile<256, 4096, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 4: launch_tile<256, 3072, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 5: launch_tile<256, 4096, NUMERIC>(h, m, ids, n, nullptr, out); break;
         default: break;
     }
 }
@@ -1050,9 +1051,9 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
             sort_list(plan.dense_ids.p, plan.ndense);
         }
     }
-    for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];  // [5] = heavy rows
-    h->stats.units[6] = plan.nsparse;
-    h->stats.units[7] = plan.ndense;
+    for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];  // [6] = heavy rows
+    h->stats.units[8] = plan.nsparse;
+    h->stats.units[9] = plan.ndense;
 }
 
 template <bool NUMERIC>

@@ -517,8 +517,11 @@ int bsp_spgemm_topk(bsp_handle h, const bsp_csr* A, const bsp_csr* At, int32_t t
                            rn.p, wj.p, ws.p, wn.p);
         launch_topk<128, 16>(h, m, plan.lists.p + co[3], cc[3], nullptr, topk, jacc_th, rj.p, rs.p,
                              rn.p, wj.p, ws.p, wn.p);
-        launch_topk<256, 16>(h, m, plan.lists.p + co[4], cc[4], nullptr, topk, jacc_th, rj.p, rs.p,
-                             rn.p, wj.p, ws.p, wn.p);
+        // light classes 4 and 5 (<= 3072, <= 4096 products) are adjacent in
+        // the row list and share the 4096-product tile
+        static_assert(NCLS == 7, "top-k launches one tile per light class");
+        launch_topk<256, 16>(h, m, plan.lists.p + co[4], cc[4] + cc[5], nullptr, topk, jacc_th,
+                             rj.p, rs.p, rn.p, wj.p, ws.p, wn.p);
         if (plan.nwin > 0) {
             const Mats mw = plan.with_starts(m);
             launch_topk<256, 16>(h, mw, plan.sparse_ids.p, plan.nsparse, plan.wins.p, topk, jacc_th,
