@@ -28,9 +28,9 @@ template <int T, int CAPM>
 struct MergeShared {
     static constexpr int NP = CAPM + CAPM / 32 + 1;
     // radix digit bits: CUB's rank storage is T x 2^RB / 2 words whatever the
-    // tile size, so the 3072-product tile (sized for 3 CTAs/SM) uses 5-bit
-    // digits (16 KB) and the power-of-two tiles 6-bit digits
-    static constexpr int RB = (CAPM & (CAPM - 1)) == 0 ? 6 : 5;
+    // tile size, so 256-thread tiles of <= 3072 products (sized for 3-4
+    // CTAs/SM) use 5-bit digits (16 KB), the others 6-bit digits
+    static constexpr int RB = (T >= 256 && CAPM <= 3072) ? 5 : 6;
     using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, RB>;
     // run offsets: tiles with more runs than this use the radix sort
     static constexpr int MAXRUNS = CAPM < 1024 ? CAPM : 1024;

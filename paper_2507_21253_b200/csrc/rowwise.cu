@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(T) esc_tile_kernel(Mats m, const int32_t* __re
 // K3': merge-based exact numeric tile and hash-count symbolic tile
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
-__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? 2 : 4)) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : 4)) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
                                                       const Window* __restrict__ wins, OutCtx out) {
     using S = MergeShared<T, CAPM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -877,7 +877,7 @@ void launch_light(bsp_handle h, int cls, const Mats& m, const int32_t* ids, int6
     switch (cls) {
         case 1: launch_tile<32, 128, NUMERIC>(h, m, ids, n, nullptr, out); break;
         case 2: launch_tile<64, 512, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 3: launch_tile<128, 2048, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 3: launch_tile<256, 2048, NUMERIC>(h, m, ids, n, nullptr, out); break;
         case 4: launch_tile<256, 3072, NUMERIC>(h, m, ids, n, nullptr, out); break;
         case 5: launch_tile<256, 4096, NUMERIC>(h, m, ids, n, nullptr, out); break;
         default: break;
@@ -1067,7 +1067,7 @@ void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCt
     static_assert(NWCLS == 4, "one launch per window tile class");
     launch_tile<256, 4096, NUMERIC>(h, m, wl(0), wn(0), plan.wins.p, out);
     launch_tile<256, 3072, NUMERIC>(h, m, wl(1), wn(1), plan.wins.p, out);
-    launch_tile<128, 2048, NUMERIC>(h, m, wl(2), wn(2), plan.wins.p, out);
+    launch_tile<256, 2048, NUMERIC>(h, m, wl(2), wn(2), plan.wins.p, out);
     launch_tile<64, 512, NUMERIC>(h, m, wl(3), wn(3), plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
