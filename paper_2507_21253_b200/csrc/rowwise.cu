@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
     using S = HashShared<T, CAPM, STAGED>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S& s = *reinterpret_cast<S*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     constexpr int NW = T / 32;
     constexpr int TS = S::TS;
     constexpr int LG = 31 - __builtin_clz(static_cast<unsigned>(TS));
@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         };
         if constexpr (STAGED) {
             int e, we, q;
-            warp_slice_begin(s.poff, nr, ct, NW, e, we, q);
+            warp_slice_begin(s.poff, nr, ct, T / 32, e, we, q);
             for (; e < we; e += 32) {
                 while (s.poff[q + 1] <= e) ++q;
                 cp_async4(&s.stage[e], m.bcol + s.pstart[q] + (e - s.poff[q]));
@@ -846,9 +846,10 @@ void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, con
         set_smem(k, sizeof(S));
         BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
     } else {
+        // BSP_HASH=plain: insert straight from the loads (no staging)
         static const bool staged = [] {
-            const char* e = std::getenv("BSP_HASH_STAGE");
-            return !(e && e[0] == '0');
+            const char* e = std::getenv("BSP_HASH");
+            return !(e && std::string(e) == "plain");
         }();
         static const std::string nm_row = "hash_count<" + std::to_string(T) + "," +
                                           std::to_string(CAPM) + ">";
