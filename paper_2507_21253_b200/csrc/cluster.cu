@@ -15,6 +15,7 @@
 // to spgemm_rowwise(cluster_to_csr(A), B).  Singleton clusters and clusters
 // with more than CAP products are routed to the row-wise bins.
 #include "esc.cuh"
+#include "merge.cuh"
 
 #include <algorithm>
 #include <numeric>
@@ -145,8 +146,8 @@ __global__ void cluster_to_csr_kernel(const int32_t* __restrict__ sizes,
 // ---------------------------------------------------------------------------
 // cluster products + routing
 // ---------------------------------------------------------------------------
-constexpr int NCC = 4;  // 0: row-wise bins, 1: <=512, 2: <=2048, 3: <=4096 products
-__constant__ int kClusterCap[NCC] = {0, 512, 2048, 4096};
+constexpr int NCC = 5;  // 0: row-wise classes, 1: <=512, 2: <=2048, 3: <=3072, 4: <=4096 products
+__constant__ int kClusterCap[NCC] = {0, 512, 2048, 3072, 4096};
 
 __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
                                         uint8_t* __restrict__ ccls, uint8_t* __restrict__ row_skip,
@@ -204,52 +205,41 @@ __global__ void cluster_bucket_kernel(const uint8_t* __restrict__ ccls, int64_t 
 }
 
 // ---------------------------------------------------------------------------
-// cluster tile kernel (composite-key radix tile; measured fastest of the
-// cluster tiles tried — DESIGN.md §4)
+// cluster tile kernel: one CTA per cluster on the row-tile machinery
+// (merge.cuh).  Expansion: for every merged column p (ascending k) the B row
+// is loaded once and its entries are written for every live member l as the
+// composite key (l << cbits | j) with value a[p][l] * b — each (p, l) block is
+// one sorted run, runs in p-major order.  The stable sort by composite key
+// (merge of the runs, CUB radix, or MSD for small tiles — sort_tile) then
+// leaves every (member, column) group in ascending k, so each head sums its
+// group left to right from 0.0 exactly as row-wise does (= the reference,
+// cluster_spgemm.hpp:129-143), and C is written directly as CSR over the
+// original rows.
 // ---------------------------------------------------------------------------
-template <int T, int I, bool NUMERIC>
-struct ClusterShared {
-    static constexpr int CAPT = T * I;
-    using Sort = cub::BlockRadixSort<uint32_t, T, I, uint32_t>;
-    using Scan = cub::BlockScan<int32_t, T>;
-    uint32_t keys[CAPT];
-    double vals[NUMERIC ? CAPT : 1];
-    union {
-        typename Sort::TempStorage sort;
-        uint32_t sidx[CAPT];
-    } u;
-    typename Scan::TempStorage scan;
-    int64_t pstart[T];
-    int64_t pvb[T];
-    int32_t plen[T];
-    int32_t poff[T];
-    uint32_t pmask[T];
-    int32_t mcnt[MAXK];
-    int32_t mstart[MAXK];
-    int64_t mbase[MAXK];
-};
-
-template <int T, int I, bool NUMERIC>
-__global__ void __launch_bounds__(T) cluster_tile_kernel(ClusterMats m, const int32_t* __restrict__ ids,
-                                                         int cbits, int64_t* __restrict__ row_nnz,
-                                                         const int64_t* __restrict__ crp,
-                                                         int32_t* __restrict__ ocol,
-                                                         double* __restrict__ oval) {
-    using S = ClusterShared<T, I, NUMERIC>;
+template <int T, int CAPM>
+__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : 4))
+    cluster_tile_kernel(ClusterMats m, const int32_t* __restrict__ ids, int cbits,
+                        const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
+                        double* __restrict__ oval) {
+    using S = MergeShared<T, CAPM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S& s = *reinterpret_cast<S*>(smem_raw);
+    __shared__ int32_t s_mstart[MAXK];
+    __shared__ int64_t s_mbase[MAXK];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = T / 32;
+    constexpr int MAXRUNS = S::MAXRUNS;
     const int32_t c = ids[blockIdx.x];
     const int K = m.sizes[c];
     const int64_t u0 = m.ccp[c], u1 = m.ccp[c + 1];
     const int64_t vbase = m.vptr[c];
-    const uint32_t colmask = (1u << cbits) - 1u;
-    if (tid < MAXK) s.mcnt[tid] = 0;
-    int total = 0;
+    if (tid < K) s_mbase[tid] = crp[m.row_map[m.member_ptr[c] + tid]];
+    uint2* slot_sm = reinterpret_cast<uint2*>(s.pav);  // per slot {segment length, member mask}
+    uint16_t* slot_rb = s.ro(1);                       // per slot first run index (idle buffer)
+    int total = 0, nruns = 0;
     for (int64_t uc = u0; uc < u1; uc += T) {
         const int64_t u = uc + tid;
-        int len = 0, seg = 0;
+        int seg = 0;
         int64_t start = 0;
         uint32_t msk = 0;
         if (u < u1) {
@@ -257,140 +247,140 @@ __global__ void __launch_bounds__(T) cluster_tile_kernel(ClusterMats m, const in
             msk = __ldg(m.mask + u);
             start = __ldg(m.brp + k);
             seg = static_cast<int>(__ldg(m.brp + k + 1) - start);
-            len = seg * __popc(msk);
         }
-        int off, chunk;
-        typename S::Scan(s.scan).ExclusiveSum(len, off, chunk);
+        const int nl = seg > 0 ? __popc(msk) : 0;
+        // packed scan: low 16 bits product offset, high 16 bits run index
+        const int packed = seg * nl | (nl << 16);
+        int off, agg;
+        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
         s.pstart[tid] = start;
-        s.plen[tid] = seg;
-        s.poff[tid] = total + off;
-        s.pmask[tid] = msk;
-        s.pvb[tid] = vbase + (u - u0) * K;
+        s.poff[tid] = total + (off & 0xffff);
+        slot_sm[tid] = make_uint2(static_cast<uint32_t>(seg), nl ? msk : 0u);
+        slot_rb[tid] = static_cast<uint16_t>(::min(nruns + (off >> 16), MAXRUNS));
         __syncthreads();
+        // run offsets: slot t's live members, in ascending member order
+        {
+            const uint2 sm = slot_sm[tid];
+            uint32_t mm = sm.y;
+            int r = slot_rb[tid];
+            int o = s.poff[tid];
+            while (mm && r < MAXRUNS) {
+                mm &= mm - 1;
+                s.ro(0)[r++] = static_cast<uint16_t>(o);
+                o += static_cast<int>(sm.x);
+            }
+        }
         const int nslots = static_cast<int>(::min(int64_t{T}, u1 - uc));
         for (int slot = warp; slot < nslots; slot += NW) {
-            const int l_seg = s.plen[slot];
-            const uint32_t msk2 = s.pmask[slot];
-            if (l_seg == 0 || msk2 == 0) continue;
+            const uint2 sm = slot_sm[slot];
+            if (sm.y == 0) continue;
+            const int l_seg = static_cast<int>(sm.x);
             const int64_t st = s.pstart[slot];
             const int o = s.poff[slot];
-            const int64_t vb = s.pvb[slot];
+            const int64_t vb = vbase + (uc + slot - u0) * K;
             for (int q = lane; q < l_seg; q += 32) {
-                // one global load of the B entry, reused by every live member
+                // one load of the B entry, reused by every live member
                 const uint32_t j = static_cast<uint32_t>(__ldg(m.bcol + st + q));
-                double bv = 0.0;
-                if (NUMERIC) bv = __ldg(m.bval + st + q);
-                uint32_t mm = msk2;
-                int r = 0;
+                const double bv = __ldg(m.bval + st + q);
+                uint32_t mm = sm.y;
+                int pos = o + q;
                 while (mm) {
                     const int l = __ffs(mm) - 1;
                     mm &= mm - 1;
-                    const int pos = o + r * l_seg + q;
-                    s.keys[pos] = (static_cast<uint32_t>(l) << cbits) | j;
-                    if (NUMERIC) s.vals[pos] = __dmul_rn(__ldg(m.aval + vb + l), bv);
-                    ++r;
+                    s.key(0)[PADI(pos)] = (static_cast<uint32_t>(l) << cbits) | j;
+                    s.idx(0)[PADI(pos)] = static_cast<uint16_t>(pos);
+                    s.val[pos] = __dmul_rn(__ldg(m.aval + vb + l), bv);
+                    pos += l_seg;
                 }
             }
         }
-        total += chunk;
+        total += agg & 0xffff;
+        nruns += agg >> 16;
         __syncthreads();
     }
-    const uint32_t pad = static_cast<uint32_t>(K) << cbits;
-    const int bits = bit_length(pad);
-    uint32_t k[I], v[I];
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        const int e = tid * I + i;
-        k[i] = e < total ? s.keys[e] : pad;
-        v[i] = static_cast<uint32_t>(e);
-    }
-    __syncthreads();
-    typename S::Sort(s.u.sort).Sort(k, v, 0, bits);
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        s.keys[tid * I + i] = k[i];
-        s.u.sidx[tid * I + i] = v[i];
-    }
-    __syncthreads();
-    bool head[I];
-    int nh = 0;
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        const int e = tid * I + i;
-        head[i] = e < total && (e == 0 || k[i] != s.keys[e - 1]);
-        nh += head[i];
-        if (head[i]) atomicAdd(&s.mcnt[k[i] >> cbits], 1);
-    }
-    int hoff, tile_cnt;
-    typename S::Scan(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
-    __syncthreads();
-    if (!NUMERIC) {
-        if (tid < K) row_nnz[m.row_map[m.member_ptr[c] + tid]] = s.mcnt[tid];
-        return;
-    }
     if (tid == 0) {
-        int acc = 0;
-        for (int l = 0; l < K; ++l) {
-            s.mstart[l] = acc;
-            acc += s.mcnt[l];
-        }
-    }
-    if (tid < K) s.mbase[tid] = crp[m.row_map[m.member_ptr[c] + tid]];
-    double res[I];
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        res[i] = 0.0;
-        if (head[i]) {
-            double acc = 0.0;
-            int e = tid * I + i;
-            do {
-                acc = __dadd_rn(acc, s.vals[s.u.sidx[e]]);
-                ++e;
-            } while (e < total && s.keys[e] == k[i]);
-            res[i] = acc;
-        }
+        if (nruns <= MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
+        s.nruns = nruns;
     }
     __syncthreads();
-    int r = hoff;
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(K) << cbits);
+
+    // reduction (element-strided, as reduce_and_write) with member -> row map
+    constexpr int R = (CAPM + T - 1) / T;
+    const uint32_t* KS = s.key(b);
+    const uint16_t* X = s.idx(b);
+    int* cnt = reinterpret_cast<int*>(s.hist);
+    const int nrows = (total + T - 1) / T;
+    unsigned hm[R];
 #pragma unroll
-    for (int i = 0; i < I; ++i) {
-        if (head[i]) {
-            s.keys[r] = k[i];
-            s.vals[r] = res[i];
-            ++r;
-        }
+    for (int r = 0; r < R; ++r) {
+        const int o = r * T + tid;
+        const bool h = o < total && (o == 0 || KS[PADI(o)] != KS[PADI(o - 1)]);
+        hm[r] = __ballot_sync(0xffffffffu, h);
+        if (lane == 0 && r < nrows) cnt[r * NW + warp] = __popc(hm[r]);
     }
     __syncthreads();
-    for (int e = tid; e < tile_cnt; e += T) {
-        const uint32_t key = s.keys[e];
+    const int v = tid < nrows * NW ? cnt[tid] : 0;
+    int pre, tile_cnt;
+    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(v, pre, tile_cnt);
+    __syncthreads();
+    if (tid < nrows * NW) cnt[tid] = pre;
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+    int rank[R];
+    double res[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        rank[r] = -1;
+        res[r] = 0.0;
+        if (!((hm[r] >> lane) & 1u)) continue;
+        const int o = r * T + tid;
+        rank[r] = cnt[r * NW + warp] + __popc(hm[r] & below);
+        const uint32_t key = KS[PADI(o)];
+        if (o == 0 || (KS[PADI(o - 1)] >> cbits) != (key >> cbits))
+            s_mstart[key >> cbits] = rank[r];  // first entry of this member
+        double acc = 0.0;
+        int e = o;
+        do {
+            acc = __dadd_rn(acc, s.val[X[PADI(e)]]);
+            ++e;
+        } while (e < total && KS[PADI(e)] == key);
+        res[r] = acc;
+    }
+    __syncthreads();
+    const uint32_t colmask = (1u << cbits) - 1u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (rank[r] < 0) continue;
+        const uint32_t key = KS[PADI(r * T + tid)];
         const int l = static_cast<int>(key >> cbits);
-        const int64_t pos = s.mbase[l] + (e - s.mstart[l]);
+        const int64_t pos = s_mbase[l] + (rank[r] - s_mstart[l]);
         ocol[pos] = static_cast<int32_t>(key & colmask);
-        oval[pos] = s.vals[e];
+        oval[pos] = res[r];
     }
 }
 
-template <int T, int I, bool NUMERIC>
+template <int T, int CAPM>
 void launch_cluster(bsp_handle h, const ClusterMats& m, const int32_t* ids, int64_t n, int cbits,
-                    int64_t* row_nnz, const int64_t* crp, int32_t* ocol, double* oval) {
+                    const int64_t* crp, int32_t* ocol, double* oval) {
     if (n <= 0) return;
-    using S = ClusterShared<T, I, NUMERIC>;
-    auto k = cluster_tile_kernel<T, I, NUMERIC>;
-    static const std::string nm = std::string(NUMERIC ? "cluster_numeric<" : "cluster_symbolic<") +
-                                  std::to_string(T) + "x" + std::to_string(I) + ">";
+    using S = MergeShared<T, CAPM>;
+    auto k = cluster_tile_kernel<T, CAPM>;
+    static const std::string nm =
+        "cluster_numeric<" + std::to_string(T) + "," + std::to_string(CAPM) + ">";
     set_smem(k, sizeof(S));
-    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, cbits, row_nnz, crp, ocol,
-               oval);
+    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, cbits, crp,
+                  ocol, oval);
 }
 
-template <bool NUMERIC>
 void run_cluster_classes(bsp_handle h, const ClusterMats& m, const int32_t* lists,
-                         const int64_t* off, const int64_t* cnt, int cbits, int64_t* row_nnz,
-                         const int64_t* crp, int32_t* ocol, double* oval) {
-    launch_cluster<64, 8, NUMERIC>(h, m, lists + off[1], cnt[1], cbits, row_nnz, crp, ocol, oval);
-    launch_cluster<128, 16, NUMERIC>(h, m, lists + off[2], cnt[2], cbits, row_nnz, crp, ocol, oval);
-    launch_cluster<256, 16, NUMERIC>(h, m, lists + off[3], cnt[3], cbits, row_nnz, crp, ocol, oval);
+                         const int64_t* off, const int64_t* cnt, int cbits, const int64_t* crp,
+                         int32_t* ocol, double* oval) {
+    static_assert(NCC == 5, "one launch per cluster tile class");
+    launch_cluster<64, 512>(h, m, lists + off[1], cnt[1], cbits, crp, ocol, oval);
+    launch_cluster<256, 2048>(h, m, lists + off[2], cnt[2], cbits, crp, ocol, oval);
+    launch_cluster<256, 3072>(h, m, lists + off[3], cnt[3], cbits, crp, ocol, oval);
+    launch_cluster<256, 4096>(h, m, lists + off[4], cnt[4], cbits, crp, ocol, oval);
 }
 
 // access statistics (reference cluster_spgemm.hpp:26-45, counted at :129-135)
@@ -703,7 +693,7 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         const Mats m = make_mats(&acsr, B);
         RowwisePlan plan;  // rows outside cluster tiles (incl. heavy windows)
         build_plan(h, m, 0, n, skip.p, plan, nullptr);
-        h->stats.units[10] = cnt[1] + cnt[2] + cnt[3];  // cluster tiles
+        h->stats.units[10] = cnt[1] + cnt[2] + cnt[3] + cnt[4];  // cluster tiles
         DBuf<int64_t> row_nnz(h, n + 1);
         BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
         // Symbolic: C's row structure does not depend on the clustering, so the
@@ -726,8 +716,7 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         const int64_t nnz = read_scalar(h, rp.p + n);
         h->stats.nnz_out = nnz;
         ResultPayload pay(h, nnz);
-        run_cluster_classes<true>(h, cm, lists.p, off, cnt, cbits, nullptr, rp.p, pay.col_idx(),
-                                  pay.values());
+        run_cluster_classes(h, cm, lists.p, off, cnt, cbits, rp.p, pay.col_idx(), pay.values());
         plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values());
         C->nrows = n;
         C->ncols = B->ncols;
