@@ -213,6 +213,9 @@ int bsp_create(int device, bsp_handle* out) {
         h->sm_count = prop.multiProcessorCount;
         BSP_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         h->own_stream = true;
+        BSP_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        BSP_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        BSP_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
         for (cudaMemPool_t* pool : {&h->scratch_pool, &h->out_pool}) {
             cudaMemPoolProps props{};
             props.allocType = cudaMemAllocationTypePinned;
@@ -238,6 +241,12 @@ int bsp_destroy(bsp_handle h) {
         if (h->own_stream) cudaStreamDestroy(h->stream);
         // pools with live allocations (results still held by the caller) are
         // released by the driver once those are freed
+        if (h->side) {
+            cudaStreamSynchronize(h->side);
+            cudaStreamDestroy(h->side);
+        }
+        if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+        if (h->ev_join) cudaEventDestroy(h->ev_join);
         if (h->rb_host) cudaFreeHost(h->rb_host);
         if (h->scratch_pool) cudaMemPoolDestroy(h->scratch_pool);
         if (h->out_pool) cudaMemPoolDestroy(h->out_pool);

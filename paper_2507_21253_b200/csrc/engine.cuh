@@ -37,6 +37,10 @@ struct bsp_handle_s {
     // Mapped pinned buffer for small synchronous readbacks (see d2h).
     void* rb_host = nullptr;
     void* rb_dev = nullptr;
+    // Side stream for work that overlaps the main stream within one call
+    // (light-row symbolic during the heavy-row planner); fork/join events.
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace bsp {
@@ -74,6 +78,27 @@ void trace_launch(bsp_handle h, const char* name, long long grid);
 // Per-launch CUDA-event profiling (bsp_profile): -1 when disabled.
 int prof_begin(bsp_handle h);
 void prof_end(bsp_handle h, int slot, const char* name);
+
+// Launches inside this scope go to the handle's side stream (forked from and,
+// by the caller, joined back into the main stream).
+struct SideStream {
+    bsp_handle h;
+    cudaStream_t saved;
+    explicit SideStream(bsp_handle hh) : h(hh), saved(hh->stream) {
+        cuda_check(cudaEventRecord(h->ev_fork, saved), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "cudaStreamWaitEvent");
+        h->stream = h->side;
+    }
+    ~SideStream() {
+        cudaEventRecord(h->ev_join, h->side);
+        h->stream = saved;
+    }
+    SideStream(const SideStream&) = delete;
+    SideStream& operator=(const SideStream&) = delete;
+};
+inline void join_side(bsp_handle h) {
+    cuda_check(cudaStreamWaitEvent(h->stream, h->ev_join, 0), "cudaStreamWaitEvent");
+}
 
 // Stream-ordered device allocation from one of the handle's pools.
 enum class Pool { scratch, out };

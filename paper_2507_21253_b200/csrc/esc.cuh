@@ -173,6 +173,7 @@ struct RowwisePlan {
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
     DBuf<int32_t> starts; // planner per-(window, segment) start tables
+    bool light_sym_done = false;  // light rows counted on the side stream
     // Matrices as seen by the window kernels (start tables attached).
     Mats with_starts(const Mats& m) const {
         Mats r = m;
@@ -182,8 +183,10 @@ struct RowwisePlan {
 };
 
 Mats make_mats(const bsp_csr* A, const bsp_csr* B);
+// early_row_nnz (zeroed, optional): count the light rows' outputs there on the
+// handle's side stream while the heavy rows are planned (plan_symbolic joins).
 void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re, const uint8_t* skip,
-                RowwisePlan& plan, int64_t* prod_out);
+                RowwisePlan& plan, int64_t* prod_out, int64_t* early_row_nnz = nullptr);
 // Symbolic counts of a plan into row_nnz (NOT zeroed here) and win_nnz (allocated).
 void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t* row_nnz,
                    DBuf<int64_t>& win_nnz);

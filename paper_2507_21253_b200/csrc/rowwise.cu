@@ -902,8 +902,12 @@ Mats make_mats(const bsp_csr* A, const bsp_csr* B) {
                 static_cast<int32_t>(B->ncols)};
 }
 
+template <bool NUMERIC>
+void run_light(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx& out);
+
 void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
-                       const uint8_t* skip, RowwisePlan& plan, int64_t* prod_out) {
+                       const uint8_t* skip, RowwisePlan& plan, int64_t* prod_out,
+                       int64_t* early_row_nnz) {
     const int64_t n = re - rb;
     plan.rb = rb;
     plan.n = n;
@@ -940,6 +944,17 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         h2d(h, cursor.p, cur.data(), NCLS);
         BSP_LAUNCH(h, bucket_kernel, static_cast<unsigned>(div_up(n, 256)), 256, 0, cls.p, rb, n,
                    cursor.p, plan.lists.p);
+    }
+    // The light rows' symbolic does not depend on the heavy-row plan: run it
+    // on the side stream while the (latency-bound) planner runs here;
+    // plan_symbolic joins it.
+    if (early_row_nnz && tot_listed > plan.class_count[NCLS - 1]) {
+        SideStream side(h);
+        OutCtx out{};
+        out.row_begin = plan.rb;
+        out.row_nnz = early_row_nnz;
+        run_light<false>(h, m, plan, out);
+        plan.light_sym_done = true;
     }
     // Heavy rows: planned column windows.
     const int64_t nh = plan.class_count[NCLS - 1];
@@ -1058,11 +1073,15 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
 }
 
 template <bool NUMERIC>
-void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCtx& out) {
-    const Mats m = plan.with_starts(m0);
-    // longest work first: the light classes from the largest, then windows
+void run_light(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx& out) {
+    // largest class first
     for (int c = NCLS - 2; c >= 1; --c)
         launch_light<NUMERIC>(h, c, m, plan.lists.p + plan.class_off[c], plan.class_count[c], out);
+}
+
+template <bool NUMERIC>
+void run_windows(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCtx& out) {
+    const Mats m = plan.with_starts(m0);
     auto wl = [&](int k) { return plan.sparse_ids.p + plan.wcls_off[k]; };
     auto wn = [&](int k) { return plan.wcls_off[k + 1] - plan.wcls_off[k]; };
     static_assert(NWCLS == 4, "one launch per window tile class");
@@ -1073,8 +1092,15 @@ void run_plan(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCt
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
 
+template <bool NUMERIC>
+void run_plan(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx& out) {
+    run_light<NUMERIC>(h, m, plan, out);
+    run_windows<NUMERIC>(h, m, plan, out);
+}
+
 // Symbolic pass of a plan: exact per-row counts (row_nnz must be zeroed by
-// the caller) and per-window counts.
+// the caller, and be the array given to build_plan when the light rows were
+// counted early) and per-window counts.
 void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t* row_nnz,
                    DBuf<int64_t>& win_nnz) {
     win_nnz = DBuf<int64_t>(h, plan.nwin + 1);
@@ -1083,7 +1109,12 @@ void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t
     out.row_begin = plan.rb;
     out.row_nnz = row_nnz;
     out.win_nnz = win_nnz.p;
-    run_plan<false>(h, m, plan, out);
+    if (plan.light_sym_done) {
+        run_windows<false>(h, m, plan, out);
+        join_side(h);
+    } else {
+        run_plan<false>(h, m, plan, out);
+    }
 }
 
 void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
@@ -1108,10 +1139,10 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     h->stats.chunks = 1;
     const Mats m = make_mats(A, B);
     const int64_t n = re - rb;
-    RowwisePlan plan;
-    build_plan(h, m, rb, re, row_skip, plan, nullptr);
     DBuf<int64_t> crp(h, n + 1);
     BSP_CUDA(cudaMemsetAsync(crp.p, 0, (n + 1) * sizeof(int64_t), h->stream));
+    RowwisePlan plan;
+    build_plan(h, m, rb, re, row_skip, plan, nullptr, crp.p);
     DBuf<int64_t> win_nnz;
     plan_symbolic(h, m, plan, crp.p, win_nnz);
     // crp currently holds per-row counts in [0, n); scan in place over n+1.
