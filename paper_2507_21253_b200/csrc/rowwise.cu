@@ -668,7 +668,7 @@ constexpr int DT = 256;
 constexpr int DI = CAP / DT;
 
 struct DenseShared {
-    using Sort = cub::BlockRadixSort<uint32_t, DT, DI, uint32_t>;
+    using Sort = cub::BlockRadixSort<uint32_t, DT, DI, uint16_t>;
     using Scan = cub::BlockScan<int32_t, DT>;
     double acc[WD];
     uint32_t bitmap[WD / 32];
@@ -676,7 +676,7 @@ struct DenseShared {
     double vals[CAP];
     union {
         typename Sort::TempStorage sort;
-        uint32_t sidx[CAP];
+        uint16_t sidx[CAP];
     } u;
     typename Scan::TempStorage scan;
     int64_t pstart[DT];
@@ -723,12 +723,23 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
         __syncthreads();
         const int nslots = static_cast<int>(::min(int64_t{DT}, re - pc));
         if (!NUMERIC) {
+            // 4 column loads in flight per lane, then their bitmap bits
             for (int slot = warp; slot < nslots; slot += NW) {
                 const int l = s.plen[slot];
                 const int64_t st = s.pstart[slot];
-                for (int q = lane; q < l; q += 32) {
-                    const uint32_t c = static_cast<uint32_t>(__ldg(m.bcol + st + q) - c0);
-                    atomicOr(&s.bitmap[c >> 5], 1u << (c & 31));
+                for (int q0 = 0; q0 < l; q0 += 128) {
+                    int32_t col[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int q = q0 + 32 * u + lane;
+                        col[u] = q < l ? __ldg(m.bcol + st + q) : -1;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (col[u] < 0) continue;
+                        const uint32_t c = static_cast<uint32_t>(col[u] - c0);
+                        atomicOr(&s.bitmap[c >> 5], 1u << (c & 31));
+                    }
                 }
             }
             __syncthreads();
@@ -743,22 +754,39 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
                 if (lo >= hi) continue;
                 const int64_t st = s.pstart[slot] + (lo - o);
                 const double a = s.pav[slot];
-                for (int q = lane; q < hi - lo; q += 32) {
-                    s.keys[lo - b0 + q] = static_cast<uint32_t>(__ldg(m.bcol + st + q) - c0);
-                    s.vals[lo - b0 + q] = __dmul_rn(a, __ldg(m.bval + st + q));
+                const int cnt = hi - lo;
+                for (int q0 = 0; q0 < cnt; q0 += 128) {  // 4 (col, val) loads in flight
+                    int32_t cv[4];
+                    double bv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int q = q0 + 32 * u + lane;
+                        cv[u] = q < cnt ? __ldg(m.bcol + st + q) : 0;
+                        bv[u] = q < cnt ? __ldg(m.bval + st + q) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int q = q0 + 32 * u + lane;
+                        if (q >= cnt) break;
+                        s.keys[lo - b0 + q] = static_cast<uint32_t>(cv[u] - c0);
+                        s.vals[lo - b0 + q] = __dmul_rn(a, bv[u]);
+                    }
                 }
             }
             __syncthreads();
             const int n = b1 - b0;
-            uint32_t k[DI], v[DI];
+            // pad key WD-1 >= every key; pads sit after the n real entries
+            // and the sort is stable: 12-bit keys (3 passes)
+            uint32_t k[DI];
+            uint16_t v[DI];
 #pragma unroll
             for (int i = 0; i < DI; ++i) {
                 const int e = tid * DI + i;
-                k[i] = e < n ? s.keys[e] : static_cast<uint32_t>(WD);
-                v[i] = static_cast<uint32_t>(e);
+                k[i] = e < n ? s.keys[e] : static_cast<uint32_t>(WD - 1);
+                v[i] = static_cast<uint16_t>(e);
             }
             __syncthreads();
-            DenseShared::Sort(s.u.sort).Sort(k, v, 0, LOG_WD + 1);
+            DenseShared::Sort(s.u.sort).Sort(k, v, 0, LOG_WD);
             __syncthreads();
 #pragma unroll
             for (int i = 0; i < DI; ++i) {
@@ -997,14 +1025,19 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         d2h(h, &hv[1], soff.p + nh, 1);
         sync(h);
         plan.nwin = hv[0];
-        // Start-table budget: what HBM holds beyond an upper bound of C
-        // (12 B x products) and a 2 GB margin, at most 2^32 entries (16 GB);
-        // the rows in scan order that fit get a table, the rest binary-search.
-        const int64_t spare = static_cast<int64_t>(available_bytes(h)) -
-                              12 * h->stats.products - (int64_t{2} << 30);
-        const int64_t budget = std::max<int64_t>(
-            0, std::min<int64_t>({hv[1], int64_t{1} << 32,
-                                  spare / static_cast<int64_t>(sizeof(int32_t))}));
+        // Start-table budget: at least min(2^30 entries, 1/8 of available
+        // HBM); up to 2^32 entries when HBM also holds an upper bound of C
+        // (12 B x products) and a 2 GB margin (the bound is loose when
+        // columns repeat: cfg3).  Rows in scan order that fit get a table,
+        // the rest binary-search.
+        const int64_t avail = static_cast<int64_t>(available_bytes(h));
+        const int64_t spare = avail - 12 * h->stats.products - (int64_t{2} << 30);
+        const int64_t floor_entries =
+            std::min<int64_t>(int64_t{1} << 30, avail / (8 * static_cast<int64_t>(sizeof(int32_t))));
+        const int64_t budget = std::min<int64_t>(
+            hv[1], std::max<int64_t>(floor_entries,
+                                     std::min<int64_t>(int64_t{1} << 32,
+                                                       spare / static_cast<int64_t>(sizeof(int32_t)))));
         const bool use_starts = budget > 0;
         if (use_starts) plan.starts = DBuf<int32_t>(h, budget);
         plan.wins = DBuf<Window>(h, plan.nwin);
