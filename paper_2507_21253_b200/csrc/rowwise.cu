@@ -685,6 +685,45 @@ struct DenseShared {
     double pav[DT];
 };
 
+// One batch of n products (k order) of a dense window: stable sort by column
+// (12-bit keys; the pad WD-1 sits after the n real entries), then every run of
+// equal columns is added to its accumulator left to right.
+__device__ __forceinline__ void dense_batch(DenseShared& s, int n) {
+    const int tid = threadIdx.x;
+    uint32_t k[DI];
+    uint16_t v[DI];
+#pragma unroll
+    for (int i = 0; i < DI; ++i) {
+        const int e = tid * DI + i;
+        k[i] = e < n ? s.keys[e] : static_cast<uint32_t>(WD - 1);
+        v[i] = static_cast<uint16_t>(e);
+    }
+    __syncthreads();
+    DenseShared::Sort(s.u.sort).Sort(k, v, 0, LOG_WD);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < DI; ++i) {
+        s.keys[tid * DI + i] = k[i];
+        s.u.sidx[tid * DI + i] = v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < DI; ++i) {
+        const int e0 = tid * DI + i;
+        if (e0 < n && (e0 == 0 || s.keys[e0 - 1] != k[i])) {
+            double acc = s.acc[k[i]];
+            int e = e0;
+            do {
+                acc = __dadd_rn(acc, s.vals[s.u.sidx[e]]);
+                ++e;
+            } while (e < n && s.keys[e] == k[i]);
+            s.acc[k[i]] = acc;
+            atomicOr(&s.bitmap[k[i] >> 5], 1u << (k[i] & 31));
+        }
+    }
+    __syncthreads();
+}
+
 template <bool NUMERIC>
 __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t* __restrict__ ids,
                                                           const Window* __restrict__ wins,
@@ -701,6 +740,7 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
         for (int e = tid; e < WD; e += DT) s.acc[e] = 0.0;
     __syncthreads();
     const int64_t rs = m.arp[row], re = m.arp[row + 1];
+    int fill = 0;  // products in the current batch (block-uniform)
     for (int64_t pc = rs; pc < re; pc += DT) {
         const int64_t p = pc + tid;
         int len = 0;
@@ -745,15 +785,17 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
             __syncthreads();
             continue;
         }
-        // NUMERIC: batches of CAP products in (k, j) order.
-        for (int b0 = 0; b0 < chunk; b0 += CAP) {
-            const int b1 = min(chunk, b0 + CAP);
+        // NUMERIC: the chunk's products are appended, in (k, j) order, to the
+        // current batch; a full batch (or the last one) is sorted and added.
+        for (int cpos = 0; cpos < chunk;) {
+            const int take = min(chunk - cpos, CAP - fill);
             for (int slot = warp; slot < nslots; slot += NW) {
                 const int o = s.poff[slot], l = s.plen[slot];
-                const int lo = max(o, b0), hi = min(o + l, b1);
+                const int lo = max(o, cpos), hi = min(o + l, cpos + take);
                 if (lo >= hi) continue;
                 const int64_t st = s.pstart[slot] + (lo - o);
                 const double a = s.pav[slot];
+                const int dst = fill + (lo - cpos);
                 const int cnt = hi - lo;
                 for (int q0 = 0; q0 < cnt; q0 += 128) {  // 4 (col, val) loads in flight
                     int32_t cv[4];
@@ -768,48 +810,24 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
                     for (int u = 0; u < 4; ++u) {
                         const int q = q0 + 32 * u + lane;
                         if (q >= cnt) break;
-                        s.keys[lo - b0 + q] = static_cast<uint32_t>(cv[u] - c0);
-                        s.vals[lo - b0 + q] = __dmul_rn(a, bv[u]);
+                        s.keys[dst + q] = static_cast<uint32_t>(cv[u] - c0);
+                        s.vals[dst + q] = __dmul_rn(a, bv[u]);
                     }
                 }
             }
-            __syncthreads();
-            const int n = b1 - b0;
-            // pad key WD-1 >= every key; pads sit after the n real entries
-            // and the sort is stable: 12-bit keys (3 passes)
-            uint32_t k[DI];
-            uint16_t v[DI];
-#pragma unroll
-            for (int i = 0; i < DI; ++i) {
-                const int e = tid * DI + i;
-                k[i] = e < n ? s.keys[e] : static_cast<uint32_t>(WD - 1);
-                v[i] = static_cast<uint16_t>(e);
+            fill += take;
+            cpos += take;
+            if (fill == CAP) {
+                __syncthreads();
+                dense_batch(s, CAP);
+                fill = 0;
             }
-            __syncthreads();
-            DenseShared::Sort(s.u.sort).Sort(k, v, 0, LOG_WD);
-            __syncthreads();
-#pragma unroll
-            for (int i = 0; i < DI; ++i) {
-                s.keys[tid * DI + i] = k[i];
-                s.u.sidx[tid * DI + i] = v[i];
-            }
-            __syncthreads();
-#pragma unroll
-            for (int i = 0; i < DI; ++i) {
-                const int e0 = tid * DI + i;
-                if (e0 < n && (e0 == 0 || s.keys[e0 - 1] != k[i])) {
-                    double acc = s.acc[k[i]];
-                    int e = e0;
-                    do {
-                        acc = __dadd_rn(acc, s.vals[s.u.sidx[e]]);
-                        ++e;
-                    } while (e < n && s.keys[e] == k[i]);
-                    s.acc[k[i]] = acc;
-                    atomicOr(&s.bitmap[k[i] >> 5], 1u << (k[i] & 31));
-                }
-            }
-            __syncthreads();
         }
+        __syncthreads();  // slot arrays are rewritten by the next chunk
+    }
+    if (NUMERIC && fill > 0) {
+        __syncthreads();
+        dense_batch(s, fill);
     }
     // Bitmap -> count (and sorted output).
     constexpr int NWORD = WD / 32;  // 128 <= DT
