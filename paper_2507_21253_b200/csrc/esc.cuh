@@ -10,7 +10,6 @@
 namespace bsp {
 
 constexpr int CAP = 4096;     // max products of one sparse tile (smem ESC)
-constexpr int CAPH = CAP / 2;
 // Sparse-window tile classes (descending): a window runs in the smallest
 // tile that holds its products (CUB's block sort always sorts the full tile).
 // The 3072 class keeps 256 threads and is sized (≈73 KB smem, 85 registers)
@@ -21,7 +20,6 @@ constexpr int LOG_WD = 12;
 constexpr int MAXBINS = 4096; // planner histogram bins per heavy row
 constexpr int NCLS = 7;       // 0 empty, 1..5 light classes, 6 heavy
 static __constant__ int kClassCap[NCLS] = {0, 128, 512, 2048, 3072, 4096, 0x7fffffff};
-constexpr int kClassCapHost[NCLS] = {0, 128, 512, 2048, 3072, 4096, 0x7fffffff};
 
 struct Mats {
     const int64_t* __restrict__ arp;
@@ -91,7 +89,8 @@ __host__ __device__ __forceinline__ int bit_length(uint32_t x) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: ESC tile kernel (light rows and sparse windows)
+// Register-staged ESC tile (CUB block radix sort of the whole tile): used by
+// the top-k candidate kernels (topk.cu); the SpGEMM tiles are in merge.cuh.
 // ---------------------------------------------------------------------------
 template <int T, int I, bool NUMERIC>
 struct EscShared {

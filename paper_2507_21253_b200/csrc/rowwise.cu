@@ -7,23 +7,25 @@
 // with the multiply rounded before the add (no FMA; spgemm.hpp:92-97,
 // hash_accumulator.hpp:57-65).
 //
-// Design (DESIGN.md §Kernels):
+// Design (DESIGN.md §4):
 //  K0 products_kernel: per-row intermediate products P_i (row_upper_bound,
-//     spgemm.hpp:31-36) and the row's work class.
+//     spgemm.hpp:31-36) and the row's class (<= 128/512/2048/3072/4096
+//     products, or heavy).
 //  K1 bucket_kernel:   row ids grouped by class.
-//  K2 plan kernels:    rows with P_i > CAP are cut into column windows with
-//     <= CAP products ("sparse" windows) or <= WD columns ("dense" windows),
-//     from a per-row product histogram over WD-wide column bins.
-//  K3 esc_tile_kernel<T,I,NUMERIC>: one CTA per row (or sparse window):
-//     expand the row's products into shared memory in (k, j) order, stable
-//     radix sort by column, then each run of equal columns is summed
-//     sequentially in k order starting from 0.0 -> bit-exact values; runs
-//     are written as sorted CSR through a coalesced smem staging pass.
-//  K4 dense_window_kernel<NUMERIC>: heavy windows with a dense smem
-//     accumulator of WD doubles + bitmap; products streamed in CAP batches
-//     in k order, each batch stable-sorted so per-column order is kept.
-//  Symbolic runs K3/K4 without values to get exact per-row counts (exact
-//  allocation as the reference), then an int64 scan gives row_ptr.
+//  K2 plan_count / plan_write: heavy rows are cut greedily into column
+//     windows of <= 3072 products (one 4096-column bin of more than 4096
+//     products is a "dense" window), with per-(window, segment) start tables.
+//  K3 hash_count_kernel (symbolic) / esc_merge_kernel (numeric): one CTA
+//     per light row or sparse window (merge.cuh): the products are gathered
+//     into shared memory in (k, j) order with cp.async, stably sorted by
+//     column (merge of the presorted runs, CUB radix or MSD), and every run
+//     of equal columns is summed left to right from 0.0 -> bit-exact values,
+//     stored coalesced.
+//  K4 dense_window_kernel<NUMERIC>: dense windows with a smem accumulator of
+//     WD doubles + bitmap; products streamed in 4096-product batches in k
+//     order, each batch stably sorted so per-column order is kept.
+//  The symbolic pass gives exact per-row counts (exact allocation, as the
+//  reference), then an int64 scan gives row_ptr.
 #include "esc.cuh"
 #include "merge.cuh"
 
@@ -399,109 +401,6 @@ __global__ void window_c0_kernel(const Window* __restrict__ wins, const int32_t*
     if (i < n) keys[i] = static_cast<uint32_t>(wins[ids[i]].c0);
 }
 
-template <int T, int I, bool NUMERIC>
-__global__ void __launch_bounds__(T) esc_tile_kernel(Mats m, const int32_t* __restrict__ ids,
-                                                     const Window* __restrict__ wins, OutCtx out) {
-    using S = EscShared<T, I, NUMERIC>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    S& s = *reinterpret_cast<S*>(smem_raw);
-    const int tid = threadIdx.x;
-    const int32_t id = ids[blockIdx.x];
-    int32_t row, c0, c1, w = -1;
-    int64_t wsofs = -1;
-    int wwi = 0;
-    if (wins) {
-        w = id;
-        const Window wd = wins[w];
-        row = wd.row;
-        c0 = wd.c0;
-        c1 = wd.c1;
-        wsofs = wd.sofs;
-        wwi = wd.wi;
-    } else {
-        row = id;
-        c0 = 0;
-        c1 = m.ncols;
-    }
-    const bool full = (wins == nullptr);
-    const int total = expand_products<T, I, NUMERIC>(m, row, c0, c1, full, s, wsofs, wwi);
-
-    // Stable LSD radix sort of (column, position) pairs.
-    const uint32_t width = static_cast<uint32_t>(c1 - c0);
-    const int bits = bit_length(width);
-    uint32_t k[I], v[I];
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        const int e = tid * I + i;
-        k[i] = e < total ? s.keys[e] : width;
-        v[i] = static_cast<uint32_t>(e);
-    }
-    __syncthreads();
-    typename S::Sort(s.u.sort).Sort(k, v, 0, bits);
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        s.keys[tid * I + i] = k[i];
-        s.u.sidx[tid * I + i] = v[i];
-    }
-    __syncthreads();
-    // Run heads = first position of every distinct column.
-    bool head[I];
-    int nh = 0;
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        const int e = tid * I + i;
-        head[i] = e < total && (e == 0 || k[i] != s.keys[e - 1]);
-        nh += head[i];
-    }
-    int hoff, tile_cnt;
-    typename S::Scan(s.scan).ExclusiveSum(nh, hoff, tile_cnt);
-    if (!NUMERIC) {
-        if (tid == 0) {
-            if (w >= 0) {
-                out.win_nnz[w] = tile_cnt;
-                atomicAdd(reinterpret_cast<unsigned long long*>(&out.row_nnz[row - out.row_begin]),
-                          static_cast<unsigned long long>(tile_cnt));
-            } else {
-                out.row_nnz[row - out.row_begin] = tile_cnt;
-            }
-        }
-        return;
-    }
-    // Ordered reduction: each run summed left to right from 0.0.
-    double res[I];
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        res[i] = 0.0;
-        if (head[i]) {
-            const int e0 = tid * I + i;
-            double acc = 0.0;
-            int e = e0;
-            do {
-                acc = __dadd_rn(acc, s.vals[s.u.sidx[e]]);
-                ++e;
-            } while (e < total && s.keys[e] == k[i]);
-            res[i] = acc;
-        }
-    }
-    __syncthreads();
-    int r = hoff;
-#pragma unroll
-    for (int i = 0; i < I; ++i) {
-        if (head[i]) {
-            s.keys[r] = k[i] + static_cast<uint32_t>(c0);
-            s.vals[r] = res[i];
-            ++r;
-        }
-    }
-    __syncthreads();
-    int64_t base = out.crp[row - out.row_begin];
-    if (w >= 0) base += out.win_scan[w] - out.win_scan[wins[w].first];
-    for (int e = tid; e < tile_cnt; e += T) {
-        out.ccol[base + e] = static_cast<int32_t>(s.keys[e]);
-        out.cval[base + e] = s.vals[e];
-    }
-}
 
 // K3': merge-based exact numeric tile and hash-count symbolic tile
 // ---------------------------------------------------------------------------
@@ -865,17 +764,6 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
 // ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
-template <int T, int I, bool NUMERIC>
-void launch_esc(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, const Window* wins,
-                const OutCtx& out) {
-    if (n <= 0) return;
-    using S = EscShared<T, I, NUMERIC>;
-    auto k = esc_tile_kernel<T, I, NUMERIC>;
-    static const std::string nm = std::string(NUMERIC ? "esc_numeric<" : "esc_symbolic<") +
-                                  std::to_string(T) + "x" + std::to_string(I) + ">";
-    set_smem(k, sizeof(S));
-    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
-}
 
 template <int T, int CAPM, bool NUMERIC>
 void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, const Window* wins,
