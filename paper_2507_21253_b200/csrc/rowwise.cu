@@ -762,6 +762,86 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
 }
 
 // ---------------------------------------------------------------------------
+// K5: narrow B (ncols <= NARROW, e.g. the tall-skinny frontier operands of
+// frontier.hpp:20-77): one warp per row with a dense accumulator of ncols
+// doubles in shared memory.  The row's segments are walked in k order; a
+// segment's entries have distinct columns, so its lanes add them in parallel,
+// and __syncwarp between segments keeps every column's additions in
+// ascending k from 0.0 — the reference's order, bit-exact, with no planning
+// and no sort.  Symbolic counts the touched columns.
+// ---------------------------------------------------------------------------
+constexpr int NARROW = 256;
+constexpr int NARROW_WARPS = 8;
+
+template <bool NUMERIC>
+__global__ void __launch_bounds__(NARROW_WARPS * 32)
+    narrow_kernel(Mats m, int64_t rb, int64_t n, int32_t ncols, int64_t* __restrict__ row_nnz,
+                  const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                  double* __restrict__ cval, unsigned long long* __restrict__ products) {
+    __shared__ double s_acc[NUMERIC ? NARROW_WARPS : 1][NUMERIC ? NARROW : 1];
+    __shared__ uint32_t s_touch[NARROW_WARPS][NARROW / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* acc = s_acc[NUMERIC ? warp : 0];
+    uint32_t* touch = s_touch[warp];
+    const int nwords = (ncols + 31) >> 5;
+    unsigned long long prod = 0;
+    for (int64_t r = blockIdx.x * int64_t{NARROW_WARPS} + warp; r < n;
+         r += int64_t{gridDim.x} * NARROW_WARPS) {
+        const int64_t row = rb + r;
+        if (NUMERIC)
+            for (int j = lane; j < ncols; j += 32) acc[j] = 0.0;
+        if (lane < nwords) touch[lane] = 0u;
+        __syncwarp();
+        const int64_t rs = m.arp[row], re = m.arp[row + 1];
+        for (int64_t pb = rs; pb < re; pb += 32) {
+            const int64_t p = pb + lane;
+            int64_t b0 = 0;
+            int len = 0;
+            double a = 0.0;
+            if (p < re) {
+                const int32_t k = __ldg(m.acol + p);
+                b0 = __ldg(m.brp + k);
+                len = static_cast<int>(__ldg(m.brp + k + 1) - b0);
+                if (NUMERIC) a = __ldg(m.aval + p);
+            }
+            const int nseg = static_cast<int>(::min(int64_t{32}, re - pb));
+            for (int j = 0; j < nseg; ++j) {
+                const int64_t sj = __shfl_sync(0xffffffffu, b0, j);
+                const int lj = __shfl_sync(0xffffffffu, len, j);
+                const double aj = __shfl_sync(0xffffffffu, a, j);
+                prod += static_cast<unsigned long long>(lane == 0 ? lj : 0);
+                for (int q = lane; q < lj; q += 32) {
+                    const int32_t c = __ldg(m.bcol + sj + q);
+                    if (NUMERIC)
+                        acc[c] = __dadd_rn(acc[c], __dmul_rn(aj, __ldg(m.bval + sj + q)));
+                    atomicOr(&touch[c >> 5], 1u << (c & 31));
+                }
+                __syncwarp();
+            }
+        }
+        if (!NUMERIC) {
+            int cnt = lane < nwords ? __popc(touch[lane]) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (lane == 0) row_nnz[r] = cnt;
+        } else {
+            int64_t pos = crp[r];
+            for (int wd = 0; wd < nwords; ++wd) {
+                const uint32_t bits = touch[wd];
+                if ((bits >> lane) & 1u) {
+                    const int64_t o = pos + __popc(bits & ((1u << lane) - 1u));
+                    ccol[o] = wd * 32 + lane;
+                    cval[o] = acc[wd * 32 + lane];
+                }
+                pos += __popc(bits);
+            }
+        }
+        __syncwarp();
+    }
+    if (!NUMERIC && lane == 0 && prod) atomicAdd(products, prod);
+}
+
+// ---------------------------------------------------------------------------
 // host orchestration
 // ---------------------------------------------------------------------------
 
@@ -1067,6 +1147,41 @@ void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const in
     run_plan<true>(h, m, plan, out);
 }
 
+// Narrow B: symbolic (+ products) -> int64 scan -> numeric, no planning.
+static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, int64_t ncols,
+                            bsp_csr* C, int64_t* row_nnz_out) {
+    DBuf<int64_t> cnt(h, n + 1);
+    BSP_CUDA(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(int64_t), h->stream));
+    DBuf<unsigned long long> prod(h, 1);
+    BSP_CUDA(cudaMemsetAsync(prod.p, 0, sizeof(unsigned long long), h->stream));
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>(div_up(std::max<int64_t>(n, 1), NARROW_WARPS),
+                             int64_t{h->sm_count} * 32)));
+    const int32_t nc = static_cast<int32_t>(ncols);
+    auto ks = narrow_kernel<false>;
+    auto kn = narrow_kernel<true>;
+    BSP_LAUNCH_AS(h, "narrow_symbolic", ks, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, cnt.p,
+                  nullptr, nullptr, nullptr, prod.p);
+    if (row_nnz_out)
+        BSP_CUDA(cudaMemcpyAsync(row_nnz_out, cnt.p, n * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                                 h->stream));
+    DBuf<int64_t> rp(h, n + 1, Pool::out);
+    exclusive_scan_i64(h, cnt.p, rp.p, n + 1);
+    const int64_t nnz = read_scalar(h, rp.p + n);
+    h->stats.products = static_cast<int64_t>(read_scalar(h, prod.p));
+    h->stats.nnz_out = nnz;
+    ResultPayload pay(h, nnz);
+    BSP_LAUNCH_AS(h, "narrow_numeric", kn, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, nullptr,
+                  rp.p, pay.col_idx(), pay.values(), nullptr);
+    C->nrows = n;
+    C->ncols = ncols;
+    C->nnz = nnz;
+    C->row_ptr = rp.release();
+    C->col_idx = pay.col_idx();
+    C->values = pay.block.release();
+    C->owned = 2;
+}
+
 void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t rb, int64_t re,
                       bsp_csr* C, const uint8_t* row_skip, int64_t* row_nnz_out) {
     check_csr(A, "spgemm_rowwise");
@@ -1078,6 +1193,12 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     h->stats.chunks = 1;
     const Mats m = make_mats(A, B);
     const int64_t n = re - rb;
+    // BSP_NARROW=0 forces the tile path (read per call, so tests can cover both)
+    const char* ne = std::getenv("BSP_NARROW");
+    if (B->ncols <= NARROW && row_skip == nullptr && !(ne && ne[0] == '0')) {
+        narrow_multiply(h, m, rb, n, B->ncols, C, row_nnz_out);
+        return;
+    }
     DBuf<int64_t> crp(h, n + 1);
     BSP_CUDA(cudaMemsetAsync(crp.p, 0, (n + 1) * sizeof(int64_t), h->stream));
     RowwisePlan plan;

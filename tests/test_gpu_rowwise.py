@@ -57,8 +57,11 @@ def test_structural_zero_kept(engine):
     assert c.nnz() == 1 and c.values[0] == 0.0
 
 
-def test_dense_oracle_corpus(engine):
-    """reference spgemm_rowwise_test.cpp:53-75 / acceptance_main.cpp:80-97."""
+@pytest.mark.parametrize("narrow", ["1", "0"])
+def test_dense_oracle_corpus(engine, monkeypatch, narrow):
+    """reference spgemm_rowwise_test.cpp:53-75 / acceptance_main.cpp:80-97; B of
+    <= 100 columns runs the narrow-B kernel, BSP_NARROW=0 forces the tiles."""
+    monkeypatch.setenv("BSP_NARROW", narrow)
     rng = np.random.default_rng(7)
     for seed in range(40):
         n, m, k = (int(x) for x in rng.integers(1, 101, size=3))
@@ -173,3 +176,26 @@ def test_heavy_rows_over_empty_b_rows(engine):
     B64 = engine.upload(b64)
     assert_csr_identical(engine.spgemm_rowwise(A, B64).download(), O.spgemm_rowwise(a, b64),
                          "dense windows over empty B rows")
+
+
+@pytest.mark.parametrize("ncols", [1, 31, 64, 200, 256, 257])
+def test_narrow_b_matches_oracle(engine, ncols):
+    """Narrow B (<= 256 columns: one warp per row, dense accumulator) against
+    the oracle, with heavy rows, hub B rows, empty rows and empty B rows;
+    257 columns takes the tile path."""
+    rng = np.random.default_rng(ncols)
+    n = 3000
+    a = B.make_config(5, 12)
+    r, c = [], []
+    for k in range(a.nrows):
+        if k % 4 == 0:
+            continue
+        d = 1 + int(rng.integers(0, min(ncols, 40)))
+        cols = np.sort(rng.choice(ncols, size=min(d, ncols), replace=False))
+        r += [k] * cols.size
+        c += cols.tolist()
+    b = B.coo_to_csr(a.nrows, ncols, np.array(r), np.array(c), rng.random(len(r)) - 0.5)
+    A, Bd = engine.upload(a), engine.upload(b)
+    got = engine.spgemm_rowwise(A, Bd).download()
+    assert_csr_identical(got, O.spgemm_rowwise(a, b), f"narrow {ncols}")
+    assert engine.exec_stats()["products"] == int(np.diff(b.row_ptr)[a.col_idx].sum())
