@@ -29,7 +29,8 @@ struct Mats {
     const int32_t* __restrict__ bcol;
     const double* __restrict__ bval;
     int32_t ncols;  // columns of B (= of C)
-    const int32_t* __restrict__ starts = nullptr;  // planner start tables (windows)
+    // planner start tables (windows): absolute B offsets per (window, segment)
+    const int64_t* __restrict__ starts = nullptr;
 };
 
 struct Window {
@@ -38,6 +39,9 @@ struct Window {
     int32_t first;  // index of the row's first window
     int32_t wi;     // index of this window within its row
     int32_t nprod;  // products in the window (sparse windows)
+    int32_t d;      // segments of the row (A row length)
+    int32_t pad_;
+    int64_t rs;     // A row start (row_ptr[row])
     int64_t sofs;   // offset of the row's per-(window, segment) start table, or -1
 };
 
@@ -63,18 +67,23 @@ __device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ c
     return lo;
 }
 
-// Segment [b0, b1) of B row k restricted to a window: from the planner's
-// start table when the row has one (no search), else by binary search.
-// b0/b1 hold the full segment on entry.
-__device__ __forceinline__ void window_bounds(const Mats& m, int64_t sofs, int wi, int64_t pl,
-                                              int64_t d, int32_t c0, int32_t c1, int64_t& b0,
-                                              int64_t& b1) {
-    if (sofs >= 0) {
-        const int32_t* st = m.starts + sofs;
-        const int64_t base = b0;
-        b1 = base + __ldg(st + int64_t{wi + 1} * d + pl);
-        b0 = base + __ldg(st + int64_t{wi} * d + pl);
-    } else {
+// B range [b0, b1) that segment p (absolute A index; A row starts at rs and
+// has d entries) contributes to a tile: the whole B row for a full row; for
+// a window, the planner's start table when the row has one — absolute
+// offsets, so no A/B row lookup at all — else a binary search for [c0, c1).
+__device__ __forceinline__ void segment_range(const Mats& m, bool full, int64_t sofs, int wi,
+                                              int64_t p, int64_t rs, int64_t d, int32_t c0,
+                                              int32_t c1, int64_t& b0, int64_t& b1) {
+    if (!full && sofs >= 0) {
+        const int64_t* st = m.starts + sofs + (p - rs);
+        b0 = __ldg(st + int64_t{wi} * d);
+        b1 = __ldg(st + int64_t{wi + 1} * d);
+        return;
+    }
+    const int32_t k = __ldg(m.acol + p);
+    b0 = __ldg(m.brp + k);
+    b1 = __ldg(m.brp + k + 1);
+    if (!full) {
         b0 = lower_bound_col(m.bcol, b0, b1, c0);
         b1 = lower_bound_col(m.bcol, b0, b1, c1);
     }
@@ -127,9 +136,8 @@ __device__ __forceinline__ int expand_products(const Mats& m, int32_t row, int32
         int64_t start = 0;
         double av = 0.0;
         if (p < re) {
-            const int32_t k = __ldg(m.acol + p);
-            int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            if (!full) window_bounds(m, wsofs, wwi, p - rs, re - rs, c0, c1, b0, b1);
+            int64_t b0, b1;
+            segment_range(m, full, wsofs, wwi, p, rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
             if (NUMERIC) av = __ldg(m.aval + p);
@@ -171,7 +179,7 @@ struct RowwisePlan {
     int64_t wcls_off[NWCLS + 1]{};
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
-    DBuf<int32_t> starts; // planner per-(window, segment) start tables
+    DBuf<int64_t> starts; // planner per-(window, segment) start tables (absolute)
     bool light_sym_done = false;  // light rows counted on the side stream
     // Matrices as seen by the window kernels (start tables attached).
     Mats with_starts(const Mats& m) const {

@@ -105,9 +105,12 @@ __device__ __forceinline__ void warp_slice_begin(const int32_t* poff, int nr, in
 template <int T, int CAPM, bool VALUES>
 __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c0, int32_t c1,
                                            bool full, MergeShared<T, CAPM>& s,
-                                           int64_t wsofs = -1, int wwi = 0) {
+                                           int64_t wsofs = -1, int wwi = 0, int64_t wrs = -1,
+                                           int64_t wd = 0) {
     const int tid = threadIdx.x;
-    const int64_t rs = m.arp[row], re = m.arp[row + 1];
+    // windows carry their A row range (one dependent load less)
+    const int64_t rs = wrs >= 0 ? wrs : m.arp[row];
+    const int64_t re = wrs >= 0 ? wrs + wd : m.arp[row + 1];
     int total = 0, nruns = 0;
     for (int64_t pc = rs; pc < re; pc += T) {
         const int64_t p = pc + tid;
@@ -115,9 +118,8 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         int64_t start = 0;
         double av = 0.0;
         if (p < re) {
-            const int32_t k = __ldg(m.acol + p);
-            int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            if (!full) window_bounds(m, wsofs, wwi, p - rs, re - rs, c0, c1, b0, b1);
+            int64_t b0, b1;
+            segment_range(m, full, wsofs, wwi, p, rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
             if (VALUES) av = __ldg(m.aval + p);

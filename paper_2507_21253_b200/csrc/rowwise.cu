@@ -120,8 +120,9 @@ struct PlanCountShared {
     typename cub::BlockScan<int32_t, PLAN_T>::TempStorage scan;
 };
 
-// Start tables of up to STAGE entries are built in smem and stored coalesced.
-constexpr int STAGE = 2 * MAXBINS;
+// Start tables of up to STAGE entries (int64) are built in smem and stored
+// coalesced.
+constexpr int STAGE = MAXBINS;
 struct PlanWriteShared {
     int32_t binwin[MAXBINS];  // bin -> window
     union {
@@ -129,7 +130,7 @@ struct PlanWriteShared {
             uint32_t wc0[MAXBINS + 1];  // window -> c0 | DENSE_BIT (+ sentinel ncols)
             int32_t wpre[MAXBINS + 1];  // window -> product prefix at c0 (+ sentinel P)
         } w;
-        int32_t stage[STAGE + 2];
+        int64_t stage[STAGE + 1];
     } u;
 };
 
@@ -137,7 +138,7 @@ struct PlanWriteShared {
 // (b0, b1) bounds of 32 upcoming segments fetched at once by the warp's lanes
 // and PLAN_U chunks of 32 B columns loaded before they are consumed, so each
 // warp keeps several independent loads in flight.  f(p, q0, len, cols[U],
-// state) is called for each group of chunks (warp-uniform; once with q0 = 0
+// state, b0) is called for each group of chunks (warp-uniform; once with q0 = 0
 // for an empty segment); cols[u] holds the column of element q0 + 32u + lane
 // or -1 past the end; `state` is an int reset to -1 at the start of every
 // segment.
@@ -170,7 +171,7 @@ __device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& 
                     const int q = q0 + 32 * u + lane;
                     cols[u] = q < len ? __ldg(m.bcol + b0 + q) : -1;
                 }
-                f(p, q0, len, cols, state);
+                f(p, q0, len, cols, state, b0);
             }
         }
     }
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
     const int lane = threadIdx.x & 31;
     for (int b = threadIdx.x; b < nbins; b += PLAN_T) s.hist[b] = 0;
     __syncthreads();
-    stream_segments(m, row, [&](int, int q0, int len, const int32_t* cols, int&) {
+    stream_segments(m, row, [&](int, int q0, int len, const int32_t* cols, int&, int64_t) {
 #pragma unroll
         for (int u = 0; u < PLAN_U; ++u) {
             if (q0 + 32 * u >= len) break;
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
     const int32_t* __restrict__ nwin, const int64_t* __restrict__ doff,
     const uint2* __restrict__ desc, const int64_t* __restrict__ win_off, Window* __restrict__ wins,
     uint8_t* __restrict__ win_cat, const int64_t* __restrict__ start_off, int64_t start_budget,
-    int32_t* __restrict__ starts) {
+    int64_t* __restrict__ starts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PlanWriteShared& s = *reinterpret_cast<PlanWriteShared*>(smem_raw);
     const int32_t hrow = blockIdx.x;
@@ -283,6 +284,9 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
         wd.first = static_cast<int32_t>(off);
         wd.wi = k;
         wd.nprod = s.u.w.wpre[k + 1] - s.u.w.wpre[k];
+        wd.d = static_cast<int32_t>(m.arp[row + 1] - m.arp[row]);
+        wd.pad_ = 0;
+        wd.rs = m.arp[row];
         wd.sofs = sofs;
         wins[off + k] = wd;
         // sparse: the smallest tile class that holds the window; dense: NWCLS
@@ -299,8 +303,10 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
     const int d = static_cast<int>(m.arp[row + 1] - m.arp[row]);
     const int64_t tsz = int64_t{wtot + 1} * d;
     const bool staged = tsz <= STAGE;
-    int32_t* tab = staged ? s.u.stage : starts + sofs;
-    stream_segments(m, row, [&](int p, int q0, int len, const int32_t* cols, int& carry) {
+    int64_t* tab = staged ? s.u.stage : starts + sofs;
+    // entries are absolute B offsets (segment start b0 + element index)
+    stream_segments(m, row, [&](int p, int q0, int len, const int32_t* cols, int& carry,
+                                int64_t b0) {
         // carry: window of the element before this group (-1 at q0 == 0)
 #pragma unroll
         for (int u = 0; u < PLAN_U; ++u) {
@@ -311,16 +317,17 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
             int wp = __shfl_up_sync(0xffffffffu, wq, 1);
             if (lane == 0) wp = carry;
             if (q < len)
-                for (int w2 = wp + 1; w2 <= wq; ++w2) tab[w2 * int64_t{d} + p] = q;
+                for (int w2 = wp + 1; w2 <= wq; ++w2) tab[w2 * int64_t{d} + p] = b0 + q;
             carry = __shfl_sync(0xffffffffu, wq, ::min(31, len - 1 - qb));
         }
         // windows after the last element start at len
         if (q0 + 32 * PLAN_U >= len)
-            for (int w2 = carry + 1 + lane; w2 <= wtot; w2 += 32) tab[w2 * int64_t{d} + p] = len;
+            for (int w2 = carry + 1 + lane; w2 <= wtot; w2 += 32)
+                tab[w2 * int64_t{d} + p] = b0 + len;
     });
     if (staged) {
         __syncthreads();
-        int32_t* st = starts + sofs;
+        int64_t* st = starts + sofs;
         for (int i = threadIdx.x; i < tsz; i += PLAN_T) st[i] = s.u.stage[i];
     }
 }
@@ -413,7 +420,7 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
     const int tid = threadIdx.x;
     const int32_t id = ids[blockIdx.x];
     int32_t row, c0, c1, w = -1;
-    int64_t wsofs = -1;
+    int64_t wsofs = -1, wrs = -1, wdn = 0;
     int wwi = 0;
     if (wins) {
         w = id;
@@ -423,12 +430,15 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
         c1 = wd.c1;
         wsofs = wd.sofs;
         wwi = wd.wi;
+        wrs = wd.rs;
+        wdn = wd.d;
     } else {
         row = id;
         c0 = 0;
         c1 = m.ncols;
     }
-    const int total = expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s, wsofs, wwi);
+    const int total =
+        expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s, wsofs, wwi, wrs, wdn);
     const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(c1 - c0));
     (void)tid;
     int64_t base = out.crp[row - out.row_begin];
@@ -466,7 +476,7 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
     constexpr int LG = 31 - __builtin_clz(static_cast<unsigned>(TS));
     const int32_t id = ids[blockIdx.x];
     int32_t row, c0, c1, w = -1;
-    int64_t wsofs = -1;
+    int64_t wsofs = -1, rs, re;
     int wwi = 0;
     if (wins) {
         w = id;
@@ -476,23 +486,25 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         c1 = wd.c1;
         wsofs = wd.sofs;
         wwi = wd.wi;
+        rs = wd.rs;
+        re = wd.rs + wd.d;
     } else {
         row = id;
         c0 = 0;
         c1 = m.ncols;
+        rs = m.arp[row];
+        re = m.arp[row + 1];
     }
     const bool full = wins == nullptr;
     for (int e = tid; e < TS; e += T) s.table[e] = -1;
-    const int64_t rs = m.arp[row], re = m.arp[row + 1];
     int cnt = 0;
     for (int64_t pc = rs; pc < re; pc += T) {
         const int64_t p = pc + tid;
         int len = 0;
         int64_t start = 0;
         if (p < re) {
-            const int32_t k = __ldg(m.acol + p);
-            int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            if (!full) window_bounds(m, wsofs, wwi, p - rs, re - rs, c0, c1, b0, b1);
+            int64_t b0, b1;
+            segment_range(m, full, wsofs, wwi, p, rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
         }
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
     if (NUMERIC)
         for (int e = tid; e < WD; e += DT) s.acc[e] = 0.0;
     __syncthreads();
-    const int64_t rs = m.arp[row], re = m.arp[row + 1];
+    const int64_t rs = wd.rs, re = wd.rs + wd.d;
     int fill = 0;  // products in the current batch (block-uniform)
     for (int64_t pc = rs; pc < re; pc += DT) {
         const int64_t p = pc + tid;
@@ -646,9 +658,8 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
         int64_t start = 0;
         double av = 0.0;
         if (p < re) {
-            const int32_t k = __ldg(m.acol + p);
-            int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-            window_bounds(m, wd.sofs, wd.wi, p - rs, re - rs, c0, c1, b0, b1);
+            int64_t b0, b1;
+            segment_range(m, false, wd.sofs, wd.wi, p, rs, re - rs, c0, c1, b0, b1);
             start = b0;
             len = static_cast<int>(b1 - b0);
             if (NUMERIC) av = __ldg(m.aval + p);
@@ -1011,21 +1022,20 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         d2h(h, &hv[1], soff.p + nh, 1);
         sync(h);
         plan.nwin = hv[0];
-        // Start-table budget: at least min(2^30 entries, 1/8 of available
-        // HBM); up to 2^32 entries when HBM also holds an upper bound of C
-        // (12 B x products) and a 2 GB margin (the bound is loose when
-        // columns repeat: cfg3).  Rows in scan order that fit get a table,
-        // the rest binary-search.
+        // Start-table budget (8-byte entries): at least min(2^30 entries,
+        // 1/16 of available HBM); up to 2^31 entries when HBM also holds an
+        // upper bound of C (12 B x products) and a 2 GB margin (the bound is
+        // loose when columns repeat: cfg3).  Rows in scan order that fit get
+        // a table, the rest binary-search.
+        constexpr int64_t EB = sizeof(int64_t);
         const int64_t avail = static_cast<int64_t>(available_bytes(h));
         const int64_t spare = avail - 12 * h->stats.products - (int64_t{2} << 30);
-        const int64_t floor_entries =
-            std::min<int64_t>(int64_t{1} << 30, avail / (8 * static_cast<int64_t>(sizeof(int32_t))));
+        const int64_t floor_entries = std::min<int64_t>(int64_t{1} << 30, avail / (16 * EB));
         const int64_t budget = std::min<int64_t>(
             hv[1], std::max<int64_t>(floor_entries,
-                                     std::min<int64_t>(int64_t{1} << 32,
-                                                       spare / static_cast<int64_t>(sizeof(int32_t)))));
+                                     std::min<int64_t>(int64_t{1} << 31, spare / EB)));
         const bool use_starts = budget > 0;
-        if (use_starts) plan.starts = DBuf<int32_t>(h, budget);
+        if (use_starts) plan.starts = DBuf<int64_t>(h, budget);
         plan.wins = DBuf<Window>(h, plan.nwin);
         DBuf<uint8_t> dense(h, plan.nwin);
         set_smem(plan_write_kernel, sizeof(PlanWriteShared));

@@ -453,10 +453,9 @@ __global__ void __launch_bounds__(TDT) topk_dense_kernel(Mats m, const int32_t* 
     if (tid == 0) s.nc = 0;
     __syncthreads();
     for (int64_t p = m.arp[row] + warp; p < m.arp[row + 1]; p += TDT / 32) {
-        const int32_t k = __ldg(m.acol + p);
-        int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
-        window_bounds(m, wd.sofs, wd.wi, p - m.arp[row], m.arp[row + 1] - m.arp[row], c0, c1, b0,
-                      b1);
+        int64_t b0, b1;
+        segment_range(m, false, wd.sofs, wd.wi, p, m.arp[row], m.arp[row + 1] - m.arp[row], c0,
+                      c1, b0, b1);
         for (int64_t q = b0 + lane; q < b1; q += 32) atomicAdd(&s.cnt[__ldg(m.bcol + q) - c0], 1);
     }
     __syncthreads();
