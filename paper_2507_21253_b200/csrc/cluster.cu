@@ -218,7 +218,8 @@ __global__ void cluster_bucket_kernel(const uint8_t* __restrict__ ccls, int64_t 
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
 __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : 4))
-    cluster_tile_kernel(ClusterMats m, const int32_t* __restrict__ ids, int cbits,
+    cluster_tile_kernel(ClusterMats m, const int32_t* __restrict__ ids, int cbits, int csort,
+                        int csort_radix_only,
                         const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
                         double* __restrict__ oval) {
     using S = MergeShared<T, CAPM>;
@@ -303,7 +304,8 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
         s.nruns = nruns;
     }
     __syncthreads();
-    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(K) << cbits);
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(K) << cbits, csort, cbits,
+                                  csort_radix_only != 0);
 
     // reduction (element-strided, as reduce_and_write) with member -> row map
     constexpr int R = (CAPM + T - 1) / T;
@@ -368,9 +370,18 @@ void launch_cluster(bsp_handle h, const ClusterMats& m, const int32_t* ids, int6
     auto k = cluster_tile_kernel<T, CAPM>;
     static const std::string nm =
         "cluster_numeric<" + std::to_string(T) + "," + std::to_string(CAPM) + ">";
+    // BSP_CSORT=0: radix/merge only (as the row-wise tiles)
+    static const int csort = [] {
+        const char* e = std::getenv("BSP_CSORT");
+        return e ? std::atoi(e) : 1000;
+    }();
     set_smem(k, sizeof(S));
-    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, cbits, crp,
-                  ocol, oval);
+    static const int ronly = [] {
+        const char* e = std::getenv("BSP_CSORT_CL_RADIX_ONLY");
+        return e ? std::atoi(e) : 1;
+    }();
+    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, cbits, csort,
+                  ronly, crp, ocol, oval);
 }
 
 void run_cluster_classes(bsp_handle h, const ClusterMats& m, const int32_t* lists,

@@ -36,6 +36,9 @@ struct MergeShared {
     static constexpr int MAXRUNS = CAPM < 1024 ? CAPM : 1024;
     // counters: MSD buckets (small tiles) or the reduction's (row, warp) heads
     static constexpr int NHIST = CAPM <= 512 ? CAPM / 2 : ((CAPM + T - 1) / T) * (T / 32);
+    // counting sort: buckets on the top column bits (about 1.5-2 products each)
+    static constexpr int NB = CAPM >= 3072 ? 2048 : (CAPM >= 2048 ? 1024 : CAPM / 2);
+    static constexpr int LNB = NB >= 2048 ? 11 : (NB >= 1024 ? 10 : (NB >= 256 ? 8 : 6));
     // buffer 0 (also the radix-sort input/output)
     uint32_t key0[NP];
     uint16_t idx0[NP];
@@ -49,6 +52,11 @@ struct MergeShared {
             uint16_t ro1[MAXRUNS + 2];
         } m;
         typename RSort::TempStorage sort;
+        struct CS {
+            uint32_t packed[CAPM];     // (low column bits << 16 | index), by bucket
+            uint32_t cnt[NB / 2 + 1];  // 16-bit bucket counts, then bucket starts
+            uint16_t bucket[CAPM];     // bucket of each bucketed slot
+        } c;
     } u;
     uint32_t hist[NHIST];
     __device__ __forceinline__ uint32_t* key(int b) { return b ? u.m.key1 : key0; }
@@ -351,9 +359,150 @@ __device__ __forceinline__ bool msd_sort_tile(MergeShared<T, CAPM>& s, int total
     return true;
 }
 
-// Sort the expanded tile: merge of presorted runs, or radix when cheaper.
+// Counting sort for tiles whose columns are nearly distinct (cf ~ 1): one
+// smem-atomic pass buckets the products on the top bits of the column
+// relative to the tile's own [min, max] column range (NB buckets, ~1.5
+// products each; 16-bit counters packed two per word), a scan lays the
+// buckets out, and each bucketed slot's final position is its bucket start
+// plus the number of bucket members with a smaller (column, expansion index)
+// — the index tie-break puts equal columns in ascending k, so the run sums
+// stay exact (spgemm.hpp:92-97).  The ranking runs over the bucketed slots, so
+// the lanes of a warp mostly share one bucket and the loop trip count (the
+// bucket size) does not diverge.
+// Composite keys (cbits > 0: key = member << cbits | column, the cluster
+// tiles) give each of the 2^lk member slots NB / 2^lk buckets over the
+// columns' range, so the order stays member-major.
+// The ranking costs sum(bucket size^2) compares (= sum over products of
+// 2 x rank-in-bucket + 1, known after the bucketing pass).  Tiles where that
+// exceeds `cost` x products (clustered or duplicate-heavy columns), whose
+// bucket width exceeds 2^16 columns, or with a bucket of more than CS_MAXB
+// products return false with buffer 0 untouched (merge / radix instead).
+// Result in buffer 0.
+constexpr int CS_MAXB = 128;
+
 template <int T, int CAPM>
-__device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width) {
+__device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width,
+                                                int cbits, int max_cost) {
+    using S = MergeShared<T, CAPM>;
+    constexpr int NB = S::NB, LNB = S::LNB, PER = NB / T, I = (CAPM + T - 1) / T;
+    static_assert(PER % 2 == 0 || PER == 1, "bucket split");
+    const int tid = threadIdx.x;
+    const uint32_t cmask = cbits > 0 ? (1u << cbits) - 1u : 0xffffffffu;
+    const int lk = cbits > 0 ? bit_length((width >> cbits) > 1 ? (width >> cbits) - 1 : 0) : 0;
+    if (lk > LNB) return false;
+    __shared__ int s_over, s_cost;
+    __shared__ uint32_t s_min, s_max;
+    uint32_t* cnt2 = s.u.c.cnt;  // NB 16-bit counters, two per word
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(s.u.c.cnt);
+    uint32_t* pk = s.u.c.packed;
+    uint16_t* bk = s.u.c.bucket;
+    for (int b = tid; b < NB / 2 + 1; b += T) cnt2[b] = 0u;
+    if (tid == 0) {
+        s_over = 0;
+        s_cost = 0;
+        s_min = 0xffffffffu;
+        s_max = 0u;
+    }
+    uint32_t kr[I], rr[I];
+    uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = i * T + tid;
+        if (e < total) {
+            kr[i] = s.key0[PADI(e)];
+            mn = min(mn, kr[i] & cmask);
+            mx = max(mx, kr[i] & cmask);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    __syncthreads();  // counters and bounds initialised
+    if ((tid & 31) == 0) {
+        atomicMin(&s_min, mn);
+        atomicMax(&s_max, mx);
+    }
+    __syncthreads();
+    const uint32_t cmin = s_min;
+    const int cb = LNB - lk;  // column bucket bits per member slot
+    const int cw = bit_length(s_max - cmin);
+    const int sh = cw > cb ? cw - cb : 0;
+    if (sh > 16) return false;
+    bool over = false;
+    int cost = 0;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = i * T + tid;
+        if (e < total) {
+            const uint32_t b = (cbits > 0 ? (kr[i] >> cbits) << cb : 0u) |
+                               (((kr[i] & cmask) - cmin) >> sh);
+            rr[i] = (atomicAdd(&cnt2[b >> 1], 1u << (16 * (b & 1))) >> (16 * (b & 1))) & 0xffffu;
+            over |= rr[i] >= CS_MAXB;
+            cost += 2 * static_cast<int>(rr[i]) + 1;
+        }
+    }
+    if (over) s_over = 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
+    if ((tid & 31) == 0) atomicAdd(&s_cost, cost);
+    __syncthreads();
+    if (s_over || s_cost > max_cost * total) return false;
+    uint32_t loc[PER];
+    int run = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        loc[j] = cnt[tid * PER + j];
+        run += static_cast<int>(loc[j]);
+    }
+    int base, agg;
+    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(run, base, agg);
+    __syncthreads();  // all counters read before they become offsets
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        cnt[tid * PER + j] = static_cast<uint16_t>(base);
+        base += static_cast<int>(loc[j]);
+    }
+    if (tid == 0) cnt[NB] = static_cast<uint16_t>(total);
+    __syncthreads();
+    const uint32_t lm = (1u << sh) - 1u;
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+        const int e = i * T + tid;
+        if (e < total) {
+            const uint32_t b = (cbits > 0 ? (kr[i] >> cbits) << cb : 0u) |
+                               (((kr[i] & cmask) - cmin) >> sh);
+            const int pos = cnt[b] + static_cast<int>(rr[i]);
+            pk[pos] = (((kr[i] & cmask) - cmin) & lm) << 16 | s.idx0[PADI(e)];
+            bk[pos] = static_cast<uint16_t>(b);
+        }
+    }
+    __syncthreads();
+    const uint32_t bm = (1u << cb) - 1u;
+    for (int q = tid; q < total; q += T) {
+        const uint32_t b = bk[q];
+        const int lo = cnt[b], hi = cnt[b + 1];
+        const uint32_t v = pk[q];
+        int c = lo;
+        if (hi - lo > 1)
+            for (int j = lo; j < hi; ++j) c += pk[j] < v;
+        const uint32_t col = cmin + (((b & bm) << sh) | (v >> 16));
+        s.key0[PADI(c)] = cbits > 0 ? ((b >> cb) << cbits) | col : col;
+        s.idx0[PADI(c)] = static_cast<uint16_t>(v & 0xffffu);
+    }
+    __syncthreads();
+    return true;
+}
+
+// Sort the expanded tile: merge of presorted runs, or radix when cheaper
+// (csort > 0: try the counting sort first when the merge tree is >= 3 levels
+// deep — or only in place of the radix sort (radix_only) — with csort as its
+// cost cap).
+template <int T, int CAPM>
+__device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width,
+                                         int csort = 0, int cbits = 0,
+                                         bool radix_only = false) {
     const int R = s.nruns;
     const int levels = R > 1 ? 32 - __clz(R - 1) : 0;
     // MSD counting sort when the columns spread evenly over the buckets (cfg2:
@@ -367,7 +516,11 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     constexpr int RB = MergeShared<T, CAPM>::RB;
     const int passes = (bits + RB - 1) / RB;
     // measured: cfg4 (5 levels vs 4 passes) prefers merge
-    if (levels > passes + 1 || R > MergeShared<T, CAPM>::MAXRUNS) {
+    const bool radix = levels > passes + 1 || R > MergeShared<T, CAPM>::MAXRUNS;
+    if (csort > 0 && levels >= 3 && (radix || !radix_only) &&
+        count_sort_tile<T, CAPM>(s, total, width, cbits, csort))
+        return 0;
+    if (radix) {
         radix_sort_tile<T, CAPM>(s, total, bits);
         return 0;
     }

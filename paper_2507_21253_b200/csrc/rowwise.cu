@@ -413,7 +413,7 @@ __global__ void window_c0_kernel(const Window* __restrict__ wins, const int32_t*
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
 __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : 4)) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
-                                                      const Window* __restrict__ wins, OutCtx out) {
+                                                      const Window* __restrict__ wins, OutCtx out, int csort) {
     using S = MergeShared<T, CAPM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S& s = *reinterpret_cast<S*>(smem_raw);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
     }
     const int total =
         expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s, wsofs, wwi, wrs, wdn);
-    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(c1 - c0));
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(c1 - c0), csort);
     (void)tid;
     int64_t base = out.crp[row - out.row_begin];
     if (w >= 0) base += out.win_scan[w] - out.win_scan[wins[w].first];
@@ -868,8 +868,14 @@ void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, con
         static const std::string nm_win = "esc_merge<" + std::to_string(T) + "," +
                                           std::to_string(CAPM) + ",win>";
         const std::string& nm = wins ? nm_win : nm_row;
+        // BSP_CSORT=0: radix/merge only (no counting sort)
+        static const int csort = [] {
+            const char* e = std::getenv("BSP_CSORT");
+            return e ? std::atoi(e) : 1000;
+        }();
         set_smem(k, sizeof(S));
-        BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out);
+        BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out,
+                      csort);
     } else {
         // BSP_HASH=plain: insert straight from the loads (no staging)
         static const bool staged = [] {
