@@ -29,8 +29,10 @@ struct Mats {
     const int32_t* __restrict__ bcol;
     const double* __restrict__ bval;
     int32_t ncols;  // columns of B (= of C)
-    // planner start tables (windows): absolute B offsets per (window, segment)
-    const int64_t* __restrict__ starts = nullptr;
+    // planner start tables (windows): absolute B offsets per (window, segment),
+    // 32-bit (tables are only built when nnz(B) < 2^32)
+    const uint32_t* __restrict__ starts = nullptr;
+    int64_t bnnz = 0;  // nnz(B) (host-side decisions)
 };
 
 struct Window {
@@ -75,7 +77,7 @@ __device__ __forceinline__ void segment_range(const Mats& m, bool full, int64_t 
                                               int64_t p, int64_t rs, int64_t d, int32_t c0,
                                               int32_t c1, int64_t& b0, int64_t& b1) {
     if (!full && sofs >= 0) {
-        const int64_t* st = m.starts + sofs + (p - rs);
+        const uint32_t* st = m.starts + sofs + (p - rs);
         b0 = __ldg(st + int64_t{wi} * d);
         b1 = __ldg(st + int64_t{wi + 1} * d);
         return;
@@ -179,7 +181,7 @@ struct RowwisePlan {
     int64_t wcls_off[NWCLS + 1]{};
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
-    DBuf<int64_t> starts; // planner per-(window, segment) start tables (absolute)
+    DBuf<uint32_t> starts; // planner per-(window, segment) start tables (absolute)
     bool light_sym_done = false;  // light rows counted on the side stream
     // Matrices as seen by the window kernels (start tables attached).
     Mats with_starts(const Mats& m) const {

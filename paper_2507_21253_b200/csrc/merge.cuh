@@ -99,15 +99,32 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // Warp-contiguous split of `ct` flattened run elements over `nwarps` warps
-// (slices rounded to 32): this lane starts at element e (< we) inside run q.
-__device__ __forceinline__ void warp_slice_begin(const int32_t* poff, int nr, int ct, int nwarps,
-                                                 int& e, int& we, int& q) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// (slices rounded to 32): this warp covers [e0, we); qa is the run holding
+// element e0 (warp-uniform).
+__device__ __forceinline__ void warp_slice(const int32_t* poff, int nr, int ct, int nwarps,
+                                           int& e0, int& we, int& qa) {
+    const int warp = threadIdx.x >> 5;
     const int ew = (((ct + nwarps - 1) / nwarps) + 31) & ~31;
-    const int wb = min(ct, warp * ew);
-    we = min(ct, wb + ew);
-    e = wb + lane;
-    q = e < we ? find_run(poff, nr, run_search_step(nr), e) : 0;
+    e0 = min(ct, warp * ew);
+    we = min(ct, e0 + ew);
+    qa = e0 < we ? find_run(poff, nr, run_search_step(nr), e0) : 0;
+}
+
+// Run of element e0 + lane, for 32 consecutive elements at once: lane l reads
+// the start of run qa + 1 + l, the starts that fall inside (e0, e0 + 32) are
+// OR-reduced into one mask (runs are non-empty, so at most 31 of them), and
+// each lane counts the starts at or below its element.  Advances qa to the
+// run holding e0 + 32.  One smem load per lane instead of a per-lane walk
+// over every run boundary (runs of heavy-row windows average a few products).
+// Warp-uniform: all 32 lanes call it.
+__device__ __forceinline__ int warp_runs(const int32_t* poff, int nr, int e0, int& qa) {
+    const int lane = threadIdx.x & 31;
+    const int idx = qa + 1 + lane;
+    const int rel = (idx <= nr ? poff[idx] : 0x3fffffff) - e0;
+    const unsigned mask = __reduce_or_sync(0xffffffffu, rel > 0 && rel < 32 ? 1u << rel : 0u);
+    const int my = qa + __popc(mask & (0xffffffffu >> (31 - lane)));
+    qa += __popc(mask) + (__any_sync(0xffffffffu, rel == 32) ? 1 : 0);
+    return my;
 }
 
 template <int T, int CAPM, bool VALUES>
@@ -156,16 +173,19 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         // fix-up pass.
         uint16_t* rid = s.idx(1);
         {
-            int e, we, q;
-            warp_slice_begin(s.poff, nr, ct, T / 32, e, we, q);
-            for (; e < we; e += 32) {
-                while (s.poff[q + 1] <= e) ++q;
-                const int64_t src = s.pstart[q] + (e - s.poff[q]);
-                const int g = total + e;
-                cp_async4(&s.key(0)[PADI(g)], m.bcol + src);
-                if (VALUES) {
-                    cp_async8(&s.val[g], m.bval + src);
-                    rid[g] = static_cast<uint16_t>(q);
+            int e0, we, qa;
+            warp_slice(s.poff, nr, ct, T / 32, e0, we, qa);
+            for (; e0 < we; e0 += 32) {
+                const int q = warp_runs(s.poff, nr, e0, qa);
+                const int e = e0 + (threadIdx.x & 31);
+                if (e < we) {
+                    const int64_t src = s.pstart[q] + (e - s.poff[q]);
+                    const int g = total + e;
+                    cp_async4(&s.key(0)[PADI(g)], m.bcol + src);
+                    if (VALUES) {
+                        cp_async8(&s.val[g], m.bval + src);
+                        rid[g] = static_cast<uint16_t>(q);
+                    }
                 }
             }
             cp_async_wait_all();

@@ -117,12 +117,13 @@ constexpr uint32_t DENSE_BIT = 0x80000000u;
 
 struct PlanCountShared {
     int32_t hist[MAXBINS];
+    int32_t pre[MAXBINS + 1];  // inclusive-exclusive prefix: pre[b] = products in bins < b
     typename cub::BlockScan<int32_t, PLAN_T>::TempStorage scan;
 };
 
-// Start tables of up to STAGE entries (int64) are built in smem and stored
+// Start tables of up to STAGE entries (uint32) are built in smem and stored
 // coalesced.
-constexpr int STAGE = MAXBINS;
+constexpr int STAGE = 2 * MAXBINS;
 struct PlanWriteShared {
     int32_t binwin[MAXBINS];  // bin -> window
     union {
@@ -130,7 +131,7 @@ struct PlanWriteShared {
             uint32_t wc0[MAXBINS + 1];  // window -> c0 | DENSE_BIT (+ sentinel ncols)
             int32_t wpre[MAXBINS + 1];  // window -> product prefix at c0 (+ sentinel P)
         } w;
-        int64_t stage[STAGE + 1];
+        uint32_t stage[STAGE + 1];
     } u;
 };
 
@@ -212,28 +213,55 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
         }
     });
     __syncthreads();
-    // Greedy cut over the bins (one thread; ~1024 bins): a window grows while
-    // it holds <= capg products; a bin above capg stands alone (dense above
-    // CAP), and the bin after it starts a new window.  Every packed window
-    // thus fits the capg-product tile.
+    // Greedy cut over the bins: a window grows while it holds <= capg
+    // products; a bin above capg stands alone (dense above CAP), and the bin
+    // after it starts a new window.  Every packed window thus fits the
+    // capg-product tile.  With the bin prefix sums, each window's end is one
+    // binary search (the largest e with pre[e] - pre[s] <= capg), so the walk
+    // costs O(windows log bins) instead of a serial pass over every bin.
+    constexpr int PB = (MAXBINS + PLAN_T - 1) / PLAN_T;
+    {
+        int loc[PB], run = 0;
+#pragma unroll
+        for (int j = 0; j < PB; ++j) {
+            const int b = threadIdx.x * PB + j;
+            loc[j] = b < nbins ? s.hist[b] : 0;
+            run += loc[j];
+        }
+        int base;
+        cub::BlockScan<int32_t, PLAN_T>(s.scan).ExclusiveSum(run, base);
+#pragma unroll
+        for (int j = 0; j < PB; ++j) {
+            const int b = threadIdx.x * PB + j;
+            if (b <= nbins) s.pre[b] = base;
+            base += loc[j];
+        }
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
         uint2* dd = desc + doff[hrow];
-        int32_t nw = 0, acc = 0, pre = 0;
-        bool prev_big = false;
-        for (int b = 0; b < nbins; ++b) {
-            const int32_t c = s.hist[b];
-            if (b == 0 || prev_big || c > capg || acc + c > capg) {
-                dd[nw++] = make_uint2(static_cast<uint32_t>(b << log_binw) | (c > CAP ? DENSE_BIT : 0u),
-                                      static_cast<uint32_t>(pre));
-                acc = c;
-            } else {
-                acc += c;
+        const int32_t* pre = s.pre;
+        int32_t nw = 0;
+        int b = 0;
+        while (b < nbins) {
+            const int32_t c = pre[b + 1] - pre[b];
+            int e = b + 1;
+            if (c <= capg) {
+                // largest e <= nbins with pre[e] <= pre[b] + capg
+                const int32_t lim = pre[b] + capg;
+                int lo = b + 1, hi = nbins;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (pre[mid] <= lim) lo = mid; else hi = mid - 1;
+                }
+                e = lo;
             }
-            prev_big = c > capg;
-            pre += c;
+            dd[nw++] = make_uint2(static_cast<uint32_t>(b << log_binw) | (c > CAP ? DENSE_BIT : 0u),
+                                  static_cast<uint32_t>(pre[b]));
+            b = e;
         }
         nwin[hrow] = nw;
-        dd[nw] = make_uint2(static_cast<uint32_t>(m.ncols), static_cast<uint32_t>(pre));
+        dd[nw] = make_uint2(static_cast<uint32_t>(m.ncols), static_cast<uint32_t>(pre[nbins]));
     }
 }
 
@@ -245,7 +273,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
     const int32_t* __restrict__ nwin, const int64_t* __restrict__ doff,
     const uint2* __restrict__ desc, const int64_t* __restrict__ win_off, Window* __restrict__ wins,
     uint8_t* __restrict__ win_cat, const int64_t* __restrict__ start_off, int64_t start_budget,
-    int64_t* __restrict__ starts) {
+    uint32_t* __restrict__ starts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PlanWriteShared& s = *reinterpret_cast<PlanWriteShared*>(smem_raw);
     const int32_t hrow = blockIdx.x;
@@ -303,7 +331,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
     const int d = static_cast<int>(m.arp[row + 1] - m.arp[row]);
     const int64_t tsz = int64_t{wtot + 1} * d;
     const bool staged = tsz <= STAGE;
-    int64_t* tab = staged ? s.u.stage : starts + sofs;
+    uint32_t* tab = staged ? s.u.stage : starts + sofs;
     // entries are absolute B offsets (segment start b0 + element index)
     stream_segments(m, row, [&](int p, int q0, int len, const int32_t* cols, int& carry,
                                 int64_t b0) {
@@ -317,17 +345,18 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
             int wp = __shfl_up_sync(0xffffffffu, wq, 1);
             if (lane == 0) wp = carry;
             if (q < len)
-                for (int w2 = wp + 1; w2 <= wq; ++w2) tab[w2 * int64_t{d} + p] = b0 + q;
+                for (int w2 = wp + 1; w2 <= wq; ++w2)
+                    tab[w2 * int64_t{d} + p] = static_cast<uint32_t>(b0 + q);
             carry = __shfl_sync(0xffffffffu, wq, ::min(31, len - 1 - qb));
         }
         // windows after the last element start at len
         if (q0 + 32 * PLAN_U >= len)
             for (int w2 = carry + 1 + lane; w2 <= wtot; w2 += 32)
-                tab[w2 * int64_t{d} + p] = b0 + len;
+                tab[w2 * int64_t{d} + p] = static_cast<uint32_t>(b0 + len);
     });
     if (staged) {
         __syncthreads();
-        int64_t* st = starts + sofs;
+        uint32_t* st = starts + sofs;
         for (int i = threadIdx.x; i < tsz; i += PLAN_T) st[i] = s.u.stage[i];
     }
 }
@@ -534,11 +563,12 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
             }
         };
         if constexpr (STAGED) {
-            int e, we, q;
-            warp_slice_begin(s.poff, nr, ct, T / 32, e, we, q);
-            for (; e < we; e += 32) {
-                while (s.poff[q + 1] <= e) ++q;
-                cp_async4(&s.stage[e], m.bcol + s.pstart[q] + (e - s.poff[q]));
+            int e0, we, qa;
+            warp_slice(s.poff, nr, ct, T / 32, e0, we, qa);
+            for (; e0 < we; e0 += 32) {
+                const int q = warp_runs(s.poff, nr, e0, qa);
+                const int e = e0 + (threadIdx.x & 31);
+                if (e < we) cp_async4(&s.stage[e], m.bcol + s.pstart[q] + (e - s.poff[q]));
             }
             cp_async_wait_all();
             __syncthreads();
@@ -877,16 +907,16 @@ void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, con
         BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins, out,
                       csort);
     } else {
-        // BSP_HASH=plain: insert straight from the loads (no staging)
-        static const bool staged = [] {
-            const char* e = std::getenv("BSP_HASH");
-            return !(e && std::string(e) == "plain");
-        }();
         static const std::string nm_row = "hash_count<" + std::to_string(T) + "," +
                                           std::to_string(CAPM) + ">";
         static const std::string nm_win = "hash_count<" + std::to_string(T) + "," +
                                           std::to_string(CAPM) + ",win>";
         const std::string& nm = wins ? nm_win : nm_row;
+        // BSP_HASH=plain: insert straight from the loads (no staging)
+        static const bool staged = [] {
+            const char* e = std::getenv("BSP_HASH");
+            return !(e && std::string(e) == "plain");
+        }();
         if (staged) {
             using S = HashShared<T, CAPM, true>;
             auto k = hash_count_kernel<T, CAPM, true>;
@@ -929,8 +959,10 @@ void launch_dense(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, co
 }  // namespace
 
 Mats make_mats(const bsp_csr* A, const bsp_csr* B) {
-    return Mats{A->row_ptr, A->col_idx, A->values, B->row_ptr, B->col_idx, B->values,
-                static_cast<int32_t>(B->ncols)};
+    Mats m{A->row_ptr, A->col_idx, A->values, B->row_ptr, B->col_idx, B->values,
+           static_cast<int32_t>(B->ncols)};
+    m.bnnz = B->nnz;
+    return m;
 }
 
 template <bool NUMERIC>
@@ -1028,20 +1060,21 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         d2h(h, &hv[1], soff.p + nh, 1);
         sync(h);
         plan.nwin = hv[0];
-        // Start-table budget (8-byte entries): at least min(2^30 entries,
-        // 1/16 of available HBM); up to 2^31 entries when HBM also holds an
-        // upper bound of C (12 B x products) and a 2 GB margin (the bound is
-        // loose when columns repeat: cfg3).  Rows in scan order that fit get
-        // a table, the rest binary-search.
-        constexpr int64_t EB = sizeof(int64_t);
+        // Start-table budget (4-byte entries, absolute B offsets: only when
+        // nnz(B) < 2^32): at least min(2^30 entries, 1/16 of available HBM);
+        // up to 2^31 entries when HBM also holds an upper bound of C (12 B x
+        // products) and a 2 GB margin (the bound is loose when columns
+        // repeat: cfg3).  Rows in scan order that fit get a table, the rest
+        // binary-search.
+        constexpr int64_t EB = sizeof(uint32_t);
         const int64_t avail = static_cast<int64_t>(available_bytes(h));
         const int64_t spare = avail - 12 * h->stats.products - (int64_t{2} << 30);
         const int64_t floor_entries = std::min<int64_t>(int64_t{1} << 30, avail / (16 * EB));
         const int64_t budget = std::min<int64_t>(
             hv[1], std::max<int64_t>(floor_entries,
                                      std::min<int64_t>(int64_t{1} << 31, spare / EB)));
-        const bool use_starts = budget > 0;
-        if (use_starts) plan.starts = DBuf<int64_t>(h, budget);
+        const bool use_starts = budget > 0 && m.bnnz < (int64_t{1} << 32);
+        if (use_starts) plan.starts = DBuf<uint32_t>(h, budget);
         plan.wins = DBuf<Window>(h, plan.nwin);
         DBuf<uint8_t> dense(h, plan.nwin);
         set_smem(plan_write_kernel, sizeof(PlanWriteShared));
