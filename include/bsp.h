@@ -116,9 +116,9 @@ typedef struct {
 typedef struct {
     int64_t products;     /* sum over rows of intermediate products */
     int64_t nnz_out;      /* nnz(C) */
-    int64_t units[16];    /* work units: [0..6] rows per class (0 empty; 1..5 light, at
-                             most 128/512/2048/3072/4096 products; 6 heavy), [8] sparse
-                             windows, [9] dense windows, [10] cluster tiles */
+    int64_t units[16];    /* work units: [0..7] rows per class (0 empty; 1..6 light, at
+                             most 128/512/1024/2048/3072/4096 products; 7 heavy), [8]
+                             sparse windows, [9] dense windows, [10] cluster tiles */
     int32_t kernels_launched;
     int32_t chunks;       /* row chunks (1 unless C exceeded the budget) */
 } bsp_exec_stats;

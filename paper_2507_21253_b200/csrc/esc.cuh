@@ -18,8 +18,8 @@ constexpr int NWCLS = 4;
 constexpr int WD = 4096;      // dense window width in columns
 constexpr int LOG_WD = 12;
 constexpr int MAXBINS = 4096; // planner histogram bins per heavy row
-constexpr int NCLS = 7;       // 0 empty, 1..5 light classes, 6 heavy
-static __constant__ int kClassCap[NCLS] = {0, 128, 512, 2048, 3072, 4096, 0x7fffffff};
+constexpr int NCLS = 8;       // 0 empty, 1..6 light classes, 7 heavy
+static __constant__ int kClassCap[NCLS] = {0, 128, 512, 1024, 2048, 3072, 4096, 0x7fffffff};
 
 struct Mats {
     const int64_t* __restrict__ arp;

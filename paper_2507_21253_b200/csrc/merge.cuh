@@ -30,7 +30,7 @@ struct MergeShared {
     // radix digit bits: CUB's rank storage is T x 2^RB / 2 words whatever the
     // tile size, so 256-thread tiles of <= 3072 products (sized for 3-4
     // CTAs/SM) use 5-bit digits (16 KB), the others 6-bit digits
-    static constexpr int RB = (T >= 256 && CAPM <= 3072) ? 5 : 6;
+    static constexpr int RB = (T >= 128 && CAPM <= 3072) ? 5 : 6;
     using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, RB>;
     // run offsets: tiles with more runs than this use the radix sort
     static constexpr int MAXRUNS = CAPM < 1024 ? CAPM : 1024;
@@ -38,7 +38,7 @@ struct MergeShared {
     static constexpr int NHIST = CAPM <= 512 ? CAPM / 2 : ((CAPM + T - 1) / T) * (T / 32);
     // counting sort: buckets on the top column bits (about 1.5-2 products each)
     static constexpr int NB = CAPM >= 3072 ? 2048 : (CAPM >= 2048 ? 1024 : CAPM / 2);
-    static constexpr int LNB = NB >= 2048 ? 11 : (NB >= 1024 ? 10 : (NB >= 256 ? 8 : 6));
+    static constexpr int LNB = 31 - __builtin_clz(static_cast<unsigned>(NB));
     // buffer 0 (also the radix-sort input/output)
     uint32_t key0[NP];
     uint16_t idx0[NP];

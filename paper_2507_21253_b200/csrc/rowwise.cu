@@ -441,7 +441,7 @@ __global__ void window_c0_kernel(const Window* __restrict__ wins, const int32_t*
 // K3': merge-based exact numeric tile and hash-count symbolic tile
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
-__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : 4)) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : (T == 128 ? 8 : 4))) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
                                                       const Window* __restrict__ wins, OutCtx out, int csort) {
     using S = MergeShared<T, CAPM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -939,9 +939,10 @@ void launch_light(bsp_handle h, int cls, const Mats& m, const int32_t* ids, int6
     switch (cls) {
         case 1: launch_tile<32, 128, NUMERIC>(h, m, ids, n, nullptr, out); break;
         case 2: launch_tile<64, 512, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 3: launch_tile<256, 2048, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 4: launch_tile<256, 3072, NUMERIC>(h, m, ids, n, nullptr, out); break;
-        case 5: launch_tile<256, 4096, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 3: launch_tile<128, 1024, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 4: launch_tile<256, 2048, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 5: launch_tile<256, 3072, NUMERIC>(h, m, ids, n, nullptr, out); break;
+        case 6: launch_tile<256, 4096, NUMERIC>(h, m, ids, n, nullptr, out); break;
         default: break;
     }
 }
@@ -1135,7 +1136,7 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
             sort_list(plan.dense_ids.p, plan.ndense);
         }
     }
-    for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];  // [6] = heavy rows
+    for (int c = 0; c < NCLS; ++c) h->stats.units[c] = plan.class_count[c];  // [7] = heavy rows
     h->stats.units[8] = plan.nsparse;
     h->stats.units[9] = plan.ndense;
 }

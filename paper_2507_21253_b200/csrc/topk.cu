@@ -514,12 +514,13 @@ int bsp_spgemm_topk(bsp_handle h, const bsp_csr* A, const bsp_csr* At, int32_t t
                            rn.p, wj.p, ws.p, wn.p);
         launch_topk<64, 8>(h, m, plan.lists.p + co[2], cc[2], nullptr, topk, jacc_th, rj.p, rs.p,
                            rn.p, wj.p, ws.p, wn.p);
-        launch_topk<128, 16>(h, m, plan.lists.p + co[3], cc[3], nullptr, topk, jacc_th, rj.p, rs.p,
-                             rn.p, wj.p, ws.p, wn.p);
-        // light classes 4 and 5 (<= 3072, <= 4096 products) are adjacent in
-        // the row list and share the 4096-product tile
-        static_assert(NCLS == 7, "top-k launches one tile per light class");
-        launch_topk<256, 16>(h, m, plan.lists.p + co[4], cc[4] + cc[5], nullptr, topk, jacc_th,
+        // light classes 3 and 4 (<= 1024, <= 2048 products) share the
+        // 2048-product tile, classes 5 and 6 (<= 3072, <= 4096) the 4096 one
+        // (adjacent in the row list)
+        static_assert(NCLS == 8, "top-k launches one tile per light class pair");
+        launch_topk<128, 16>(h, m, plan.lists.p + co[3], cc[3] + cc[4], nullptr, topk, jacc_th,
+                             rj.p, rs.p, rn.p, wj.p, ws.p, wn.p);
+        launch_topk<256, 16>(h, m, plan.lists.p + co[5], cc[5] + cc[6], nullptr, topk, jacc_th,
                              rj.p, rs.p, rn.p, wj.p, ws.p, wn.p);
         if (plan.nwin > 0) {
             const Mats mw = plan.with_starts(m);
