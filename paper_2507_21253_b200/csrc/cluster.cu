@@ -146,8 +146,8 @@ __global__ void cluster_to_csr_kernel(const int32_t* __restrict__ sizes,
 // ---------------------------------------------------------------------------
 // cluster products + routing
 // ---------------------------------------------------------------------------
-constexpr int NCC = 5;  // 0: row-wise classes, 1: <=512, 2: <=2048, 3: <=3072, 4: <=4096 products
-__constant__ int kClusterCap[NCC] = {0, 512, 2048, 3072, 4096};
+constexpr int NCC = 6;  // 0: row-wise classes, 1: <=512, 2: <=1024, 3: <=2048, 4: <=3072, 5: <=4096 products
+__constant__ int kClusterCap[NCC] = {0, 512, 1024, 2048, 3072, 4096};
 
 __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
                                         uint8_t* __restrict__ ccls, uint8_t* __restrict__ row_skip,
@@ -217,7 +217,7 @@ __global__ void cluster_bucket_kernel(const uint8_t* __restrict__ ccls, int64_t 
 // original rows.
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
-__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : 4))
+__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : (T == 128 ? 8 : 4)))
     cluster_tile_kernel(ClusterMats m, const int32_t* __restrict__ ids, int cbits, int csort,
                         int csort_radix_only,
                         const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
@@ -235,8 +235,10 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
     const int64_t u0 = m.ccp[c], u1 = m.ccp[c + 1];
     const int64_t vbase = m.vptr[c];
     if (tid < K) s_mbase[tid] = crp[m.row_map[m.member_ptr[c] + tid]];
-    uint2* slot_sm = reinterpret_cast<uint2*>(s.pav);  // per slot {segment length, member mask}
+    auto& x = s.ex();
+    uint2* slot_sm = reinterpret_cast<uint2*>(x.pav);  // per slot {segment length, member mask}
     uint16_t* slot_rb = s.ro(1);                       // per slot first run index (idle buffer)
+    static_assert(S::EX_IN_U, "cluster tiles keep the expansion state in the union (below ro1)");
     int total = 0, nruns = 0;
     for (int64_t uc = u0; uc < u1; uc += T) {
         const int64_t u = uc + tid;
@@ -254,8 +256,8 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
         const int packed = seg * nl | (nl << 16);
         int off, agg;
         cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
-        s.pstart[tid] = start;
-        s.poff[tid] = total + (off & 0xffff);
+        x.pstart[tid] = start;
+        x.poff[tid] = total + (off & 0xffff);
         slot_sm[tid] = make_uint2(static_cast<uint32_t>(seg), nl ? msk : 0u);
         slot_rb[tid] = static_cast<uint16_t>(::min(nruns + (off >> 16), MAXRUNS));
         __syncthreads();
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
             const uint2 sm = slot_sm[tid];
             uint32_t mm = sm.y;
             int r = slot_rb[tid];
-            int o = s.poff[tid];
+            int o = x.poff[tid];
             while (mm && r < MAXRUNS) {
                 mm &= mm - 1;
                 s.ro(0)[r++] = static_cast<uint16_t>(o);
@@ -276,8 +278,8 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
             const uint2 sm = slot_sm[slot];
             if (sm.y == 0) continue;
             const int l_seg = static_cast<int>(sm.x);
-            const int64_t st = s.pstart[slot];
-            const int o = s.poff[slot];
+            const int64_t st = x.pstart[slot];
+            const int o = x.poff[slot];
             const int64_t vb = vbase + (uc + slot - u0) * K;
             for (int q = lane; q < l_seg; q += 32) {
                 // one load of the B entry, reused by every live member
@@ -387,11 +389,12 @@ void launch_cluster(bsp_handle h, const ClusterMats& m, const int32_t* ids, int6
 void run_cluster_classes(bsp_handle h, const ClusterMats& m, const int32_t* lists,
                          const int64_t* off, const int64_t* cnt, int cbits, const int64_t* crp,
                          int32_t* ocol, double* oval) {
-    static_assert(NCC == 5, "one launch per cluster tile class");
+    static_assert(NCC == 6, "one launch per cluster tile class");
     launch_cluster<64, 512>(h, m, lists + off[1], cnt[1], cbits, crp, ocol, oval);
-    launch_cluster<256, 2048>(h, m, lists + off[2], cnt[2], cbits, crp, ocol, oval);
-    launch_cluster<256, 3072>(h, m, lists + off[3], cnt[3], cbits, crp, ocol, oval);
-    launch_cluster<256, 4096>(h, m, lists + off[4], cnt[4], cbits, crp, ocol, oval);
+    launch_cluster<128, 1024>(h, m, lists + off[2], cnt[2], cbits, crp, ocol, oval);
+    launch_cluster<256, 2048>(h, m, lists + off[3], cnt[3], cbits, crp, ocol, oval);
+    launch_cluster<256, 3072>(h, m, lists + off[4], cnt[4], cbits, crp, ocol, oval);
+    launch_cluster<256, 4096>(h, m, lists + off[5], cnt[5], cbits, crp, ocol, oval);
 }
 
 // access statistics (reference cluster_spgemm.hpp:26-45, counted at :129-135)
@@ -704,7 +707,7 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         const Mats m = make_mats(&acsr, B);
         RowwisePlan plan;  // rows outside cluster tiles (incl. heavy windows)
         build_plan(h, m, 0, n, skip.p, plan, nullptr);
-        h->stats.units[10] = cnt[1] + cnt[2] + cnt[3] + cnt[4];  // cluster tiles
+        h->stats.units[10] = cnt[1] + cnt[2] + cnt[3] + cnt[4] + cnt[5];  // cluster tiles
         DBuf<int64_t> row_nnz(h, n + 1);
         BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
         // Symbolic: C's row structure does not depend on the clustering, so the

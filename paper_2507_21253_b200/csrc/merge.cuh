@@ -15,6 +15,8 @@
 
 #include "esc.cuh"
 
+#include <type_traits>
+
 #include <cub/block/block_radix_sort.cuh>
 
 namespace bsp {
@@ -36,19 +38,28 @@ struct MergeShared {
     static constexpr int MAXRUNS = CAPM < 1024 ? CAPM : 1024;
     // counters: MSD buckets (small tiles) or the reduction's (row, warp) heads
     static constexpr int NHIST = CAPM <= 512 ? CAPM / 2 : ((CAPM + T - 1) / T) * (T / 32);
-    // counting sort: buckets on the top column bits (about 1.5-2 products each)
-    static constexpr int NB = CAPM >= 3072 ? 2048 : (CAPM >= 2048 ? 1024 : CAPM / 2);
+    // counting sort: buckets on the top column bits (about one product each)
+    static constexpr int NB = CAPM >= 3072 ? 4096 : (CAPM >= 2048 ? 2048 : CAPM / 2);
     static constexpr int LNB = 31 - __builtin_clz(static_cast<unsigned>(NB));
+    // expansion-only state (compacted segments of the current chunk)
+    struct Ex {
+        int64_t pstart[T];
+        int32_t poff[T + 1];
+        double pav[T];
+    };
+    // ... lives in the union (over key1, idle during the expansion) when it fits
+    static constexpr bool EX_IN_U = sizeof(Ex) <= sizeof(uint32_t) * NP;
     // buffer 0 (also the radix-sort input/output)
     uint32_t key0[NP];
     uint16_t idx0[NP];
     uint16_t ro0[MAXRUNS + 2];
     double val[CAPM];
-    // buffer 1 of the merge, aliased with the radix sort's temp storage
+    // buffer 1 of the merge, aliased with the radix sort's temp storage, the
+    // counting sort's arrays and the expansion state
     union U {
         struct B1 {
             uint32_t key1[NP];
-            uint16_t idx1[NP];
+            uint16_t idx1[NP];  // also the expansion's run id per product
             uint16_t ro1[MAXRUNS + 2];
         } m;
         typename RSort::TempStorage sort;
@@ -57,15 +68,18 @@ struct MergeShared {
             uint32_t cnt[NB / 2 + 1];  // 16-bit bucket counts, then bucket starts
             uint16_t bucket[CAPM];     // bucket of each bucketed slot
         } c;
+        Ex x;
     } u;
+    struct NoEx {};
+    std::conditional_t<EX_IN_U, NoEx, Ex> xo;
     uint32_t hist[NHIST];
     __device__ __forceinline__ uint32_t* key(int b) { return b ? u.m.key1 : key0; }
     __device__ __forceinline__ uint16_t* idx(int b) { return b ? u.m.idx1 : idx0; }
     __device__ __forceinline__ uint16_t* ro(int b) { return b ? u.m.ro1 : ro0; }
+    __device__ __forceinline__ Ex& ex() {
+        if constexpr (EX_IN_U) return u.x; else return xo;
+    }
     typename cub::BlockScan<int32_t, T>::TempStorage scan;
-    int64_t pstart[T];
-    int32_t poff[T + 1];
-    double pav[T];
     int nruns;
 };
 
@@ -137,6 +151,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
     const int64_t rs = wrs >= 0 ? wrs : m.arp[row];
     const int64_t re = wrs >= 0 ? wrs + wd : m.arp[row + 1];
     int total = 0, nruns = 0;
+    auto& x = s.ex();
     for (int64_t pc = rs; pc < re; pc += T) {
         const int64_t p = pc + tid;
         int len = 0;
@@ -158,12 +173,12 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         if (len > 0) {
             if (nruns + r < MergeShared<T, CAPM>::MAXRUNS)
                 s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
-            s.pstart[r] = start;
-            s.poff[r] = off & 0xffff;
-            if (VALUES) s.pav[r] = av;
+            x.pstart[r] = start;
+            x.poff[r] = off & 0xffff;
+            if (VALUES) x.pav[r] = av;
         }
         const int nr = agg >> 16, ct = agg & 0xffff;
-        if (tid == 0) s.poff[nr] = ct;
+        if (tid == 0) x.poff[nr] = ct;
         __syncthreads();
         // Gather: warp w takes a contiguous slice of the chunk's products, its
         // lanes consecutive ones (coalesced), and copies each product's B
@@ -174,12 +189,12 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         uint16_t* rid = s.idx(1);
         {
             int e0, we, qa;
-            warp_slice(s.poff, nr, ct, T / 32, e0, we, qa);
+            warp_slice(x.poff, nr, ct, T / 32, e0, we, qa);
             for (; e0 < we; e0 += 32) {
-                const int q = warp_runs(s.poff, nr, e0, qa);
+                const int q = warp_runs(x.poff, nr, e0, qa);
                 const int e = e0 + (threadIdx.x & 31);
                 if (e < we) {
-                    const int64_t src = s.pstart[q] + (e - s.poff[q]);
+                    const int64_t src = x.pstart[q] + (e - x.poff[q]);
                     const int g = total + e;
                     cp_async4(&s.key(0)[PADI(g)], m.bcol + src);
                     if (VALUES) {
@@ -196,7 +211,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
             const int g = total + e;
             s.key(0)[PADI(g)] -= static_cast<uint32_t>(c0);
             s.idx(0)[PADI(g)] = static_cast<uint16_t>(g);
-            if (VALUES) s.val[g] = __dmul_rn(s.pav[rid[g]], s.val[g]);
+            if (VALUES) s.val[g] = __dmul_rn(x.pav[rid[g]], s.val[g]);
         }
         total += ct;
         nruns += nr;
