@@ -1380,6 +1380,12 @@ int bsp_spgemm_rowwise_host(bsp_handle h, const bsp_host_csr* A, const bsp_host_
     });
 }
 
+// Partition cost of a row with P intermediate products (the rule
+// distributed.product_split mirrors).
+constexpr int64_t row_cost(int64_t P) {
+    return P > 65536 ? 3 * P : (P > 4096 ? 2 * P : P);
+}
+
 int bsp_partition_rows(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int32_t nparts,
                        int64_t* bounds_out) {
     return guarded([&] {
@@ -1390,14 +1396,19 @@ int bsp_partition_rows(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int32_t
         const int rc = bsp_spgemm_products(h, A, B, prod.p, &total);
         if (rc != BSP_OK) throw std::runtime_error(bsp_last_error());
         BSP_CUDA(cudaMemsetAsync(prod.p + n, 0, sizeof(int64_t), h->stream));
-        DBuf<int64_t> scan(h, n + 1);
-        exclusive_scan_i64(h, prod.p, scan.p, n + 1);
-        std::vector<int64_t> hs(n + 1);
-        d2h(h, hs.data(), scan.p, n + 1);
+        // Split on a per-row cost, not the raw product count: a heavy row's
+        // products (> 4096, planned into windows, counted by the window
+        // symbolic) cost about twice a light row's, the hub rows' (> 65536)
+        // three times (measured per-shard times, tools/shard_projection.py).
+        std::vector<int64_t> hp(n);
+        d2h(h, hp.data(), prod.p, n);
         sync(h);
+        std::vector<int64_t> hs(n + 1, 0);
+        for (int64_t i = 0; i < n; ++i)
+            hs[i + 1] = hs[i] + row_cost(hp[i]);
         bounds_out[0] = 0;
         for (int32_t g = 1; g < nparts; ++g) {
-            // first row whose exclusive prefix reaches total*g/nparts
+            // first row whose exclusive cost prefix reaches total*g/nparts
             const int64_t target = static_cast<int64_t>(
                 (static_cast<__int128>(hs[n]) * g) / nparts);
             const int64_t r = std::lower_bound(hs.begin(), hs.end(), target) - hs.begin();

@@ -16,13 +16,22 @@ from typing import Tuple
 import numpy as np
 
 
+def row_cost(row_products: np.ndarray) -> np.ndarray:
+    """Partition cost of each row (bsp_partition_rows' rule): a heavy row's
+    products (> 4096: planned windows + window symbolic) cost ~2 light ones,
+    a hub row's (> 65536) ~3 (per-shard timings, tools/shard_projection.py)."""
+    rp = np.asarray(row_products, dtype=np.int64)
+    return np.where(rp > 65536, 3 * rp, np.where(rp > 4096, 2 * rp, rp))
+
+
 def product_split(row_products: np.ndarray, nparts: int) -> np.ndarray:
-    """Bounds b[0..nparts] with b[g] = first row whose exclusive product
-    prefix reaches total*g/nparts (monotone, b[0]=0, b[-1]=nrows); identical
-    to the device rule of bsp_partition_rows."""
+    """Bounds b[0..nparts] with b[g] = first row whose exclusive cost prefix
+    reaches total*g/nparts (cost = row_cost); monotone, b[0]=0,
+    b[-1]=nrows; identical to the rule of bsp_partition_rows."""
     n = int(row_products.size)
+    cost = row_cost(row_products)
     pre = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(row_products, out=pre[1:])
+    np.cumsum(cost, out=pre[1:])
     total = int(pre[-1])
     b = np.zeros(nparts + 1, dtype=np.int64)
     for g in range(1, nparts):

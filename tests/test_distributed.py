@@ -79,9 +79,14 @@ def test_sharded_multiply_equals_single_rank():
 
 
 def test_product_split_rule():
-    prods = np.array([5, 0, 0, 100, 1, 1, 1, 1, 50, 2], dtype=np.int64)
-    b = D.product_split(prods, 3)
-    assert b[0] == 0 and b[-1] == prods.size and np.all(np.diff(b) >= 0)
-    pre = np.concatenate([[0], np.cumsum(prods)])
-    for g in range(1, 3):  # first row whose exclusive prefix reaches total*g/3
-        assert pre[b[g]] >= prods.sum() * g // 3 and (b[g] == 0 or pre[b[g] - 1] < prods.sum() * g // 3)
+    prods = np.array([5, 0, 0, 100, 1, 5000, 1, 1, 50, 2, 4097, 3, 70000, 9], dtype=np.int64)
+    for parts in (2, 3, 5):
+        b = D.product_split(prods, parts)
+        assert b[0] == 0 and b[-1] == prods.size and np.all(np.diff(b) >= 0)
+        cost = np.array([3 * p if p > 65536 else (2 * p if p > 4096 else p) for p in prods])
+        pre = np.concatenate([[0], np.cumsum(cost)])
+        for g in range(1, parts):  # first row whose exclusive cost prefix reaches total*g/parts
+            t = cost.sum() * g // parts
+            assert pre[b[g]] >= t and (b[g] == 0 or pre[b[g] - 1] < t)
+
+

@@ -124,6 +124,12 @@ def test_row_range_shards_concatenate(engine):
     full = engine.spgemm_rowwise(A, A).download()
     bounds = engine.partition_rows(A, A, 4)
     assert bounds[0] == 0 and bounds[-1] == a.nrows and np.all(np.diff(bounds) >= 0)
+    # the device split follows the documented cost rule (distributed.product_split)
+    deg = np.diff(a.row_ptr)
+    prods = np.add.reduceat(deg[a.col_idx], a.row_ptr[:-1].clip(max=a.nnz() - 1))
+    prods[np.diff(a.row_ptr) == 0] = 0
+    from paper_2507_21253_b200 import distributed as D
+    assert np.array_equal(bounds, D.product_split(prods, 4))
     parts = [engine.spgemm_rowwise_range(A, A, int(bounds[g]), int(bounds[g + 1])).download()
              for g in range(4)]
     assert np.array_equal(np.concatenate([p.col_idx for p in parts]), full.col_idx)
