@@ -145,7 +145,7 @@ template <int T, int CAPM, bool VALUES>
 __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c0, int32_t c1,
                                            bool full, MergeShared<T, CAPM>& s,
                                            int64_t wsofs = -1, int wwi = 0, int64_t wrs = -1,
-                                           int64_t wd = 0) {
+                                           int64_t wd = 0, bool defer = false) {
     const int tid = threadIdx.x;
     // windows carry their A row range (one dependent load less)
     const int64_t rs = wrs >= 0 ? wrs : m.arp[row];
@@ -206,11 +206,14 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
             cp_async_wait_all();
         }
         __syncthreads();
-        // fix-up: window-relative key, position, product a_ik * b_kj
+        // fix-up: product a_ik * b_kj; window-relative key and position
+        // (deferred: sort_tile applies them only on the paths that read them)
         for (int e = tid; e < ct; e += T) {
             const int g = total + e;
-            s.key(0)[PADI(g)] -= static_cast<uint32_t>(c0);
-            s.idx(0)[PADI(g)] = static_cast<uint16_t>(g);
+            if (!defer) {
+                s.key(0)[PADI(g)] -= static_cast<uint32_t>(c0);
+                s.idx(0)[PADI(g)] = static_cast<uint16_t>(g);
+            }
             if (VALUES) s.val[g] = __dmul_rn(x.pav[rid[g]], s.val[g]);
         }
         total += ct;
@@ -417,7 +420,7 @@ constexpr int CS_MAXB = 128;
 
 template <int T, int CAPM>
 __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width,
-                                                int cbits, int max_cost) {
+                                                int cbits, int max_cost, int kofs = -1) {
     using S = MergeShared<T, CAPM>;
     constexpr int NB = S::NB, LNB = S::LNB, PER = NB / T, I = (CAPM + T - 1) / T;
     static_assert(PER % 2 == 0 || PER == 1, "bucket split");
@@ -509,7 +512,8 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
             const uint32_t b = (cbits > 0 ? (kr[i] >> cbits) << cb : 0u) |
                                (((kr[i] & cmask) - cmin) >> sh);
             const int pos = cnt[b] + static_cast<int>(rr[i]);
-            pk[pos] = (((kr[i] & cmask) - cmin) & lm) << 16 | s.idx0[PADI(e)];
+            const uint32_t ix = kofs >= 0 ? static_cast<uint32_t>(e) : s.idx0[PADI(e)];
+            pk[pos] = (((kr[i] & cmask) - cmin) & lm) << 16 | ix;
             bk[pos] = static_cast<uint16_t>(b);
         }
     }
@@ -522,7 +526,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
         int c = lo;
         if (hi - lo > 1)
             for (int j = lo; j < hi; ++j) c += pk[j] < v;
-        const uint32_t col = cmin + (((b & bm) << sh) | (v >> 16));
+        const uint32_t col = cmin + (((b & bm) << sh) | (v >> 16)) - (kofs > 0 ? kofs : 0);
         s.key0[PADI(c)] = cbits > 0 ? ((b >> cb) << cbits) | col : col;
         s.idx0[PADI(c)] = static_cast<uint16_t>(v & 0xffffu);
     }
@@ -537,14 +541,29 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
 template <int T, int CAPM>
 __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width,
                                          int csort = 0, int cbits = 0,
-                                         bool radix_only = false) {
+                                         bool radix_only = false, int kofs = -1) {
     const int R = s.nruns;
     const int levels = R > 1 ? 32 - __clz(R - 1) : 0;
+    // kofs >= 0: the expansion deferred its fix-up (keys absolute, idx0 not
+    // set); the counting sort reads them as they are, the other sorts after
+    // this pass.
+    auto prep = [&] {
+        if (kofs < 0) return;
+        for (int e = threadIdx.x; e < total; e += T) {
+            s.key0[PADI(e)] -= static_cast<uint32_t>(kofs);
+            s.idx0[PADI(e)] = static_cast<uint16_t>(e);
+        }
+        __syncthreads();
+    };
     // MSD counting sort when the columns spread evenly over the buckets (cfg2:
     // 1.3x faster tiles); skewed / duplicate-heavy tiles fall through.
     // (measured: small tiles only; cfg4/cfg5's larger tiles are slower with it)
     if constexpr (CAPM <= 512)
-        if (levels >= 2 && msd_sort_tile<T, CAPM>(s, total, width)) return 1;
+        if (levels >= 2) {
+            prep();
+            kofs = -1;
+            if (msd_sort_tile<T, CAPM>(s, total, width)) return 1;
+        }
     // pad key = 2^bits - 1 >= every key (<= width-1); pads sit after `total`
     // and the sort is stable, so real entries keep the first `total` slots.
     const int bits = bit_length(width > 1 ? width - 1 : 1);
@@ -553,8 +572,9 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     // measured: cfg4 (5 levels vs 4 passes) prefers merge
     const bool radix = levels > passes + 1 || R > MergeShared<T, CAPM>::MAXRUNS;
     if (csort > 0 && levels >= 3 && (radix || !radix_only) &&
-        count_sort_tile<T, CAPM>(s, total, width, cbits, csort))
+        count_sort_tile<T, CAPM>(s, total, width, cbits, csort, kofs))
         return 0;
+    prep();
     if (radix) {
         radix_sort_tile<T, CAPM>(s, total, bits);
         return 0;

@@ -467,8 +467,9 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
         c1 = m.ncols;
     }
     const int total =
-        expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s, wsofs, wwi, wrs, wdn);
-    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(c1 - c0), csort);
+        expand_runs<T, CAPM, true>(m, row, c0, c1, wins == nullptr, s, wsofs, wwi, wrs, wdn,
+                                   /*defer=*/true);
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(c1 - c0), csort, 0, false, c0);
     (void)tid;
     int64_t base = out.crp[row - out.row_begin];
     if (w >= 0) base += out.win_scan[w] - out.win_scan[wins[w].first];
