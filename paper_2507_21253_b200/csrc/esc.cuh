@@ -14,7 +14,7 @@ constexpr int CAP = 4096;     // max products of one sparse tile (smem ESC)
 // tile that holds its products (CUB's block sort always sorts the full tile).
 // The 3072 class keeps 256 threads and is sized (≈73 KB smem, 85 registers)
 // for 3 CTAs/SM; a 192-thread 3072 tile (2 CTAs x 6 warps) measured slower.
-constexpr int NWCLS = 4;
+constexpr int NWCLS = 5;
 constexpr int WD = 4096;      // dense window width in columns
 constexpr int LOG_WD = 12;
 constexpr int MAXBINS = 4096; // planner histogram bins per heavy row

@@ -111,7 +111,7 @@ __global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64
 // K2: heavy-row planner
 // ---------------------------------------------------------------------------
 constexpr int PLAN_T = 256;
-__constant__ int kWinCapDev[NWCLS] = {4096, 3072, 2048, 512};
+__constant__ int kWinCapDev[NWCLS] = {4096, 3072, 2048, 1024, 512};
 constexpr int PLAN_U = 8;  // B-row chunks of 32 loaded ahead per warp
 constexpr uint32_t DENSE_BIT = 0x80000000u;
 
@@ -1032,11 +1032,12 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                 "planner: heavy rows need ncols <= 16M (MAXBINS*WD) in this build");
         DBuf<int32_t> nwin(h, nh + 1);
         BSP_CUDA(cudaMemsetAsync(nwin.p, 0, (nh + 1) * sizeof(int32_t), h->stream));
-        // window packing capacity (products; BSP_WTARGET to tune): the 3072
-        // tile runs 3 CTAs/SM
+        // window packing capacity (products; BSP_WTARGET to tune): windows of
+        // <= 2048 products run in the 2048 tile at 4 CTAs/SM (measured: cfg5
+        // 353 ms vs 360 ms at 3072, 370 ms at 1536, 390 ms at 1024)
         static const int32_t capg = [] {
             const char* e = std::getenv("BSP_WTARGET");
-            const int v = e ? std::atoi(e) : 3072;
+            const int v = e ? std::atoi(e) : 2048;
             return std::max(64, std::min(v, CAP));
         }();
         // window descriptors: per heavy row a slot sized by the window bound
@@ -1154,11 +1155,12 @@ void run_windows(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const Ou
     const Mats m = plan.with_starts(m0);
     auto wl = [&](int k) { return plan.sparse_ids.p + plan.wcls_off[k]; };
     auto wn = [&](int k) { return plan.wcls_off[k + 1] - plan.wcls_off[k]; };
-    static_assert(NWCLS == 4, "one launch per window tile class");
+    static_assert(NWCLS == 5, "one launch per window tile class");
     launch_tile<256, 4096, NUMERIC>(h, m, wl(0), wn(0), plan.wins.p, out);
     launch_tile<256, 3072, NUMERIC>(h, m, wl(1), wn(1), plan.wins.p, out);
     launch_tile<256, 2048, NUMERIC>(h, m, wl(2), wn(2), plan.wins.p, out);
-    launch_tile<64, 512, NUMERIC>(h, m, wl(3), wn(3), plan.wins.p, out);
+    launch_tile<128, 1024, NUMERIC>(h, m, wl(3), wn(3), plan.wins.p, out);
+    launch_tile<64, 512, NUMERIC>(h, m, wl(4), wn(4), plan.wins.p, out);
     launch_dense<NUMERIC>(h, m, plan.dense_ids.p, plan.ndense, plan.wins.p, out);
 }
 
