@@ -123,9 +123,9 @@ struct PlanCountShared {
 
 // Start tables of up to STAGE entries (uint32) are built in smem and stored
 // coalesced.
-constexpr int STAGE = 2 * MAXBINS;
+constexpr int STAGE = 6144;
 struct PlanWriteShared {
-    int32_t binwin[MAXBINS];  // bin -> window
+    uint16_t binwin[MAXBINS];  // bin -> window (a row has < 2^16 windows)
     union {
         struct {
             uint32_t wc0[MAXBINS + 1];  // window -> c0 | DENSE_BIT (+ sentinel ncols)
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
 // K2b: emit the Window records of each heavy row and its per-(window,
 // segment) start table: starts[sofs + w*d + p] = number of elements of
 // segment p lying in windows < w (one streaming pass over the row).
-__global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
+__global__ void __launch_bounds__(PLAN_T, 5) plan_write_kernel(
     Mats m, const int32_t* __restrict__ heavy, int32_t nbins, int log_binw,
     const int32_t* __restrict__ nwin, const int64_t* __restrict__ doff,
     const uint2* __restrict__ desc, const int64_t* __restrict__ win_off, Window* __restrict__ wins,
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(PLAN_T) plan_write_kernel(
             const int mid = (lo + hi + 1) >> 1;
             if ((s.u.w.wc0[mid] & ~DENSE_BIT) <= c) lo = mid; else hi = mid - 1;
         }
-        s.binwin[b] = lo;
+        s.binwin[b] = static_cast<uint16_t>(lo);
     }
     const int64_t off = win_off[hrow];
     // rows past the table budget binary-search their segments instead
