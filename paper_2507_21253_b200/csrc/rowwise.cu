@@ -116,8 +116,7 @@ constexpr int PLAN_U = 8;  // B-row chunks of 32 loaded ahead per warp
 constexpr uint32_t DENSE_BIT = 0x80000000u;
 
 struct PlanCountShared {
-    int32_t hist[MAXBINS];
-    int32_t pre[MAXBINS + 1];  // inclusive-exclusive prefix: pre[b] = products in bins < b
+    int32_t hist[MAXBINS + 1];  // per-bin products, then (in place) pre[b] = products in bins < b
     typename cub::BlockScan<int32_t, PLAN_T>::TempStorage scan;
 };
 
@@ -181,7 +180,7 @@ __device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& 
 // K2a: per heavy row, a product histogram over `nbins` column bins, then the
 // greedy window cut (below).  Writes the window count and the descriptors
 // {c0 | DENSE_BIT, product prefix} (+ sentinel {ncols, P}) at desc[doff[h]].
-__global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
+__global__ void __launch_bounds__(PLAN_T, 8) plan_count_kernel(Mats m,
                                                             const int32_t* __restrict__ heavy,
                                                             int32_t nbins, int log_binw,
                                                             int32_t* __restrict__ nwin,
@@ -233,14 +232,15 @@ __global__ void __launch_bounds__(PLAN_T) plan_count_kernel(Mats m,
 #pragma unroll
         for (int j = 0; j < PB; ++j) {
             const int b = threadIdx.x * PB + j;
-            if (b <= nbins) s.pre[b] = base;
+            if (b <= nbins) s.hist[b] = base;  // every thread read its bins before the scan
             base += loc[j];
         }
+        if (threadIdx.x == PLAN_T - 1 && nbins == PB * PLAN_T) s.hist[nbins] = base;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         uint2* dd = desc + doff[hrow];
-        const int32_t* pre = s.pre;
+        const int32_t* pre = s.hist;
         int32_t nw = 0;
         int b = 0;
         while (b < nbins) {
