@@ -1013,7 +1013,12 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     // The light rows' symbolic does not depend on the heavy-row plan: run it
     // on the side stream while the (latency-bound) planner runs here;
     // plan_symbolic joins it.
-    if (early_row_nnz && tot_listed > plan.class_count[NCLS - 1]) {
+    // BSP_SIDE=0: count the light rows on the main stream (no overlap)
+    static const bool side_ok = [] {
+        const char* e = std::getenv("BSP_SIDE");
+        return !(e && e[0] == '0');
+    }();
+    if (side_ok && early_row_nnz && tot_listed > plan.class_count[NCLS - 1]) {
         SideStream side(h);
         OutCtx out{};
         out.row_begin = plan.rb;
