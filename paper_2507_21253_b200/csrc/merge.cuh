@@ -63,10 +63,11 @@ struct MergeShared {
             uint16_t ro1[MAXRUNS + 2];
         } m;
         typename RSort::TempStorage sort;
-        struct CS {
-            uint32_t packed[CAPM];     // (low column bits << 16 | index), by bucket
+        struct alignas(16) CS {
+            uint32_t packed[CAPM + 4]; // per bucketed slot: (column - min) << IB | index,
+                                       // or (low column bits << 16 | index) + bucket[]
             uint32_t cnt[NB / 2 + 1];  // 16-bit bucket counts, then bucket starts
-            uint16_t bucket[CAPM];     // bucket of each bucketed slot
+            uint16_t bucket[CAPM];     // bucket of each bucketed slot (wide tiles)
         } c;
         Ex x;
     } u;
@@ -505,6 +506,43 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
     if (tid == 0) cnt[NB] = static_cast<uint16_t>(total);
     __syncthreads();
     const uint32_t lm = (1u << sh) - 1u;
+    // Narrow row tiles: the whole (column - min, index) fits one 32-bit word,
+    // globally ordered and unique, so a slot's rank is the count of smaller
+    // words from its bucket start rounded down to 4 (lower buckets hold only
+    // smaller words, higher ones and the pad only larger) — 4 per 16-byte load,
+    // no bucket array, no tie path.
+    constexpr int IB = 32 - __builtin_clz(static_cast<unsigned>(CAPM - 1));
+    if (cbits == 0 && cw + IB <= 32) {
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+            const int e = i * T + tid;
+            if (e < total) {
+                const uint32_t rel = kr[i] - cmin;
+                const uint32_t ix = kofs >= 0 ? static_cast<uint32_t>(e) : s.idx0[PADI(e)];
+                pk[cnt[rel >> sh] + static_cast<int>(rr[i])] = (rel << IB) | ix;
+            }
+        }
+        if (tid < 4) pk[total + tid] = 0xffffffffu;
+        __syncthreads();
+        const uint32_t im = (1u << IB) - 1u;
+        for (int q = tid; q < total; q += T) {
+            const uint32_t v = pk[q];
+            const uint32_t b = (v >> IB) >> sh;
+            const int lo = cnt[b], hi = cnt[b + 1];
+            int c = lo;
+            if (hi - lo > 1) {
+                c = lo & ~3;
+                for (int j = c; j < hi; j += 4) {
+                    const uint4 w = *reinterpret_cast<const uint4*>(pk + j);
+                    c += (w.x < v) + (w.y < v) + (w.z < v) + (w.w < v);
+                }
+            }
+            s.key0[PADI(c)] = (v >> IB) + cmin - static_cast<uint32_t>(kofs > 0 ? kofs : 0);
+            s.idx0[PADI(c)] = static_cast<uint16_t>(v & im);
+        }
+        __syncthreads();
+        return true;
+    }
 #pragma unroll
     for (int i = 0; i < I; ++i) {
         const int e = i * T + tid;
