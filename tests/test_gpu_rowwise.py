@@ -205,3 +205,38 @@ def test_narrow_b_matches_oracle(engine, ncols):
     got = engine.spgemm_rowwise(A, Bd).download()
     assert_csr_identical(got, O.spgemm_rowwise(a, b), f"narrow {ncols}")
     assert engine.exec_stats()["products"] == int(np.diff(b.row_ptr)[a.col_idx].sum())
+
+
+def test_counting_sort_wide_and_duplicate_tiles(engine):
+    """The tile sort's paths at a 2^22 + 123-column B (cfg5's width): light
+    rows whose columns span all 22 bits (counting sort with a bucket array),
+    windows of heavy rows (packed-word counting sort), and rows whose products
+    pile >128 copies of a few columns into one bucket (fallback to the merge /
+    radix sorts after the deferred fix-up).  Ties must still sum in k order."""
+    rng = np.random.default_rng(2025)
+    ncols = (1 << 22) + 123
+    nb = 700
+    rows_b = []
+    for k in range(nb):
+        if k < 64:  # duplicate group: every row shares columns 100..110
+            cols = np.arange(100, 111)
+        else:
+            cols = rng.choice(ncols, size=int(rng.integers(4, 48)), replace=False)
+        rows_b.append(np.unique(cols))
+    rb = np.concatenate([[k] * len(c) for k, c in enumerate(rows_b)])
+    cb = np.concatenate(rows_b)
+    b = B.coo_to_csr(nb, ncols, rb, cb, rng.uniform(-4.0, 4.0, size=cb.size))
+    ra, ca = [], []
+    for i, d in enumerate([3, 20, 40, 70, 110, 150, 400, 690]):  # light .. heavy rows
+        ks = rng.choice(np.arange(64, nb), size=min(d, nb - 64), replace=False)
+        ra += [i] * len(ks)
+        ca += list(ks)
+    for i in range(8, 12):  # duplicate-heavy rows: 64 x 11 products on 11 columns
+        ks = np.concatenate([np.arange(64), rng.choice(np.arange(64, nb), 30, replace=False)])
+        ra += [i] * len(ks)
+        ca += list(ks)
+    a = B.coo_to_csr(12, nb, np.array(ra), np.array(ca), rng.uniform(-4.0, 4.0, size=len(ra)))
+    c = gpu_mul(engine, a, b)
+    o = O.spgemm_rowwise(a, b)
+    assert_csr_identical(c, o, "wide / duplicate tiles")
+    assert engine.exec_stats()["units"][7] > 0, "no heavy rows"
