@@ -288,6 +288,12 @@ def main():
     ms_per_step = total_ms / args.steps
     value = 2.0 * total_products / (ms_per_step * 1e-3) / 1e9
 
+    # ---- e2e: host-buffer pipeline through the public API (all ranks) ----
+    e2e = None
+    if not args.no_e2e:
+        host = [t_.cpu().numpy() for t_ in (rp_t, ci_t, v_t)]
+        e2e = run_e2e(B, eng, host, n, ncols, args, total_products, rank, world, dist)
+
     if rank != 0:
         if dist:
             dist.barrier()
@@ -330,9 +336,8 @@ def main():
         "clocks": clk.summary(),
     }
 
-    # ---- e2e: host-buffer pipeline through the public API ----------------
-    if not args.no_e2e and world == 1:
-        line["e2e"] = run_e2e(B, eng, a, args, total_products)
+    if e2e is not None:
+        line["e2e"] = e2e
     # ---- cpu baseline (rank 0, N=1) --------------------------------------
     if not args.no_cpu and world == 1:
         import oracle as O
@@ -441,23 +446,27 @@ def run_tall_skinny(B, args, num_frontiers=10, batch=64, seed=0):
     print(json.dumps(line))
 
 
-def run_e2e(B, eng, a, args, total_products):
+def run_e2e(B, eng, host, n, ncols, args, total_products, rank=0, world=1, dist=None):
     """Reference-shaped call with HOST buffers: pinned A -> device (H2D), the
     multiply in row chunks, each chunk of C copied back (D2H) into a pinned
     host ring by a second engine handle whose stream waits on the compute
-    stream, so the copy engine overlaps the next chunk's kernels."""
+    stream, so the copy engine overlaps the next chunk's kernels.  With N
+    ranks each rank copies A in, multiplies its row shard (the chunks of the
+    same cost split, so shard bounds coincide with bench's) and copies its
+    shard of C out; the step time is the max over ranks."""
     import torch
 
     nchunks = args.e2e_chunks
-    hp = [torch.from_numpy(x).pin_memory() for x in (a.row_ptr, a.col_idx, a.values)]
+    hp = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in host]
     h2d = sum(x.numel() * x.element_size() for x in hp)
     ce = B.Engine(eng.device)  # copy handle (own stream)
     cstream = torch.cuda.ExternalStream(ce.stream_ptr())
     # size the pinned ring from one untimed pass
     dev = [x.cuda() for x in hp]
     torch.cuda.synchronize()
-    A = eng.view_torch(a.nrows, a.ncols, *dev)
-    bounds = eng.partition_rows(A, A, nchunks)
+    A = eng.view_torch(n, ncols, *dev)
+    allb = eng.partition_rows(A, A, nchunks * world)
+    bounds = allb[rank * nchunks:(rank + 1) * nchunks + 1]
     sizes = []
     for g in range(nchunks):
         C = eng.spgemm_rowwise_range(A, A, int(bounds[g]), int(bounds[g + 1]))
@@ -475,10 +484,12 @@ def run_e2e(B, eng, a, args, total_products):
     mstream = torch.cuda.ExternalStream(eng.stream_ptr())
     for s in range(1 + steps):
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
         with torch.cuda.stream(mstream):
             dev = [x.cuda(non_blocking=True) for x in hp]
-        A = eng.view_torch(a.nrows, a.ncols, *dev)
+        A = eng.view_torch(n, ncols, *dev)
         slot_ev = [None, None]
         d2h = 0
         for g in range(nchunks):
@@ -497,16 +508,22 @@ def run_e2e(B, eng, a, args, total_products):
         ce.synchronize()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt, float(d2h)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+            dt, d2h = float(t[0]), int(t[1])
         if s > 0:
             times.append(dt)
         del dev, A
     ce.close()
     t = statistics.median(times)
     return {"value": 2.0 * total_products / t / 1e9, "unit": "GFLOP/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t,
-            "chunks": nchunks,
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t,
+            "chunks": nchunks * world,
             "path": "pinned H2D of A + bsp_spgemm_rowwise_range per row chunk + "
-                    "bsp_csr_download_async of every chunk of C into a pinned host ring"}
+                    "bsp_csr_download_async of every chunk of C into a pinned host ring"
+                    + (f" (per rank, {world} ranks, max over ranks)" if world > 1 else "")}
 
 
 if __name__ == "__main__":
