@@ -45,43 +45,51 @@ namespace {
 // ---------------------------------------------------------------------------
 // K0: products and class per row
 // ---------------------------------------------------------------------------
+// A warp per row (grid-stride over rows): the lanes read the row's A entries
+// coalesced and sum the B row lengths, so a hub row (~10^4 entries) is not a
+// single thread's serial loop.
 __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restrict__ prod,
                                 uint8_t* __restrict__ cls, const uint8_t* __restrict__ skip,
                                 int64_t* __restrict__ class_count,
                                 int64_t* __restrict__ class_products) {
-    __shared__ int64_t s_cnt[NCLS], s_prod[NCLS];
+    __shared__ unsigned long long s_cnt[NCLS], s_prod[NCLS];
     if (threadIdx.x < NCLS) {
         s_cnt[threadIdx.x] = 0;
         s_prod[threadIdx.x] = 0;
     }
     __syncthreads();
-    for (int64_t r = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; r < n;
-         r += int64_t{gridDim.x} * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = int64_t{gridDim.x} * (blockDim.x >> 5);
+    for (int64_t r = blockIdx.x * int64_t{blockDim.x >> 5} + (threadIdx.x >> 5); r < n;
+         r += nwarps) {
         const int64_t i = rb + r;
+        const int64_t p0 = m.arp[i], p1 = m.arp[i + 1];
         int64_t P = 0;
-        for (int64_t p = m.arp[i]; p < m.arp[i + 1]; ++p) {
+        for (int64_t p = p0 + lane; p < p1; p += 32) {
             const int32_t k = __ldg(m.acol + p);
             P += __ldg(m.brp + k + 1) - __ldg(m.brp + k);
         }
-        int c = 0;
-        if (skip && skip[r]) {
-            c = 0;
-        } else if (P > 0) {
-            c = 1;
-            while (c < NCLS - 1 && P > kClassCap[c]) ++c;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) P += __shfl_xor_sync(0xffffffffu, P, o);
+        if (lane == 0) {
+            int c = 0;
+            if (skip && skip[r]) {
+                c = 0;
+            } else if (P > 0) {
+                c = 1;
+                while (c < NCLS - 1 && P > kClassCap[c]) ++c;
+            }
+            if (prod) prod[r] = P;
+            cls[r] = static_cast<uint8_t>(c);
+            atomicAdd(&s_cnt[c], 1ull);
+            atomicAdd(&s_prod[c], static_cast<unsigned long long>(P));
         }
-        if (prod) prod[r] = P;
-        cls[r] = static_cast<uint8_t>(c);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[c]), 1ull);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&s_prod[c]),
-                  static_cast<unsigned long long>(P));
     }
     __syncthreads();
     if (threadIdx.x < NCLS) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&class_count[threadIdx.x]),
-                  static_cast<unsigned long long>(s_cnt[threadIdx.x]));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&class_count[threadIdx.x]), s_cnt[threadIdx.x]);
         atomicAdd(reinterpret_cast<unsigned long long*>(&class_products[threadIdx.x]),
-                  static_cast<unsigned long long>(s_prod[threadIdx.x]));
+                  s_prod[threadIdx.x]);
     }
 }
 
@@ -984,7 +992,7 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     DBuf<uint8_t> cls(h, n);
     DBuf<int64_t> counters(h, 2 * NCLS);
     BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * NCLS * sizeof(int64_t), h->stream));
-    const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 256),
+    const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 8),
                                                         int64_t{h->sm_count} * 8));
     BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, rb, n, prod_out, cls.p, skip, counters.p,
                counters.p + NCLS);
@@ -1311,7 +1319,7 @@ int bsp_spgemm_products(bsp_handle h, const bsp_csr* A, const bsp_csr* B,
         DBuf<int64_t> counters(h, 2 * NCLS);
         BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * NCLS * sizeof(int64_t), h->stream));
         const int grid = static_cast<int>(std::min<int64_t>(
-            div_up(std::max<int64_t>(n, 1), 256), int64_t{h->sm_count} * 8));
+            div_up(std::max<int64_t>(n, 1), 8), int64_t{h->sm_count} * 8));
         BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, 0, n, prod, cls.p, nullptr, counters.p,
                    counters.p + NCLS);
         int64_t hc[2 * NCLS];
