@@ -854,8 +854,11 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32)
                 len = static_cast<int>(__ldg(m.brp + k + 1) - b0);
                 if (NUMERIC) a = __ldg(m.aval + p);
             }
-            const int nseg = static_cast<int>(::min(int64_t{32}, re - pb));
-            for (int j = 0; j < nseg; ++j) {
+            // non-empty segments only, in k order (frontier rows are mostly empty)
+            unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+            while (ne) {
+                const int j = __ffs(ne) - 1;
+                ne &= ne - 1;
                 const int64_t sj = __shfl_sync(0xffffffffu, b0, j);
                 const int lj = __shfl_sync(0xffffffffu, len, j);
                 const double aj = __shfl_sync(0xffffffffu, a, j);
@@ -1214,8 +1217,98 @@ void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const in
 }
 
 // Narrow B: symbolic (+ products) -> int64 scan -> numeric, no planning.
+// B with <= 64 columns (the tall-skinny frontier operands): each B row as a
+// 64-bit column mask, built once per multiply.
+__global__ void row_mask64_kernel(const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol,
+                                  int64_t nb, unsigned long long* __restrict__ mask) {
+    for (int64_t k = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; k < nb;
+         k += int64_t{gridDim.x} * blockDim.x) {
+        unsigned long long mk = 0;
+        for (int64_t q = brp[k]; q < brp[k + 1]; ++q) mk |= 1ull << __ldg(bcol + q);
+        mask[k] = mk;
+    }
+}
+
+// A warp per row; lane l owns output columns l and l + 32 and keeps their sums
+// in registers.  The row's non-empty segments are walked in k order, each
+// broadcast (B offset, column mask, a_ik) once: a lane whose column is in the
+// mask adds a_ik * b_kj, b_kj found at the popcount of the mask below its bit
+// — ascending k per column, so the sums are the reference's.  Symbolic: the
+// popcount of the OR of the masks.
+template <bool NUMERIC>
+__global__ void __launch_bounds__(NARROW_WARPS * 32)
+    narrow64_kernel(Mats m, const unsigned long long* __restrict__ bmask, int64_t rb, int64_t n,
+                    int64_t* __restrict__ row_nnz, const int64_t* __restrict__ crp,
+                    int32_t* __restrict__ ccol, double* __restrict__ cval,
+                    unsigned long long* __restrict__ products) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned long long below0 = (1ull << lane) - 1ull, below1 = (1ull << (lane + 32)) - 1ull;
+    unsigned long long prod = 0;
+    for (int64_t r = blockIdx.x * int64_t{NARROW_WARPS} + warp; r < n;
+         r += int64_t{gridDim.x} * NARROW_WARPS) {
+        const int64_t row = rb + r;
+        const int64_t rs = m.arp[row], re = m.arp[row + 1];
+        unsigned long long touch = 0;
+        double acc0 = 0.0, acc1 = 0.0;
+        for (int64_t pb = rs; pb < re; pb += 32) {
+            const int64_t p = pb + lane;
+            unsigned long long mk = 0;
+            int64_t b0 = 0;
+            double a = 0.0;
+            if (p < re) {
+                const int32_t k = __ldg(m.acol + p);
+                mk = __ldg(bmask + k);
+                if (NUMERIC) {
+                    b0 = __ldg(m.brp + k);
+                    a = __ldg(m.aval + p);
+                } else {
+                    prod += static_cast<unsigned long long>(__popcll(mk));
+                }
+            }
+            touch |= mk;
+            if (NUMERIC) {
+                unsigned ne = __ballot_sync(0xffffffffu, mk != 0);
+                while (ne) {
+                    const int j = __ffs(ne) - 1;
+                    ne &= ne - 1;
+                    const unsigned long long mj = __shfl_sync(0xffffffffu, mk, j);
+                    const int64_t bj = __shfl_sync(0xffffffffu, b0, j);
+                    const double aj = __shfl_sync(0xffffffffu, a, j);
+                    if ((mj >> lane) & 1ull)
+                        acc0 = __dadd_rn(acc0, __dmul_rn(aj, __ldg(m.bval + bj + __popcll(mj & below0))));
+                    if ((mj >> (lane + 32)) & 1ull)
+                        acc1 = __dadd_rn(acc1, __dmul_rn(aj, __ldg(m.bval + bj + __popcll(mj & below1))));
+                }
+            }
+        }
+        // OR of the lanes' masks
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) touch |= __shfl_xor_sync(0xffffffffu, touch, o);
+        if (!NUMERIC) {
+            if (lane == 0) row_nnz[r] = __popcll(touch);
+        } else {
+            const int64_t pos = crp[r];
+            if ((touch >> lane) & 1ull) {
+                const int64_t o = pos + __popcll(touch & below0);
+                ccol[o] = lane;
+                cval[o] = acc0;
+            }
+            if ((touch >> (lane + 32)) & 1ull) {
+                const int64_t o = pos + __popcll(touch & below1);
+                ccol[o] = lane + 32;
+                cval[o] = acc1;
+            }
+        }
+    }
+    if (!NUMERIC) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+        if (lane == 0 && prod) atomicAdd(products, prod);
+    }
+}
+
 static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, int64_t ncols,
-                            bsp_csr* C, int64_t* row_nnz_out) {
+                            int64_t bnrows, bsp_csr* C, int64_t* row_nnz_out) {
     DBuf<int64_t> cnt(h, n + 1);
     BSP_CUDA(cudaMemsetAsync(cnt.p, 0, (n + 1) * sizeof(int64_t), h->stream));
     DBuf<unsigned long long> prod(h, 1);
@@ -1226,8 +1319,20 @@ static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, 
     const int32_t nc = static_cast<int32_t>(ncols);
     auto ks = narrow_kernel<false>;
     auto kn = narrow_kernel<true>;
-    BSP_LAUNCH_AS(h, "narrow_symbolic", ks, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, cnt.p,
-                  nullptr, nullptr, nullptr, prod.p);
+    // <= 64 columns: B rows as 64-bit masks, sums in registers
+    const bool m64 = ncols <= 64;
+    DBuf<unsigned long long> bmask;
+    if (m64) {
+        bmask = DBuf<unsigned long long>(h, std::max<int64_t>(bnrows, 1));
+        const unsigned gm = static_cast<unsigned>(std::max<int64_t>(
+            1, std::min<int64_t>(div_up(std::max<int64_t>(bnrows, 1), 256), int64_t{h->sm_count} * 8)));
+        BSP_LAUNCH(h, row_mask64_kernel, gm, 256, 0, m.brp, m.bcol, bnrows, bmask.p);
+        BSP_LAUNCH_AS(h, "narrow64_symbolic", narrow64_kernel<false>, grid, NARROW_WARPS * 32, 0, m,
+                      bmask.p, rb, n, cnt.p, nullptr, nullptr, nullptr, prod.p);
+    } else {
+        BSP_LAUNCH_AS(h, "narrow_symbolic", ks, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, cnt.p,
+                      nullptr, nullptr, nullptr, prod.p);
+    }
     if (row_nnz_out)
         BSP_CUDA(cudaMemcpyAsync(row_nnz_out, cnt.p, n * sizeof(int64_t), cudaMemcpyDeviceToDevice,
                                  h->stream));
@@ -1237,8 +1342,12 @@ static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, 
     h->stats.products = static_cast<int64_t>(read_scalar(h, prod.p));
     h->stats.nnz_out = nnz;
     ResultPayload pay(h, nnz);
-    BSP_LAUNCH_AS(h, "narrow_numeric", kn, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, nullptr,
-                  rp.p, pay.col_idx(), pay.values(), nullptr);
+    if (m64)
+        BSP_LAUNCH_AS(h, "narrow64_numeric", narrow64_kernel<true>, grid, NARROW_WARPS * 32, 0, m,
+                      bmask.p, rb, n, nullptr, rp.p, pay.col_idx(), pay.values(), nullptr);
+    else
+        BSP_LAUNCH_AS(h, "narrow_numeric", kn, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, nullptr,
+                      rp.p, pay.col_idx(), pay.values(), nullptr);
     C->nrows = n;
     C->ncols = ncols;
     C->nnz = nnz;
@@ -1262,7 +1371,7 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     // BSP_NARROW=0 forces the tile path (read per call, so tests can cover both)
     const char* ne = std::getenv("BSP_NARROW");
     if (B->ncols <= NARROW && row_skip == nullptr && !(ne && ne[0] == '0')) {
-        narrow_multiply(h, m, rb, n, B->ncols, C, row_nnz_out);
+        narrow_multiply(h, m, rb, n, B->ncols, B->nrows, C, row_nnz_out);
         return;
     }
     DBuf<int64_t> crp(h, n + 1);

@@ -184,9 +184,10 @@ def test_heavy_rows_over_empty_b_rows(engine):
                          "dense windows over empty B rows")
 
 
-@pytest.mark.parametrize("ncols", [1, 31, 64, 200, 256, 257])
+@pytest.mark.parametrize("ncols", [1, 31, 33, 63, 64, 65, 200, 256, 257])
 def test_narrow_b_matches_oracle(engine, ncols):
-    """Narrow B (<= 256 columns: one warp per row, dense accumulator) against
+    """Narrow B (<= 64 columns: 64-bit row masks, sums in registers; <= 256:
+    one warp per row, dense accumulator) against
     the oracle, with heavy rows, hub B rows, empty rows and empty B rows;
     257 columns takes the tile path."""
     rng = np.random.default_rng(ncols)
