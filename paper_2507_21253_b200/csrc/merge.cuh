@@ -400,22 +400,25 @@ __device__ __forceinline__ bool msd_sort_tile(MergeShared<T, CAPM>& s, int total
 
 // Counting sort for tiles whose columns are nearly distinct (cf ~ 1): one
 // smem-atomic pass buckets the products on the top bits of the column
-// relative to the tile's own [min, max] column range (NB buckets, ~1.5
-// products each; 16-bit counters packed two per word), a scan lays the
-// buckets out, and each bucketed slot's final position is its bucket start
-// plus the number of bucket members with a smaller (column, expansion index)
-// — the index tie-break puts equal columns in ascending k, so the run sums
-// stay exact (spgemm.hpp:92-97).  The ranking runs over the bucketed slots, so
-// the lanes of a warp mostly share one bucket and the loop trip count (the
-// bucket size) does not diverge.
+// relative to the tile's own [min, max] column range (NB buckets, about one
+// product each; 16-bit counters packed two per word), a scan lays the buckets
+// out, and each bucketed slot's final position is its bucket start plus the
+// number of bucket members with a smaller (column, expansion index) — the
+// index tie-break puts equal columns in ascending k, so the run sums stay
+// exact (spgemm.hpp:92-97).  The ranking runs over the bucketed slots, so the
+// lanes of a warp mostly share one bucket and the loop trip count (the bucket
+// size) does not diverge.  Narrow tiles (column range + index bits <= 32)
+// rank one packed word per slot with 4-wide vector compares; wide ones keep
+// (low column bits, index) words plus a bucket id per slot.
 // Composite keys (cbits > 0: key = member << cbits | column, the cluster
 // tiles) give each of the 2^lk member slots NB / 2^lk buckets over the
 // columns' range, so the order stays member-major.
 // The ranking costs sum(bucket size^2) compares (= sum over products of
 // 2 x rank-in-bucket + 1, known after the bucketing pass).  Tiles where that
-// exceeds `cost` x products (clustered or duplicate-heavy columns), whose
-// bucket width exceeds 2^16 columns, or with a bucket of more than CS_MAXB
-// products return false with buffer 0 untouched (merge / radix instead).
+// exceeds `max_cost` x products, whose bucket width exceeds 2^16 columns, or
+// with a bucket of more than CS_MAXB products (duplicate-heavy columns)
+// return false with buffer 0 untouched (merge / radix instead).
+// kofs >= 0: the expansion deferred its fix-up (absolute columns, idx0 unset).
 // Result in buffer 0.
 constexpr int CS_MAXB = 128;
 
