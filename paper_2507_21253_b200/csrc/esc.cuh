@@ -176,6 +176,7 @@ struct RowwisePlan {
     int64_t class_count[NCLS]{}, class_products[NCLS]{};
     int64_t class_off[NCLS + 1]{};
     DBuf<int32_t> lists;  // all non-empty rows grouped by class
+    DBuf<int64_t> prod;   // intermediate products per row (relative to rb)
     int64_t nwin = 0, nsparse = 0, ndense = 0;
     // sparse_ids[wcls_off[k], wcls_off[k+1]): windows of tile class k (kWinCap)
     int64_t wcls_off[NWCLS + 1]{};

@@ -987,10 +987,9 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     const int64_t n = re - rb;
     plan.rb = rb;
     plan.n = n;
-    DBuf<int64_t> prod_tmp;
     if (!prod_out) {
-        prod_tmp = DBuf<int64_t>(h, n);
-        prod_out = prod_tmp.p;
+        plan.prod = DBuf<int64_t>(h, n);
+        prod_out = plan.prod.p;
     }
     DBuf<uint8_t> cls(h, n);
     DBuf<int64_t> counters(h, 2 * NCLS);
@@ -1205,6 +1204,140 @@ void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t
     }
 }
 
+// ---------------------------------------------------------------------------
+// Duplicate-heavy light rows (products >= 2 x outputs, <= HACC_MAX outputs;
+// cfg4's stencil rows: 729 products -> 125 columns): a warp per row
+// accumulates into a per-warp smem hash (column -> running sum), one segment
+// at a time in k order — a segment's columns are distinct, so its lanes never
+// collide, and every column's sum is ((0.0 + p1) + p2) + ... in ascending k as
+// the reference forms it — then sorts only the row's distinct columns (rank by
+// counting against the compacted keys, read as warp broadcasts).
+// ---------------------------------------------------------------------------
+constexpr int HACC_WARPS = 8, HACC_HS = 512, HACC_MAX = 256;
+struct HaccShared {
+    int32_t key[HACC_WARPS][HACC_HS];
+    double val[HACC_WARPS][HACC_HS];
+};
+
+__global__ void __launch_bounds__(HACC_WARPS * 32)
+    hashacc_kernel(Mats m, const int32_t* __restrict__ rows, int64_t nrows, int64_t rb,
+                   const int64_t* __restrict__ crp, int32_t* __restrict__ ccol,
+                   double* __restrict__ cval) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HaccShared& s = *reinterpret_cast<HaccShared*>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t* keys = s.key[warp];
+    double* vals = s.val[warp];
+    constexpr int LG = 31 - __builtin_clz(static_cast<unsigned>(HACC_HS));
+    constexpr int PER = HACC_MAX / 32;
+    for (int64_t t = blockIdx.x * int64_t{HACC_WARPS} + warp; t < nrows;
+         t += int64_t{gridDim.x} * HACC_WARPS) {
+        const int32_t row = rows[t];
+        for (int i = lane; i < HACC_HS; i += 32) keys[i] = -1;
+        __syncwarp();
+        const int64_t rs = m.arp[row], re = m.arp[row + 1];
+        for (int64_t pb = rs; pb < re; pb += 32) {
+            const int64_t p = pb + lane;
+            int64_t b0 = 0;
+            int len = 0;
+            double a = 0.0;
+            if (p < re) {
+                const int32_t k = __ldg(m.acol + p);
+                b0 = __ldg(m.brp + k);
+                len = static_cast<int>(__ldg(m.brp + k + 1) - b0);
+                a = __ldg(m.aval + p);
+            }
+            unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+            while (ne) {
+                const int j = __ffs(ne) - 1;
+                ne &= ne - 1;
+                const int64_t bj = __shfl_sync(0xffffffffu, b0, j);
+                const int lj = __shfl_sync(0xffffffffu, len, j);
+                const double aj = __shfl_sync(0xffffffffu, a, j);
+                for (int q = lane; q < lj; q += 32) {
+                    const int32_t col = __ldg(m.bcol + bj + q);
+                    const double v = __dmul_rn(aj, __ldg(m.bval + bj + q));
+                    uint32_t slot = col_hash(static_cast<uint32_t>(col), LG);
+                    for (;;) {
+                        const int32_t prev = atomicCAS(&keys[slot], -1, col);
+                        if (prev == -1) {
+                            vals[slot] = __dadd_rn(0.0, v);
+                            break;
+                        }
+                        if (prev == col) {
+                            vals[slot] = __dadd_rn(vals[slot], v);
+                            break;
+                        }
+                        slot = (slot + 1) & (HACC_HS - 1);
+                    }
+                }
+                __syncwarp();  // the next segment adds after this one
+            }
+        }
+        // compact the occupied slots to the front (ascending slot order; a
+        // block's slots are read before any position inside it is written)
+        int nnz = 0;
+        for (int i0 = 0; i0 < HACC_HS; i0 += 32) {
+            const int32_t kk = keys[i0 + lane];
+            const double vv = vals[i0 + lane];
+            const unsigned occ = __ballot_sync(0xffffffffu, kk >= 0);
+            __syncwarp();
+            if (kk >= 0) {
+                const int pos = nnz + __popc(occ & ((1u << lane) - 1u));
+                keys[pos] = kk;
+                vals[pos] = vv;
+            }
+            nnz += __popc(occ);
+            __syncwarp();
+        }
+        // rank each distinct column among the row's columns
+        int32_t mk[PER];
+        double mv[PER];
+        int rk[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = u * 32 + lane;
+            mk[u] = i < nnz ? keys[i] : 0x7fffffff;
+            mv[u] = i < nnz ? vals[i] : 0.0;
+            rk[u] = 0;
+        }
+        for (int jj = 0; jj < nnz; ++jj) {
+            const int32_t kj = keys[jj];
+#pragma unroll
+            for (int u = 0; u < PER; ++u) rk[u] += kj < mk[u];
+        }
+        const int64_t base = crp[row - rb];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            if (u * 32 + lane < nnz) {
+                ccol[base + rk[u]] = mk[u];
+                cval[base + rk[u]] = mv[u];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Split the light rows: duplicate-heavy ones (products >= 2 x outputs, <=
+// HACC_MAX outputs) to hlist, the rest back into per-class lists.
+__global__ void route_light_kernel(const int32_t* __restrict__ lists, int64_t nlight, int64_t rb,
+                                   const int64_t* __restrict__ prod, const int64_t* __restrict__ crp,
+                                   unsigned long long* __restrict__ cursor,
+                                   int32_t* __restrict__ hlist, int32_t* __restrict__ tlists) {
+    const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (t >= nlight) return;
+    const int32_t row = lists[t];
+    const int64_t r = row - rb;
+    const int64_t P = prod[r], nz = crp[r + 1] - crp[r];
+    if (P >= 2 * nz && nz <= HACC_MAX) {
+        hlist[atomicAdd(&cursor[0], 1ull)] = row;
+    } else {
+        int c = 1;
+        while (c < NCLS - 1 && P > kClassCap[c]) ++c;
+        tlists[atomicAdd(&cursor[c], 1ull)] = row;
+    }
+}
+
 void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
                   const int64_t* win_scan, int32_t* ccol, double* cval) {
     OutCtx out{};
@@ -1213,7 +1346,48 @@ void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const in
     out.win_scan = win_scan;
     out.ccol = ccol;
     out.cval = cval;
-    run_plan<true>(h, m, plan, out);
+    // BSP_HACC=0: duplicate-heavy light rows stay on the sort tiles
+    static const bool hacc = [] {
+        const char* e = std::getenv("BSP_HACC");
+        return !(e && e[0] == '0');
+    }();
+    const int64_t nlight = plan.class_off[NCLS - 1] - plan.class_off[1];
+    // route only when columns repeat overall (compression factor >= 1.25:
+    // cfg3 2.95, cfg4 5.84; not cfg2/cfg5 ~1.0, which would only pay the
+    // routing pass and its readback)
+    int64_t planned = 0;
+    for (int c = 1; c < NCLS; ++c) planned += plan.class_products[c];
+    const bool repeats = 4 * planned >= 5 * std::max<int64_t>(1, h->stats.nnz_out);
+    if (!hacc || !repeats || nlight <= 0 || plan.prod.p == nullptr) {
+        run_plan<true>(h, m, plan, out);
+        return;
+    }
+    DBuf<int32_t> hlist(h, nlight), tl(h, nlight);
+    DBuf<unsigned long long> cursor(h, NCLS);
+    unsigned long long cur[NCLS];
+    cur[0] = 0;
+    for (int c = 1; c < NCLS; ++c)
+        cur[c] = static_cast<unsigned long long>(plan.class_off[c] - plan.class_off[1]);
+    h2d(h, cursor.p, cur, NCLS);
+    BSP_LAUNCH(h, route_light_kernel, static_cast<unsigned>(div_up(nlight, 256)), 256, 0,
+               plan.lists.p + plan.class_off[1], nlight, plan.rb, plan.prod.p, crp, cursor.p,
+               hlist.p, tl.p);
+    unsigned long long hc[NCLS];
+    d2h(h, hc, cursor.p, NCLS);
+    const int64_t nh = static_cast<int64_t>(hc[0]);
+    if (nh > 0) {
+        set_smem(hashacc_kernel, sizeof(HaccShared));
+        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+            1, std::min<int64_t>(div_up(nh, HACC_WARPS), int64_t{h->sm_count} * 16)));
+        BSP_LAUNCH(h, hashacc_kernel, grid, HACC_WARPS * 32, sizeof(HaccShared), m, hlist.p, nh,
+                   plan.rb, crp, ccol, cval);
+    }
+    for (int c = NCLS - 2; c >= 1; --c) {
+        const int64_t b0 = plan.class_off[c] - plan.class_off[1];
+        const int64_t cnt = static_cast<int64_t>(hc[c]) - b0;
+        launch_light<true>(h, c, m, tl.p + b0, cnt, out);
+    }
+    run_windows<true>(h, m, plan, out);
 }
 
 // Narrow B: symbolic (+ products) -> int64 scan -> numeric, no planning.
