@@ -241,3 +241,28 @@ def test_counting_sort_wide_and_duplicate_tiles(engine):
     o = O.spgemm_rowwise(a, b)
     assert_csr_identical(c, o, "wide / duplicate tiles")
     assert engine.exec_stats()["units"][7] > 0, "no heavy rows"
+
+
+def test_duplicate_heavy_rows_hash_accumulator(engine):
+    """Rows whose products repeat columns (compression factor >= 2, <= 256
+    outputs) run on the warp hash accumulator, summed in k order; rows with
+    more outputs stay on the sort tiles.  Mixed signs make any reordering of a
+    sum visible in the bits."""
+    rng = np.random.default_rng(77)
+    n = 4000
+    rows, cols = [], []
+    for i in range(n):
+        if i % 7 == 0:  # wide rows: > 256 distinct outputs through the tiles
+            cs = rng.choice(n, size=40, replace=False)
+        else:  # stencil-like: neighbours in a small window
+            cs = np.unique(np.clip(i + rng.integers(-12, 13, size=20), 0, n - 1))
+        rows += [i] * len(cs)
+        cols += list(cs)
+    a = B.coo_to_csr(n, n, np.array(rows), np.array(cols), rng.uniform(-4, 4, size=len(rows)))
+    A = engine.upload(a)
+    engine.profile(True)
+    c = engine.spgemm_rowwise(A, A).download()
+    prof = engine.profile_report()
+    engine.profile(False)
+    assert_csr_identical(c, O.spgemm_rowwise(a, a), "duplicate-heavy rows")
+    assert "hashacc_kernel" in prof, sorted(prof)
