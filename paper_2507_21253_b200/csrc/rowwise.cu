@@ -615,18 +615,20 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
 // K4: dense window kernel (heavy windows, width <= WD, any product count)
 // ---------------------------------------------------------------------------
 constexpr int DT = 256;
-constexpr int DI = CAP / DT;
+// products per sorted batch (2048: the tile fits 3 CTAs/SM)
+constexpr int DCAP = 2048;
+constexpr int DI = DCAP / DT;
 
 struct DenseShared {
     using Sort = cub::BlockRadixSort<uint32_t, DT, DI, uint16_t>;
     using Scan = cub::BlockScan<int32_t, DT>;
     double acc[WD];
     uint32_t bitmap[WD / 32];
-    uint32_t keys[CAP];
-    double vals[CAP];
+    uint32_t keys[DCAP];
+    double vals[DCAP];
     union {
         typename Sort::TempStorage sort;
-        uint16_t sidx[CAP];
+        uint16_t sidx[DCAP];
     } u;
     typename Scan::TempStorage scan;
     int64_t pstart[DT];
@@ -675,7 +677,7 @@ __device__ __forceinline__ void dense_batch(DenseShared& s, int n) {
 }
 
 template <bool NUMERIC>
-__global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(DT, 3) dense_window_kernel(Mats m, const int32_t* __restrict__ ids,
                                                           const Window* __restrict__ wins,
                                                           OutCtx out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -737,7 +739,7 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
         // NUMERIC: the chunk's products are appended, in (k, j) order, to the
         // current batch; a full batch (or the last one) is sorted and added.
         for (int cpos = 0; cpos < chunk;) {
-            const int take = min(chunk - cpos, CAP - fill);
+            const int take = min(chunk - cpos, DCAP - fill);
             for (int slot = warp; slot < nslots; slot += NW) {
                 const int o = s.poff[slot], l = s.plen[slot];
                 const int lo = max(o, cpos), hi = min(o + l, cpos + take);
@@ -766,9 +768,9 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
             }
             fill += take;
             cpos += take;
-            if (fill == CAP) {
+            if (fill == DCAP) {
                 __syncthreads();
-                dense_batch(s, CAP);
+                dense_batch(s, DCAP);
                 fill = 0;
             }
         }
@@ -793,21 +795,18 @@ __global__ void __launch_bounds__(DT) dense_window_kernel(Mats m, const int32_t*
         return;
     }
     const int64_t base = out.crp[row - out.row_begin] + out.win_scan[w] - out.win_scan[wd.first];
-    // stage sorted output in keys/vals (batch buffers are free now)
+    // sorted output: word t of the bitmap holds columns 32t..32t+31; its
+    // entries start at woff (the batch buffers may be smaller than WD, so the
+    // output is not staged)
     uint32_t wbits = word;
-    int r = woff;
+    int64_t r = base + woff;
     while (wbits) {
         const int b = __ffs(wbits) - 1;
         wbits &= wbits - 1;
         const uint32_t c = static_cast<uint32_t>(tid * 32 + b);
-        s.keys[r] = c + static_cast<uint32_t>(c0);
-        s.vals[r] = s.acc[c];
+        out.ccol[r] = static_cast<int32_t>(c + static_cast<uint32_t>(c0));
+        out.cval[r] = s.acc[c];
         ++r;
-    }
-    __syncthreads();
-    for (int e = tid; e < tot; e += DT) {
-        out.ccol[base + e] = static_cast<int32_t>(s.keys[e]);
-        out.cval[base + e] = s.vals[e];
     }
 }
 
