@@ -619,13 +619,15 @@ constexpr int DT = 256;
 constexpr int DCAP = 2048;
 constexpr int DI = DCAP / DT;
 
-struct DenseShared {
+template <bool NUMERIC>
+struct DenseSharedT {
     using Sort = cub::BlockRadixSort<uint32_t, DT, DI, uint16_t>;
     using Scan = cub::BlockScan<int32_t, DT>;
-    double acc[WD];
+    static constexpr int NV = NUMERIC ? 1 : 0;  // the symbolic pass keeps only the bitmap
+    double acc[NUMERIC ? WD : 1];
     uint32_t bitmap[WD / 32];
-    uint32_t keys[DCAP];
-    double vals[DCAP];
+    uint32_t keys[NUMERIC ? DCAP : 1];
+    double vals[NUMERIC ? DCAP : 1];
     union {
         typename Sort::TempStorage sort;
         uint16_t sidx[DCAP];
@@ -640,7 +642,8 @@ struct DenseShared {
 // One batch of n products (k order) of a dense window: stable sort by column
 // (12-bit keys; the pad WD-1 sits after the n real entries), then every run of
 // equal columns is added to its accumulator left to right.
-__device__ __forceinline__ void dense_batch(DenseShared& s, int n) {
+template <class SD>
+__device__ __forceinline__ void dense_batch(SD& s, int n) {
     const int tid = threadIdx.x;
     uint32_t k[DI];
     uint16_t v[DI];
@@ -651,7 +654,7 @@ __device__ __forceinline__ void dense_batch(DenseShared& s, int n) {
         v[i] = static_cast<uint16_t>(e);
     }
     __syncthreads();
-    DenseShared::Sort(s.u.sort).Sort(k, v, 0, LOG_WD);
+    typename SD::Sort(s.u.sort).Sort(k, v, 0, LOG_WD);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < DI; ++i) {
@@ -681,7 +684,8 @@ __global__ void __launch_bounds__(DT, 3) dense_window_kernel(Mats m, const int32
                                                           const Window* __restrict__ wins,
                                                           OutCtx out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    DenseShared& s = *reinterpret_cast<DenseShared*>(smem_raw);
+    using SD = DenseSharedT<NUMERIC>;
+    SD& s = *reinterpret_cast<SD*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = DT / 32;
     const int32_t w = ids[blockIdx.x];
@@ -706,7 +710,7 @@ __global__ void __launch_bounds__(DT, 3) dense_window_kernel(Mats m, const int32
             if (NUMERIC) av = __ldg(m.aval + p);
         }
         int off, chunk;
-        DenseShared::Scan(s.scan).ExclusiveSum(len, off, chunk);
+        typename SD::Scan(s.scan).ExclusiveSum(len, off, chunk);
         s.pstart[tid] = start;
         s.plen[tid] = len;
         s.poff[tid] = off;
@@ -785,7 +789,7 @@ __global__ void __launch_bounds__(DT, 3) dense_window_kernel(Mats m, const int32
     const uint32_t word = tid < NWORD ? s.bitmap[tid] : 0u;
     const int pc = __popc(word);
     int woff, tot;
-    DenseShared::Scan(s.scan).ExclusiveSum(pc, woff, tot);
+    typename SD::Scan(s.scan).ExclusiveSum(pc, woff, tot);
     if (!NUMERIC) {
         if (tid == 0) {
             out.win_nnz[w] = tot;
@@ -963,9 +967,9 @@ void launch_dense(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, co
                   const OutCtx& out) {
     if (n <= 0) return;
     auto k = dense_window_kernel<NUMERIC>;
-    set_smem(k, sizeof(DenseShared));
+    set_smem(k, sizeof(DenseSharedT<NUMERIC>));
     BSP_LAUNCH_AS(h, NUMERIC ? "dense_window_numeric" : "dense_window_symbolic", k,
-                  static_cast<unsigned>(n), DT, sizeof(DenseShared), m, ids, wins, out);
+                  static_cast<unsigned>(n), DT, sizeof(DenseSharedT<NUMERIC>), m, ids, wins, out);
 }
 
 }  // namespace
