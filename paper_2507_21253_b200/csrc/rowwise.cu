@@ -615,8 +615,8 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
 // K4: dense window kernel (heavy windows, width <= WD, any product count)
 // ---------------------------------------------------------------------------
 constexpr int DT = 256;
-// products per sorted batch (2048: the tile fits 3 CTAs/SM)
-constexpr int DCAP = 2048;
+// products per sorted batch (1024: the tile fits 4 CTAs/SM)
+constexpr int DCAP = 1024;
 constexpr int DI = DCAP / DT;
 
 template <bool NUMERIC>
@@ -680,7 +680,7 @@ __device__ __forceinline__ void dense_batch(SD& s, int n) {
 }
 
 template <bool NUMERIC>
-__global__ void __launch_bounds__(DT, 3) dense_window_kernel(Mats m, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(DT, 4) dense_window_kernel(Mats m, const int32_t* __restrict__ ids,
                                                           const Window* __restrict__ wins,
                                                           OutCtx out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
