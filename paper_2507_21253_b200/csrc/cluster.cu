@@ -444,6 +444,109 @@ int grid_for(bsp_handle h, int64_t n, int block) {
         1, std::min<int64_t>(div_up(std::max<int64_t>(n, 1), block), int64_t{h->sm_count} * 16)));
 }
 
+// Narrow-B routing: clusters of 2..MAXK members go to the cluster kernel and
+// their rows are skipped by the row kernel.
+__global__ void narrow_route_kernel(ClusterMats m, int64_t ncl, uint8_t* __restrict__ skip,
+                                    int32_t* __restrict__ lists,
+                                    unsigned long long* __restrict__ count) {
+    for (int64_t c = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; c < ncl;
+         c += int64_t{gridDim.x} * blockDim.x) {
+        const int64_t mb = m.member_ptr[c], K = m.member_ptr[c + 1] - mb;
+        if (K < 2 || K > MAXK) continue;
+        lists[atomicAdd(count, 1ull)] = static_cast<int32_t>(c);
+        for (int64_t l = 0; l < K; ++l) skip[m.row_map[mb + l]] = 1;
+    }
+}
+
+// Cluster-wise multiply for B with <= 64 columns (the tall-skinny frontier
+// operands): a warp per cluster walks its merged columns in k order; each B
+// row's 64-bit column mask and values are loaded ONCE and scattered into the
+// register accumulators (columns lane, lane + 32) of every live member — the
+// paper's B-row reuse across a cluster.  Per member and column the adds come in
+// ascending k from 0.0, as in the member's row-wise multiply.  Members are
+// taken 8 at a time (accumulators in registers).
+constexpr int CN_WARPS = 8, CN_GROUP = 8;
+
+__global__ void __launch_bounds__(CN_WARPS * 32)
+    cluster_narrow64_kernel(ClusterMats m, const unsigned long long* __restrict__ bmask,
+                            const int32_t* __restrict__ ids, int64_t ncl,
+                            const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
+                            double* __restrict__ oval) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned long long below0 = (1ull << lane) - 1ull, below1 = (1ull << (lane + 32)) - 1ull;
+    for (int64_t t = blockIdx.x * int64_t{CN_WARPS} + warp; t < ncl;
+         t += int64_t{gridDim.x} * CN_WARPS) {
+        const int32_t c = ids[t];
+        const int64_t mb = m.member_ptr[c];
+        const int K = static_cast<int>(m.member_ptr[c + 1] - mb);
+        const int64_t u0 = m.ccp[c], u1 = m.ccp[c + 1], vb = m.vptr[c];
+        for (int g0 = 0; g0 < K; g0 += CN_GROUP) {
+            const uint32_t gmask = ((K - g0 >= 32) ? 0xffffffffu : ((1u << (K - g0)) - 1u)) &
+                                   ((1u << CN_GROUP) - 1u);
+            double acc0[CN_GROUP], acc1[CN_GROUP];
+            unsigned long long touch[CN_GROUP];
+#pragma unroll
+            for (int l = 0; l < CN_GROUP; ++l) {
+                acc0[l] = 0.0;
+                acc1[l] = 0.0;
+                touch[l] = 0ull;
+            }
+            for (int64_t ub = u0; ub < u1; ub += 32) {
+                const int64_t u = ub + lane;
+                unsigned long long mk = 0;
+                int64_t b0 = 0;
+                uint32_t mm = 0;
+                if (u < u1) {
+                    const int32_t k = __ldg(m.ccol + u);
+                    mm = (__ldg(m.mask + u) >> g0) & gmask;
+                    if (mm) {
+                        mk = __ldg(bmask + k);
+                        b0 = __ldg(m.brp + k);
+                    }
+                }
+                unsigned ne = __ballot_sync(0xffffffffu, mk != 0 && mm != 0);
+                while (ne) {
+                    const int j = __ffs(ne) - 1;
+                    ne &= ne - 1;
+                    const unsigned long long mj = __shfl_sync(0xffffffffu, mk, j);
+                    const int64_t bj = __shfl_sync(0xffffffffu, b0, j);
+                    const uint32_t mmj = __shfl_sync(0xffffffffu, mm, j);
+                    const int64_t uj = ub + j;
+                    const bool h0 = (mj >> lane) & 1ull, h1 = (mj >> (lane + 32)) & 1ull;
+                    const double bv0 = h0 ? __ldg(m.bval + bj + __popcll(mj & below0)) : 0.0;
+                    const double bv1 = h1 ? __ldg(m.bval + bj + __popcll(mj & below1)) : 0.0;
+                    const double* av = m.aval + vb + (uj - u0) * K + g0;
+#pragma unroll
+                    for (int l = 0; l < CN_GROUP; ++l) {
+                        if (!((mmj >> l) & 1u)) continue;
+                        const double a = __ldg(av + l);
+                        if (h0) acc0[l] = __dadd_rn(acc0[l], __dmul_rn(a, bv0));
+                        if (h1) acc1[l] = __dadd_rn(acc1[l], __dmul_rn(a, bv1));
+                        touch[l] |= mj;
+                    }
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < CN_GROUP; ++l) {
+                if (g0 + l >= K) break;
+                const int32_t row = m.row_map[mb + g0 + l];
+                const int64_t pos = crp[row];
+                const unsigned long long T = touch[l];  // warp-uniform (broadcast masks)
+                if ((T >> lane) & 1ull) {
+                    const int64_t o = pos + __popcll(T & below0);
+                    ocol[o] = lane;
+                    oval[o] = acc0[l];
+                }
+                if ((T >> (lane + 32)) & 1ull) {
+                    const int64_t o = pos + __popcll(T & below1);
+                    ocol[o] = lane + 32;
+                    oval[o] = acc1[l];
+                }
+            }
+        }
+    }
+}
+
 ClusterMats make_cluster_mats(const bsp_csr_cluster* a, const bsp_csr* b) {
     return ClusterMats{a->cluster_sizes, a->member_ptr, a->cluster_col_ptr, a->col_idx,
                        a->value_ptr,     a->values,     a->member_mask,     a->row_map,
@@ -678,6 +781,59 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         }
         const ClusterMats cm = make_cluster_mats(A, B);
         const int cbits = bit_length(static_cast<uint32_t>(std::max<int64_t>(B->ncols - 1, 0)));
+        // B with <= 64 columns and CSR output only (BSP_NARROW=0 forces the
+        // tiles): every row
+        // counted by the row-wise mask kernel (C's structure does not depend on
+        // the clustering), tiled clusters on the cluster mask kernel, the
+        // other rows on the row-wise one.
+        const char* ne_env = std::getenv("BSP_NARROW");
+        const Mats m = make_mats(&acsr, B);
+        if (B->ncols <= 64 && !(ne_env && ne_env[0] == '0') && C_cluster == nullptr) {
+            // clusters of 2..MAXK members on the cluster kernel (their rows
+            // skipped by the row kernel), the rest row by row
+            DBuf<uint8_t> skip(h, n);
+            BSP_CUDA(cudaMemsetAsync(skip.p, 0, std::max<int64_t>(n, 1), h->stream));
+            DBuf<int32_t> lists(h, std::max<int64_t>(ncl, 1));
+            DBuf<unsigned long long> ccount(h, 1);
+            BSP_CUDA(cudaMemsetAsync(ccount.p, 0, sizeof(unsigned long long), h->stream));
+            BSP_LAUNCH(h, narrow_route_kernel, grid_for(h, ncl, 256), 256, 0, cm, ncl, skip.p,
+                       lists.p, ccount.p);
+            const int64_t acc = static_cast<int64_t>(read_scalar(h, ccount.p));
+            DBuf<unsigned long long> bmask;
+            narrow64_row_masks(h, m, B->nrows, bmask);
+            DBuf<int64_t> row_nnz(h, n + 1);
+            BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
+            DBuf<unsigned long long> prod(h, 1);
+            BSP_CUDA(cudaMemsetAsync(prod.p, 0, sizeof(unsigned long long), h->stream));
+            narrow64_rows(h, m, bmask.p, n, nullptr, row_nnz.p, nullptr, nullptr, nullptr, prod.p);
+            DBuf<int64_t> rp(h, n + 1, Pool::out);
+            exclusive_scan_i64(h, row_nnz.p, rp.p, n + 1);
+            const int64_t nnz = read_scalar(h, rp.p + n);
+            h->stats.products = static_cast<int64_t>(read_scalar(h, prod.p));
+            h->stats.nnz_out = nnz;
+            h->stats.units[10] = acc;
+            ResultPayload pay(h, nnz);
+            if (acc > 0)
+                BSP_LAUNCH_AS(h, "cluster_narrow64", cluster_narrow64_kernel,
+                              grid_for(h, div_up(acc, CN_WARPS), 1), CN_WARPS * 32, 0, cm, bmask.p,
+                              lists.p, acc, rp.p, pay.col_idx(), pay.values());
+            narrow64_rows(h, m, bmask.p, n, skip.p, nullptr, rp.p, pay.col_idx(), pay.values(),
+                          nullptr);
+            C->nrows = n;
+            C->ncols = B->ncols;
+            C->nnz = nnz;
+            C->row_ptr = rp.release();
+            C->col_idx = pay.col_idx();
+            C->values = pay.block.release();
+            C->owned = 2;
+            if (tmp_csr.owned) {
+                dfree(h, tmp_csr.row_ptr);
+                dfree(h, tmp_csr.col_idx);
+                dfree(h, tmp_csr.values);
+            }
+            return;
+        }
+
         DBuf<uint8_t> ccls(h, ncl);
         DBuf<uint8_t> skip(h, n);
         BSP_CUDA(cudaMemsetAsync(skip.p, 0, std::max<int64_t>(n, 1), h->stream));
@@ -704,7 +860,6 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
             BSP_LAUNCH(h, cluster_bucket_kernel, grid_for(h, ncl, 256), 256, 0, ccls.p, ncl,
                        cursor.p, lists.p);
         }
-        const Mats m = make_mats(&acsr, B);
         RowwisePlan plan;  // rows outside cluster tiles (incl. heavy windows)
         build_plan(h, m, 0, n, skip.p, plan, nullptr);
         h->stats.units[10] = cnt[1] + cnt[2] + cnt[3] + cnt[4] + cnt[5];  // cluster tiles

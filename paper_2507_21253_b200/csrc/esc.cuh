@@ -203,6 +203,15 @@ void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t
 void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
                   const int64_t* win_scan, int32_t* ccol, double* cval);
 
+// B with <= 64 columns: per-row 64-bit column masks of B, then the row-wise
+// narrow kernel over rows [0, n) of A (skip[r] != 0 rows left out): symbolic
+// when crp == nullptr (row_nnz, products), else numeric into C at crp.
+void narrow64_row_masks(bsp_handle h, const Mats& m, int64_t bnrows,
+                        DBuf<unsigned long long>& mask);
+void narrow64_rows(bsp_handle h, const Mats& m, const unsigned long long* mask, int64_t n,
+                   const uint8_t* skip, int64_t* row_nnz, const int64_t* crp, int32_t* ccol,
+                   double* cval, unsigned long long* products);
+
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
     BSP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

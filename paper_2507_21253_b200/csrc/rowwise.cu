@@ -1417,12 +1417,13 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32)
     narrow64_kernel(Mats m, const unsigned long long* __restrict__ bmask, int64_t rb, int64_t n,
                     int64_t* __restrict__ row_nnz, const int64_t* __restrict__ crp,
                     int32_t* __restrict__ ccol, double* __restrict__ cval,
-                    unsigned long long* __restrict__ products) {
+                    unsigned long long* __restrict__ products, const uint8_t* __restrict__ skip) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned long long below0 = (1ull << lane) - 1ull, below1 = (1ull << (lane + 32)) - 1ull;
     unsigned long long prod = 0;
     for (int64_t r = blockIdx.x * int64_t{NARROW_WARPS} + warp; r < n;
          r += int64_t{gridDim.x} * NARROW_WARPS) {
+        if (skip && skip[r]) continue;  // warp-uniform (rows of a cluster tile)
         const int64_t row = rb + r;
         const int64_t rs = m.arp[row], re = m.arp[row + 1];
         unsigned long long touch = 0;
@@ -1505,7 +1506,7 @@ static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, 
             1, std::min<int64_t>(div_up(std::max<int64_t>(bnrows, 1), 256), int64_t{h->sm_count} * 8)));
         BSP_LAUNCH(h, row_mask64_kernel, gm, 256, 0, m.brp, m.bcol, bnrows, bmask.p);
         BSP_LAUNCH_AS(h, "narrow64_symbolic", narrow64_kernel<false>, grid, NARROW_WARPS * 32, 0, m,
-                      bmask.p, rb, n, cnt.p, nullptr, nullptr, nullptr, prod.p);
+                      bmask.p, rb, n, cnt.p, nullptr, nullptr, nullptr, prod.p, nullptr);
     } else {
         BSP_LAUNCH_AS(h, "narrow_symbolic", ks, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, cnt.p,
                       nullptr, nullptr, nullptr, prod.p);
@@ -1521,7 +1522,7 @@ static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, 
     ResultPayload pay(h, nnz);
     if (m64)
         BSP_LAUNCH_AS(h, "narrow64_numeric", narrow64_kernel<true>, grid, NARROW_WARPS * 32, 0, m,
-                      bmask.p, rb, n, nullptr, rp.p, pay.col_idx(), pay.values(), nullptr);
+                      bmask.p, rb, n, nullptr, rp.p, pay.col_idx(), pay.values(), nullptr, nullptr);
     else
         BSP_LAUNCH_AS(h, "narrow_numeric", kn, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, nullptr,
                       rp.p, pay.col_idx(), pay.values(), nullptr);
@@ -1532,6 +1533,28 @@ static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, 
     C->col_idx = pay.col_idx();
     C->values = pay.block.release();
     C->owned = 2;
+}
+
+void narrow64_row_masks(bsp_handle h, const Mats& m, int64_t bnrows,
+                        DBuf<unsigned long long>& mask) {
+    mask = DBuf<unsigned long long>(h, std::max<int64_t>(bnrows, 1));
+    const unsigned gm = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>(div_up(std::max<int64_t>(bnrows, 1), 256), int64_t{h->sm_count} * 8)));
+    BSP_LAUNCH(h, row_mask64_kernel, gm, 256, 0, m.brp, m.bcol, bnrows, mask.p);
+}
+
+void narrow64_rows(bsp_handle h, const Mats& m, const unsigned long long* mask, int64_t n,
+                   const uint8_t* skip, int64_t* row_nnz, const int64_t* crp, int32_t* ccol,
+                   double* cval, unsigned long long* products) {
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>(div_up(std::max<int64_t>(n, 1), NARROW_WARPS),
+                             int64_t{h->sm_count} * 32)));
+    if (crp == nullptr)
+        BSP_LAUNCH_AS(h, "narrow64_symbolic", narrow64_kernel<false>, grid, NARROW_WARPS * 32, 0, m,
+                      mask, int64_t{0}, n, row_nnz, nullptr, nullptr, nullptr, products, skip);
+    else
+        BSP_LAUNCH_AS(h, "narrow64_numeric", narrow64_kernel<true>, grid, NARROW_WARPS * 32, 0, m,
+                      mask, int64_t{0}, n, nullptr, crp, ccol, cval, nullptr, skip);
 }
 
 void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t rb, int64_t re,
