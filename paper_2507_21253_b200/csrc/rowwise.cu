@@ -1445,17 +1445,34 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32)
             }
             touch |= mk;
             if (NUMERIC) {
+                // non-empty segments in k order, NP at a time: their b loads
+                // are all issued before the ordered adds (latency overlap)
+                constexpr int NP = 4;
                 unsigned ne = __ballot_sync(0xffffffffu, mk != 0);
                 while (ne) {
-                    const int j = __ffs(ne) - 1;
-                    ne &= ne - 1;
-                    const unsigned long long mj = __shfl_sync(0xffffffffu, mk, j);
-                    const int64_t bj = __shfl_sync(0xffffffffu, b0, j);
-                    const double aj = __shfl_sync(0xffffffffu, a, j);
-                    if ((mj >> lane) & 1ull)
-                        acc0 = __dadd_rn(acc0, __dmul_rn(aj, __ldg(m.bval + bj + __popcll(mj & below0))));
-                    if ((mj >> (lane + 32)) & 1ull)
-                        acc1 = __dadd_rn(acc1, __dmul_rn(aj, __ldg(m.bval + bj + __popcll(mj & below1))));
+                    double aj[NP], v0[NP], v1[NP];
+                    bool h0[NP], h1[NP];
+#pragma unroll
+                    for (int u = 0; u < NP; ++u) {
+                        h0[u] = h1[u] = false;
+                        aj[u] = v0[u] = v1[u] = 0.0;
+                        if (ne) {
+                            const int j = __ffs(ne) - 1;
+                            ne &= ne - 1;
+                            const unsigned long long mj = __shfl_sync(0xffffffffu, mk, j);
+                            const int64_t bj = __shfl_sync(0xffffffffu, b0, j);
+                            aj[u] = __shfl_sync(0xffffffffu, a, j);
+                            h0[u] = (mj >> lane) & 1ull;
+                            h1[u] = (mj >> (lane + 32)) & 1ull;
+                            if (h0[u]) v0[u] = __ldg(m.bval + bj + __popcll(mj & below0));
+                            if (h1[u]) v1[u] = __ldg(m.bval + bj + __popcll(mj & below1));
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < NP; ++u) {
+                        if (h0[u]) acc0 = __dadd_rn(acc0, __dmul_rn(aj[u], v0[u]));
+                        if (h1[u]) acc1 = __dadd_rn(acc1, __dmul_rn(aj[u], v1[u]));
+                    }
                 }
             }
         }
