@@ -266,3 +266,30 @@ def test_duplicate_heavy_rows_hash_accumulator(engine):
     engine.profile(False)
     assert_csr_identical(c, O.spgemm_rowwise(a, a), "duplicate-heavy rows")
     assert "hashacc_kernel" in prof, sorted(prof)
+
+
+@pytest.mark.parametrize("nout", [255, 256, 257])
+def test_hash_accumulator_output_bound(engine, nout):
+    """Rows right at the hash accumulator's 256-output bound (routed when
+    <= 256, tiles above), each column hit by 4 segments in k order."""
+    rng = np.random.default_rng(nout)
+    kseg = 4
+    rows_b = [np.sort(rng.choice(nout, size=nout // 2, replace=False)) for _ in range(kseg * 8)]
+    for r in range(kseg):  # make sure all nout columns occur
+        rows_b[r] = np.arange(nout)
+    rb_ = np.concatenate([[k] * len(cs) for k, cs in enumerate(rows_b)])
+    # the nout columns spread over 5000 (B wider than the narrow kernels' 256)
+    colmap = np.sort(rng.choice(5000, size=nout, replace=False))
+    b = B.coo_to_csr(len(rows_b), 5000, rb_, colmap[np.concatenate(rows_b)],
+                     rng.uniform(-3, 3, size=rb_.size))
+    ra = np.repeat(np.arange(40), 12)
+    ca = np.concatenate([np.sort(rng.choice(len(rows_b), 12, replace=False)) for _ in range(40)])
+    ca[:12] = np.arange(12)  # row 0 covers the full columns (4 full B rows)
+    a = B.coo_to_csr(40, len(rows_b), ra, ca, rng.uniform(-3, 3, size=ra.size))
+    A, Bd = engine.upload(a), engine.upload(b)
+    engine.profile(True)
+    c = engine.spgemm_rowwise(A, Bd).download()
+    prof = engine.profile_report()
+    engine.profile(False)
+    assert_csr_identical(c, O.spgemm_rowwise(a, b), f"{nout} outputs")
+    assert "hashacc_kernel" in prof  # rows with fewer outputs are routed in every case
