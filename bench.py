@@ -185,6 +185,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # plumbing check only (not a measurement): BSP_BENCH_SHARED_GPU=1 puts every
+    # rank on cuda:0 and talks gloo, so the N-rank code path runs on one GPU
+    shared_gpu = os.environ.get("BSP_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
 
     import paper_2507_21253_b200 as B
 
@@ -206,7 +211,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 
     # ---- input: generated on rank 0, replicated with an NCCL broadcast ----
     if rank == 0:
