@@ -515,22 +515,29 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
     // smaller words, higher ones and the pad only larger) — 4 per 16-byte load,
     // no bucket array, no tie path.
     constexpr int IB = 32 - __builtin_clz(static_cast<unsigned>(CAPM - 1));
-    if (cbits == 0 && cw + IB <= 32) {
+    if (lk + cw + IB <= 32) {
+        // (member, column - min, index) in one word: member-major like the
+        // buckets (cluster tiles; member = 0 for rows and windows)
 #pragma unroll
         for (int i = 0; i < I; ++i) {
             const int e = i * T + tid;
             if (e < total) {
-                const uint32_t rel = kr[i] - cmin;
+                const uint32_t mem = cbits > 0 ? kr[i] >> cbits : 0u;
+                const uint32_t rel = (kr[i] & cmask) - cmin;
+                const uint32_t b = (mem << cb) | (rel >> sh);
                 const uint32_t ix = kofs >= 0 ? static_cast<uint32_t>(e) : s.idx0[PADI(e)];
-                pk[cnt[rel >> sh] + static_cast<int>(rr[i])] = (rel << IB) | ix;
+                pk[cnt[b] + static_cast<int>(rr[i])] = (((mem << cw) | rel) << IB) | ix;
             }
         }
         if (tid < 4) pk[total + tid] = 0xffffffffu;
         __syncthreads();
         const uint32_t im = (1u << IB) - 1u;
+        const uint32_t rm = (1u << cw) - 1u;  // cw <= 32 - IB
         for (int q = tid; q < total; q += T) {
             const uint32_t v = pk[q];
-            const uint32_t b = (v >> IB) >> sh;
+            const uint32_t mr = v >> IB;
+            const uint32_t mem = mr >> cw, rel = mr & rm;
+            const uint32_t b = (mem << cb) | (rel >> sh);
             const int lo = cnt[b], hi = cnt[b + 1];
             int c = lo;
             if (hi - lo > 1) {
@@ -540,7 +547,8 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
                     c += (w.x < v) + (w.y < v) + (w.z < v) + (w.w < v);
                 }
             }
-            s.key0[PADI(c)] = (v >> IB) + cmin - static_cast<uint32_t>(kofs > 0 ? kofs : 0);
+            const uint32_t col = rel + cmin - static_cast<uint32_t>(kofs > 0 ? kofs : 0);
+            s.key0[PADI(c)] = cbits > 0 ? (mem << cbits) | col : col;
             s.idx0[PADI(c)] = static_cast<uint16_t>(v & im);
         }
         __syncthreads();
