@@ -217,7 +217,7 @@ __global__ void cluster_bucket_kernel(const uint8_t* __restrict__ ccls, int64_t 
 // original rows.
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
-__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : (T == 128 ? 8 : 4)))
+__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : (T == 128 ? 8 : 16)))
     cluster_tile_kernel(ClusterMats m, const int32_t* __restrict__ ids, int cbits, int csort,
                         int csort_radix_only,
                         const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,

@@ -449,7 +449,7 @@ __global__ void window_c0_kernel(const Window* __restrict__ wins, const int32_t*
 // K3': merge-based exact numeric tile and hash-count symbolic tile
 // ---------------------------------------------------------------------------
 template <int T, int CAPM>
-__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : (T == 128 ? 8 : (T == 64 ? 16 : 4)))) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
+__global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 2048 ? 4 : 2) : (T == 128 ? 8 : (T == 64 ? 16 : 32)))) esc_merge_kernel(Mats m, const int32_t* __restrict__ ids,
                                                       const Window* __restrict__ wins, OutCtx out, int csort) {
     using S = MergeShared<T, CAPM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
