@@ -85,6 +85,7 @@ typedef struct {
     int32_t* csr_col_idx;
     double* csr_values;
     int32_t owned;
+    int64_t csr_nnz;          /* nnz of the row view (0: unknown / no view) */
 } bsp_csr_cluster;
 
 /* Host mirror of CSR_Cluster (for download / host-side checks). */

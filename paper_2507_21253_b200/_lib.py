@@ -40,7 +40,7 @@ class bsp_csr_cluster(C.Structure):
                 ("nslots", i64), ("cluster_sizes", vp), ("member_ptr", vp),
                 ("cluster_col_ptr", vp), ("col_idx", vp), ("value_ptr", vp), ("values", vp),
                 ("valid", vp), ("member_mask", vp), ("row_map", vp), ("csr_row_ptr", vp),
-                ("csr_col_idx", vp), ("csr_values", vp), ("owned", i32)]
+                ("csr_col_idx", vp), ("csr_values", vp), ("owned", i32), ("csr_nnz", i64)]
 
 
 class bsp_host_csr_cluster(C.Structure):

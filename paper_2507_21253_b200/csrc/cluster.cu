@@ -605,6 +605,7 @@ void build_cluster_device(bsp_handle h, const bsp_csr* A, int64_t ncl, int64_t* 
     out->csr_row_ptr = nullptr;
     out->csr_col_idx = nullptr;
     out->csr_values = nullptr;
+    out->csr_nnz = 0;
     if (keep_csr) {
         DBuf<int64_t> rp(h, A->nrows + 1, Pool::out);
         DBuf<int32_t> ci(h, A->nnz, Pool::out);
@@ -618,6 +619,7 @@ void build_cluster_device(bsp_handle h, const bsp_csr* A, int64_t ncl, int64_t* 
         out->csr_row_ptr = rp.release();
         out->csr_col_idx = ci.release();
         out->csr_values = v.release();
+        out->csr_nnz = A->nnz;
     }
     out->owned = 1;
 }
@@ -771,9 +773,11 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         bsp_csr acsr{};
         bsp_csr tmp_csr{};
         if (A->csr_row_ptr) {
-            int64_t nnz = 0;
-            d2h(h, &nnz, A->csr_row_ptr + n, 1);
-            sync(h);
+            int64_t nnz = A->csr_nnz;  // recorded at build time (no readback)
+            if (nnz <= 0) {
+                d2h(h, &nnz, A->csr_row_ptr + n, 1);
+                sync(h);
+            }
             acsr = bsp_csr{n, A->ncols, nnz, A->csr_row_ptr, A->csr_col_idx, A->csr_values, 0};
         } else {
             cluster_to_csr_device(h, A, &tmp_csr);
