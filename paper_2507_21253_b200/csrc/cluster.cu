@@ -187,12 +187,6 @@ __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
     if (threadIdx.x < NCC) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
 }
 
-__global__ void invert_mask_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                                   int64_t n) {
-    for (int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; i < n;
-         i += int64_t{gridDim.x} * blockDim.x)
-        out[i] = in[i] ? 0 : 1;
-}
 
 __global__ void cluster_bucket_kernel(const uint8_t* __restrict__ ccls, int64_t ncl,
                                       unsigned long long* __restrict__ cursor,
@@ -864,19 +858,16 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
             BSP_LAUNCH(h, cluster_bucket_kernel, grid_for(h, ncl, 256), 256, 0, ccls.p, ncl,
                        cursor.p, lists.p);
         }
-        RowwisePlan plan;  // rows outside cluster tiles (incl. heavy windows)
-        build_plan(h, m, 0, n, skip.p, plan, nullptr);
+        RowwisePlan plan;    // rows outside cluster tiles (incl. heavy windows)
+        RowwisePlan plan_c;  // the cluster tiles' rows, for their symbolic counts
+        build_plan(h, m, 0, n, skip.p, plan, nullptr, nullptr, &plan_c);
         h->stats.units[10] = cnt[1] + cnt[2] + cnt[3] + cnt[4] + cnt[5];  // cluster tiles
         DBuf<int64_t> row_nnz(h, n + 1);
         BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
         // Symbolic: C's row structure does not depend on the clustering, so the
-        // cluster rows are counted by the (cheaper) row-wise hash tiles of a
-        // second plan restricted to them.
+        // cluster rows are counted by the (cheaper) row-wise hash tiles of the
+        // shadow plan built in the same pass.
         {
-            DBuf<uint8_t> only(h, n);
-            BSP_LAUNCH(h, invert_mask_kernel, grid_for(h, n, 256), 256, 0, skip.p, only.p, n);
-            RowwisePlan plan_c;
-            build_plan(h, m, 0, n, only.p, plan_c, nullptr);
             DBuf<int64_t> wn_c;
             plan_symbolic(h, m, plan_c, row_nnz.p, wn_c);
         }

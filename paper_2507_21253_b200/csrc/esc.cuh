@@ -195,8 +195,11 @@ struct RowwisePlan {
 Mats make_mats(const bsp_csr* A, const bsp_csr* B);
 // early_row_nnz (zeroed, optional): count the light rows' outputs there on the
 // handle's side stream while the heavy rows are planned (plan_symbolic joins).
+// shadow (optional, with skip): the skipped rows planned apart in the same
+// pass (light rows only; used for the cluster rows' symbolic).
 void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re, const uint8_t* skip,
-                RowwisePlan& plan, int64_t* prod_out, int64_t* early_row_nnz = nullptr);
+                RowwisePlan& plan, int64_t* prod_out, int64_t* early_row_nnz = nullptr,
+                RowwisePlan* shadow = nullptr);
 // Symbolic counts of a plan into row_nnz (NOT zeroed here) and win_nnz (allocated).
 void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t* row_nnz,
                    DBuf<int64_t>& win_nnz);

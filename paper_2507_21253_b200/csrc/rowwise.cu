@@ -51,9 +51,10 @@ namespace {
 __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restrict__ prod,
                                 uint8_t* __restrict__ cls, const uint8_t* __restrict__ skip,
                                 int64_t* __restrict__ class_count,
-                                int64_t* __restrict__ class_products) {
-    __shared__ unsigned long long s_cnt[NCLS], s_prod[NCLS];
-    if (threadIdx.x < NCLS) {
+                                int64_t* __restrict__ class_products, int shadow) {
+    // shadow: skipped rows get their own classes NCLS + c (a second plan)
+    __shared__ unsigned long long s_cnt[2 * NCLS], s_prod[2 * NCLS];
+    if (threadIdx.x < 2 * NCLS) {
         s_cnt[threadIdx.x] = 0;
         s_prod[threadIdx.x] = 0;
     }
@@ -73,12 +74,11 @@ __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restri
         for (int o = 16; o > 0; o >>= 1) P += __shfl_xor_sync(0xffffffffu, P, o);
         if (lane == 0) {
             int c = 0;
-            if (skip && skip[r]) {
-                c = 0;
-            } else if (P > 0) {
+            if (P > 0) {
                 c = 1;
                 while (c < NCLS - 1 && P > kClassCap[c]) ++c;
             }
+            if (skip && skip[r]) c = (shadow && c > 0) ? NCLS + c : 0;
             if (prod) prod[r] = P;
             cls[r] = static_cast<uint8_t>(c);
             atomicAdd(&s_cnt[c], 1ull);
@@ -86,7 +86,7 @@ __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restri
         }
     }
     __syncthreads();
-    if (threadIdx.x < NCLS) {
+    if (threadIdx.x < (shadow ? 2 * NCLS : NCLS)) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&class_count[threadIdx.x]), s_cnt[threadIdx.x]);
         atomicAdd(reinterpret_cast<unsigned long long*>(&class_products[threadIdx.x]),
                   s_prod[threadIdx.x]);
@@ -96,10 +96,11 @@ __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restri
 // K1: group row ids (absolute) by class into per-class regions.
 __global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64_t n,
                               unsigned long long* __restrict__ cursor,
-                              int32_t* __restrict__ lists) {
-    __shared__ unsigned s_cnt[NCLS];
-    __shared__ unsigned long long s_base[NCLS];
-    if (threadIdx.x < NCLS) s_cnt[threadIdx.x] = 0;
+                              int32_t* __restrict__ lists, int32_t* __restrict__ lists2) {
+    // classes NCLS + c (shadow plan) go to lists2 at cursor[NCLS + c]
+    __shared__ unsigned s_cnt[2 * NCLS];
+    __shared__ unsigned long long s_base[2 * NCLS];
+    if (threadIdx.x < 2 * NCLS) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     const int64_t r = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
     int c = 0;
@@ -109,10 +110,11 @@ __global__ void bucket_kernel(const uint8_t* __restrict__ cls, int64_t rb, int64
         if (c > 0) rank = atomicAdd(&s_cnt[c], 1u);
     }
     __syncthreads();
-    if (threadIdx.x > 0 && threadIdx.x < NCLS)
+    if (threadIdx.x > 0 && threadIdx.x < 2 * NCLS && s_cnt[threadIdx.x])
         s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], s_cnt[threadIdx.x]);
     __syncthreads();
-    if (r < n && c > 0) lists[s_base[c] + rank] = static_cast<int32_t>(rb + r);
+    if (r < n && c > 0)
+        (c < NCLS ? lists : lists2)[s_base[c] + rank] = static_cast<int32_t>(rb + r);
 }
 
 // ---------------------------------------------------------------------------
@@ -986,7 +988,7 @@ void run_light(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCt
 
 void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                        const uint8_t* skip, RowwisePlan& plan, int64_t* prod_out,
-                       int64_t* early_row_nnz) {
+                       int64_t* early_row_nnz, RowwisePlan* shadow) {
     const int64_t n = re - rb;
     plan.rb = rb;
     plan.n = n;
@@ -994,16 +996,32 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         plan.prod = DBuf<int64_t>(h, n);
         prod_out = plan.prod.p;
     }
+    const int ncl = shadow ? 2 * NCLS : NCLS;  // shadow: skipped rows' own classes
     DBuf<uint8_t> cls(h, n);
-    DBuf<int64_t> counters(h, 2 * NCLS);
-    BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * NCLS * sizeof(int64_t), h->stream));
+    DBuf<int64_t> counters(h, 2 * ncl);
+    BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * ncl * sizeof(int64_t), h->stream));
     const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 8),
                                                         int64_t{h->sm_count} * 8));
     BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, rb, n, prod_out, cls.p, skip, counters.p,
-               counters.p + NCLS);
-    int64_t hc[2 * NCLS];
-    d2h(h, hc, counters.p, 2 * NCLS);
+               counters.p + ncl, shadow ? 1 : 0);
+    int64_t hc[4 * NCLS];
+    d2h(h, hc, counters.p, 2 * ncl);
     sync(h);
+    if (shadow) {  // rows of the skip mask, planned apart (light rows only)
+        require(hc[NCLS + NCLS - 1] == 0, "build_plan: shadow rows must be light");
+        shadow->rb = rb;
+        shadow->n = n;
+        int64_t t = 0;
+        for (int c = 0; c < NCLS; ++c) {
+            shadow->class_count[c] = c == 0 ? 0 : hc[NCLS + c];
+            shadow->class_products[c] = c == 0 ? 0 : hc[ncl + NCLS + c];
+            shadow->class_off[c] = t;
+            if (c > 0) t += hc[NCLS + c];
+        }
+        shadow->class_off[NCLS] = t;
+        shadow->lists = DBuf<int32_t>(h, t);
+        for (int c = 0; c < NCLS; ++c) hc[NCLS + c] = hc[ncl + c];  // products of plan rows
+    }
     int64_t tot_listed = 0;
     for (int c = 0; c < NCLS; ++c) {
         plan.class_count[c] = hc[c];
@@ -1015,13 +1033,17 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     h->stats.products = 0;
     for (int c = 0; c < NCLS; ++c) h->stats.products += plan.class_products[c];
     plan.lists = DBuf<int32_t>(h, tot_listed);
-    if (tot_listed > 0) {
-        DBuf<unsigned long long> cursor(h, NCLS);
-        std::vector<unsigned long long> cur(NCLS, 0);
-        for (int c = 1; c < NCLS; ++c) cur[c] = static_cast<unsigned long long>(plan.class_off[c]);
-        h2d(h, cursor.p, cur.data(), NCLS);
+    const int64_t tot_shadow = shadow ? shadow->class_off[NCLS] : 0;
+    if (tot_listed + tot_shadow > 0) {
+        DBuf<unsigned long long> cursor(h, 2 * NCLS);
+        std::vector<unsigned long long> cur(2 * NCLS, 0);
+        for (int c = 1; c < NCLS; ++c) {
+            cur[c] = static_cast<unsigned long long>(plan.class_off[c]);
+            if (shadow) cur[NCLS + c] = static_cast<unsigned long long>(shadow->class_off[c]);
+        }
+        h2d(h, cursor.p, cur.data(), 2 * NCLS);
         BSP_LAUNCH(h, bucket_kernel, static_cast<unsigned>(div_up(n, 256)), 256, 0, cls.p, rb, n,
-                   cursor.p, plan.lists.p);
+                   cursor.p, plan.lists.p, shadow ? shadow->lists.p : nullptr);
     }
     // The light rows' symbolic does not depend on the heavy-row plan: run it
     // on the side stream while the (latency-bound) planner runs here;
@@ -1647,7 +1669,7 @@ int bsp_spgemm_products(bsp_handle h, const bsp_csr* A, const bsp_csr* B,
         const int grid = static_cast<int>(std::min<int64_t>(
             div_up(std::max<int64_t>(n, 1), 8), int64_t{h->sm_count} * 8));
         BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, 0, n, prod, cls.p, nullptr, counters.p,
-                   counters.p + NCLS);
+                   counters.p + NCLS, 0);
         int64_t hc[2 * NCLS];
         d2h(h, hc, counters.p, 2 * NCLS);
         sync(h);
