@@ -1439,14 +1439,36 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32)
     narrow64_kernel(Mats m, const unsigned long long* __restrict__ bmask, int64_t rb, int64_t n,
                     int64_t* __restrict__ row_nnz, const int64_t* __restrict__ crp,
                     int32_t* __restrict__ ccol, double* __restrict__ cval,
-                    unsigned long long* __restrict__ products, const uint8_t* __restrict__ skip) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                    unsigned long long* __restrict__ products, const uint8_t* __restrict__ skip,
+                    unsigned long long* __restrict__ next) {
+    const int lane = threadIdx.x & 31;
     const unsigned long long below0 = (1ull << lane) - 1ull, below1 = (1ull << (lane + 32)) - 1ull;
     unsigned long long prod = 0;
-    for (int64_t r = blockIdx.x * int64_t{NARROW_WARPS} + warp; r < n;
-         r += int64_t{gridDim.x} * NARROW_WARPS) {
-        if (skip && skip[r]) continue;  // warp-uniform (rows of a cluster tile)
-        const int64_t row = rb + r;
+    // numeric: rows handed out dynamically in pairs (hub rows first, as they
+    // come first), so a warp that drew a hub row does not also carry a fixed
+    // share of the rest; symbolic (cheap per row): a static grid stride
+    constexpr int64_t G = 2;
+    const int64_t nwarps = int64_t{gridDim.x} * NARROW_WARPS;
+    int64_t r = NUMERIC ? 0 : blockIdx.x * int64_t{NARROW_WARPS} + (threadIdx.x >> 5);
+    int64_t rend = NUMERIC ? 0 : n;
+    for (;;) {
+        if constexpr (NUMERIC) {
+            if (r >= rend) {
+                int64_t g = 0;
+                if (lane == 0)
+                    g = static_cast<int64_t>(atomicAdd(next, static_cast<unsigned long long>(G)));
+                g = __shfl_sync(0xffffffffu, g, 0);
+                if (g >= n) break;
+                r = g;
+                rend = ::min(n, g + G);
+            }
+        } else {
+            if (r >= n) break;
+        }
+        const int64_t r_ = r;
+        r += NUMERIC ? 1 : nwarps;
+        if (skip && skip[r_]) continue;  // warp-uniform (rows of a cluster tile)
+        const int64_t row = rb + r_;
         const int64_t rs = m.arp[row], re = m.arp[row + 1];
         unsigned long long touch = 0;
         double acc0 = 0.0, acc1 = 0.0;
@@ -1502,9 +1524,9 @@ __global__ void __launch_bounds__(NARROW_WARPS * 32)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) touch |= __shfl_xor_sync(0xffffffffu, touch, o);
         if (!NUMERIC) {
-            if (lane == 0) row_nnz[r] = __popcll(touch);
+            if (lane == 0) row_nnz[r_] = __popcll(touch);
         } else {
-            const int64_t pos = crp[r];
+            const int64_t pos = crp[r_];
             if ((touch >> lane) & 1ull) {
                 const int64_t o = pos + __popcll(touch & below0);
                 ccol[o] = lane;
@@ -1544,8 +1566,10 @@ static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, 
         const unsigned gm = static_cast<unsigned>(std::max<int64_t>(
             1, std::min<int64_t>(div_up(std::max<int64_t>(bnrows, 1), 256), int64_t{h->sm_count} * 8)));
         BSP_LAUNCH(h, row_mask64_kernel, gm, 256, 0, m.brp, m.bcol, bnrows, bmask.p);
+        DBuf<unsigned long long> nx(h, 1);
+        BSP_CUDA(cudaMemsetAsync(nx.p, 0, sizeof(unsigned long long), h->stream));
         BSP_LAUNCH_AS(h, "narrow64_symbolic", narrow64_kernel<false>, grid, NARROW_WARPS * 32, 0, m,
-                      bmask.p, rb, n, cnt.p, nullptr, nullptr, nullptr, prod.p, nullptr);
+                      bmask.p, rb, n, cnt.p, nullptr, nullptr, nullptr, prod.p, nullptr, nx.p);
     } else {
         BSP_LAUNCH_AS(h, "narrow_symbolic", ks, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, cnt.p,
                       nullptr, nullptr, nullptr, prod.p);
@@ -1559,12 +1583,16 @@ static void narrow_multiply(bsp_handle h, const Mats& m, int64_t rb, int64_t n, 
     h->stats.products = static_cast<int64_t>(read_scalar(h, prod.p));
     h->stats.nnz_out = nnz;
     ResultPayload pay(h, nnz);
-    if (m64)
+    if (m64) {
+        DBuf<unsigned long long> nx(h, 1);
+        BSP_CUDA(cudaMemsetAsync(nx.p, 0, sizeof(unsigned long long), h->stream));
         BSP_LAUNCH_AS(h, "narrow64_numeric", narrow64_kernel<true>, grid, NARROW_WARPS * 32, 0, m,
-                      bmask.p, rb, n, nullptr, rp.p, pay.col_idx(), pay.values(), nullptr, nullptr);
-    else
+                      bmask.p, rb, n, nullptr, rp.p, pay.col_idx(), pay.values(), nullptr, nullptr,
+                      nx.p);
+    } else {
         BSP_LAUNCH_AS(h, "narrow_numeric", kn, grid, NARROW_WARPS * 32, 0, m, rb, n, nc, nullptr,
                       rp.p, pay.col_idx(), pay.values(), nullptr);
+    }
     C->nrows = n;
     C->ncols = ncols;
     C->nnz = nnz;
@@ -1588,12 +1616,14 @@ void narrow64_rows(bsp_handle h, const Mats& m, const unsigned long long* mask, 
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
         1, std::min<int64_t>(div_up(std::max<int64_t>(n, 1), NARROW_WARPS),
                              int64_t{h->sm_count} * 32)));
+    DBuf<unsigned long long> nx(h, 1);
+    BSP_CUDA(cudaMemsetAsync(nx.p, 0, sizeof(unsigned long long), h->stream));
     if (crp == nullptr)
         BSP_LAUNCH_AS(h, "narrow64_symbolic", narrow64_kernel<false>, grid, NARROW_WARPS * 32, 0, m,
-                      mask, int64_t{0}, n, row_nnz, nullptr, nullptr, nullptr, products, skip);
+                      mask, int64_t{0}, n, row_nnz, nullptr, nullptr, nullptr, products, skip, nx.p);
     else
         BSP_LAUNCH_AS(h, "narrow64_numeric", narrow64_kernel<true>, grid, NARROW_WARPS * 32, 0, m,
-                      mask, int64_t{0}, n, nullptr, crp, ccol, cval, nullptr, skip);
+                      mask, int64_t{0}, n, nullptr, crp, ccol, cval, nullptr, skip, nx.p);
 }
 
 void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t rb, int64_t re,
