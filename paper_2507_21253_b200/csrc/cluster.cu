@@ -811,12 +811,17 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
             h->stats.nnz_out = nnz;
             h->stats.units[10] = acc;
             ResultPayload pay(h, nnz);
-            if (acc > 0)
+            // the cluster kernel on the side stream: the row kernel's tail (hub
+            // rows) leaves SMs idle that it fills (disjoint rows of C)
+            if (acc > 0) {
+                SideStream side(h);
                 BSP_LAUNCH_AS(h, "cluster_narrow64", cluster_narrow64_kernel,
                               grid_for(h, div_up(acc, CN_WARPS), 1), CN_WARPS * 32, 0, cm, bmask.p,
                               lists.p, acc, rp.p, pay.col_idx(), pay.values());
+            }
             narrow64_rows(h, m, bmask.p, n, skip.p, nullptr, rp.p, pay.col_idx(), pay.values(),
                           nullptr);
+            if (acc > 0) join_side(h);
             C->nrows = n;
             C->ncols = B->ncols;
             C->nnz = nnz;
