@@ -9,21 +9,26 @@
 //
 // Design:
 //  K0 products_kernel: per-row intermediate products P_i (row_upper_bound,
-//     spgemm.hpp:31-36) and the row's class (<= 128/512/2048/3072/4096
-//     products, or heavy).
+//     spgemm.hpp:31-36) and the row's class (<= 128/512/1024/2048/3072/4096
+//     products, or heavy); a warp per row.
 //  K1 bucket_kernel:   row ids grouped by class.
 //  K2 plan_count / plan_write: heavy rows are cut greedily into column
-//     windows of <= 3072 products (one 4096-column bin of more than 4096
+//     windows of <= 2048 products (one 4096-column bin of more than 4096
 //     products is a "dense" window), with per-(window, segment) start tables.
 //  K3 hash_count_kernel (symbolic) / esc_merge_kernel (numeric): one CTA
 //     per light row or sparse window (merge.cuh): the products are gathered
-//     into shared memory in (k, j) order with cp.async, stably sorted by
-//     column (merge of the presorted runs, CUB radix or MSD), and every run
-//     of equal columns is summed left to right from 0.0 -> bit-exact values,
-//     stored coalesced.
+//     into shared memory in (k, j) order with cp.async, sorted by column
+//     (counting sort with an expansion-index tie-break, else a stable merge
+//     of the presorted runs, CUB radix or MSD), and every run of equal
+//     columns is summed left to right from 0.0 -> bit-exact values, stored
+//     coalesced.
 //  K4 dense_window_kernel<NUMERIC>: dense windows with a smem accumulator of
-//     WD doubles + bitmap; products streamed in 4096-product batches in k
+//     WD doubles + bitmap; products streamed in 1024-product batches in k
 //     order, each batch stably sorted so per-column order is kept.
+//  K5 hashacc_kernel: duplicate-heavy light rows (products >= 2 x outputs)
+//     accumulated segment by segment in k order into a warp's smem hash.
+//  K6 narrow64_kernel / narrow_kernel: B with <= 64 / <= 256 columns, a
+//     warp per row with register / smem accumulators, no sort.
 //  The symbolic pass gives exact per-row counts (exact allocation, as the
 //  reference), then an int64 scan gives row_ptr.
 #include "esc.cuh"
