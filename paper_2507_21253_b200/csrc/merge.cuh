@@ -1,16 +1,18 @@
-// On-chip stable merge of presorted runs and hash-based distinct counting.
+// The ESC tile shared by the row, window and cluster kernels.
 //
-// Numeric (exact) tile = ESC with a MERGE sort instead of a radix sort: the
-// products of a tile are expanded into shared memory in (k ascending, j
-// ascending) order, i.e. as one sorted run per contributing B-row segment.
-// A bottom-up merge-path merge of adjacent runs (ties taken from the left
-// run, i.e. from the smaller k) sorts them by column while keeping equal
-// columns in ascending-k order, so the per-column sums are formed exactly
-// as the reference forms them (0.0 + p1 + p2 + ..., spgemm.hpp:92-97).
+// Numeric (exact) tile: the products of a tile are expanded into shared
+// memory in (k ascending, j ascending) order — one sorted run per
+// contributing B-row segment — and sorted by column with equal columns kept
+// in ascending k, so the per-column sums are formed exactly as the reference
+// forms them (0.0 + p1 + p2 + ..., spgemm.hpp:92-97).  The sort is chosen per
+// tile: a counting sort on the column's top bits with an expansion-index
+// tie-break (count_sort_tile), a bottom-up merge-path merge of the runs (ties
+// from the left run, i.e. the smaller k), an MSD counting sort for small
+// tiles, or a stable CUB block radix sort.
 //
-// Symbolic tile = distinct-column count through an open-addressed smem hash
-// (atomicCAS insert), the GPU form of HashAccumulator::insert_key
-// (hash_accumulator.hpp:48-54).
+// Symbolic tile (rowwise.cu) = distinct-column count through an open-addressed
+// smem hash (atomicCAS insert), the GPU form of HashAccumulator::insert_key
+// (hash_accumulator.hpp:48-54); col_hash below.
 #pragma once
 
 #include "esc.cuh"
