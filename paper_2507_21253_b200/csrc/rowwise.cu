@@ -494,10 +494,10 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
 
 constexpr int pow2_ceil(int x) { return x <= 1 ? 1 : 2 * pow2_ceil((x + 1) / 2); }
 
-template <int T, int CAPM, bool STAGED = true>
+template <int T, int CAPM, bool STAGED = true, int TSM = 2>
 struct HashShared {
-    static constexpr int TS = pow2_ceil(2 * CAPM);  // open-addressing slots (power of two)
-    int32_t table[TS];
+    static constexpr int TS = pow2_ceil(TSM * CAPM);  // open-addressing slots (power of two)
+    alignas(16) int32_t table[TS];
     int32_t stage[STAGED ? CAPM : 1];  // gathered columns of the current chunk
     typename cub::BlockReduce<int32_t, T>::TempStorage red;
     typename cub::BlockScan<int32_t, T>::TempStorage scan;
@@ -508,11 +508,11 @@ struct HashShared {
 // Distinct output columns of (row, [c0,c1)) with <= CAPM products.
 // STAGED: the chunk's columns are first gathered into smem with cp.async
 // (warp-contiguous, all loads in flight), then hashed from smem.
-template <int T, int CAPM, bool STAGED>
+template <int T, int CAPM, bool STAGED, int TSM = 2>
 __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __restrict__ ids,
                                                        const Window* __restrict__ wins,
                                                        OutCtx out) {
-    using S = HashShared<T, CAPM, STAGED>;
+    using S = HashShared<T, CAPM, STAGED, TSM>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S& s = *reinterpret_cast<S*>(smem_raw);
     const int tid = threadIdx.x;
@@ -541,7 +541,9 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         re = m.arp[row + 1];
     }
     const bool full = wins == nullptr;
-    for (int e = tid; e < TS; e += T) s.table[e] = -1;
+    static_assert(TS % (4 * T) == 0, "table init is int4-wide");
+    for (int e = 4 * tid; e < TS; e += 4 * T)
+        *reinterpret_cast<int4*>(&s.table[e]) = make_int4(-1, -1, -1, -1);
     int cnt = 0;
     for (int64_t pc = rs; pc < re; pc += T) {
         const int64_t p = pc + tid;
@@ -939,7 +941,24 @@ void launch_tile(bsp_handle h, const Mats& m, const int32_t* ids, int64_t n, con
             const char* e = std::getenv("BSP_HASH");
             return !(e && std::string(e) == "plain");
         }();
-        if (staged) {
+        // Table slots per product: 4 for heavy-row windows (fewer probe
+        // collisions, measured 3 ms faster on cfg5 than 2 at 5 instead of 8
+        // CTAs/SM); BSP_HTS / BSP_HTSL (light rows <= 2048 products) = 2 or 4.
+        static const int hts_win = [] {
+            const char* e = std::getenv("BSP_HTS");
+            return e ? std::atoi(e) : 4;
+        }();
+        static const int hts_light = [] {
+            const char* e = std::getenv("BSP_HTSL");
+            return e ? std::atoi(e) : 2;
+        }();
+        if (staged && CAPM <= 2048 && (wins ? hts_win : hts_light) == 4) {
+            using S = HashShared<T, CAPM, true, 4>;
+            auto k = hash_count_kernel<T, CAPM, true, 4>;
+            set_smem(k, sizeof(S));
+            BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(S), m, ids, wins,
+                          out);
+        } else if (staged) {
             using S = HashShared<T, CAPM, true>;
             auto k = hash_count_kernel<T, CAPM, true>;
             set_smem(k, sizeof(S));
