@@ -1,20 +1,25 @@
-"""Parity at BASELINE.json's full sizes.
+"""Parity at BASELINE.json's full sizes, pinned to the reference.
 
-The oracle finishes cfg1 and cfg2 at full size in seconds, so those are compared
-bit-for-bit (test_gpu_rowwise covers cfg1 at full size; cfg2 is here, row-wise and
-cluster-wise).  cfg3 (C ~285 GB, in 4 row ranges), cfg4 (1.5e9 products) and cfg5
-(1.2e10 products, 138 GB of C) are checked on the device through size-independent properties of C = A·A:
+cfg1 (test_gpu_rowwise) and cfg2 are compared bit-for-bit against the oracle at full
+size.  cfg4's whole C (1.49e9 products, 2.5e8 outputs) is compared bit-for-bit against
+the unmodified reference (`oracle/_ref`, OpenMP on every host core), row-wise and
+cluster-wise.  cfg5 (138 GB of C) and cfg3 (285 GB, produced in 4 row chunks) exceed
+the reference's int32 offsets, so they are pinned the way SURVEY 8(c) prescribes:
 
-- structure: row_ptr starts at 0, is non-decreasing, ends at nnz(C), and every
-  row's length equals the symbolic pass's count; the number of products equals
-  the pinned count of the seeded recipe;
-- sortedness: column indices strictly increase inside every row and lie in
-  [0, ncols) (the reference's sorted, duplicate-free rows, spgemm.hpp:98-104);
-- linearity: C·x = A·(A·x) for a seeded x in [0, 1).  All values of these
-  recipes are >= 0 except cfg4's off-diagonal -1, so the bound is taken against
-  |C|·|x|: |C·x - A·(A·x)| <= 1e-9 · (|C|·|x|) entrywise (fp64, summation
-  orders differ between the two sides; the kernels themselves are bit-exact).
+- every row's count against the reference's own `spgemm_symbolic` (spgemm.hpp:41-63);
+- row blocks cut out of the engine's FULL C (so int64 offsets past 2^31, the
+  start-table budget and the hub rows are the code paths under test) compared
+  bit-exactly with the reference's `spgemm_rowwise` on the same rows
+  (spgemm.hpp:70-106; each block's nnz(C) < 2^31): the block holding the row with the
+  most products (R-MAT hub rows; cfg3's dense windows), three product-weighted random
+  blocks and the last rows of the matrix;
+- plus size-independent properties of the whole C: sortedness and linearity
+  (C·x = A·(A·x) within 1e-9 · (|C|·|x|) entrywise; fp64 summation orders differ
+  between the two sides, the kernels themselves are bit-exact).
 """
+import os
+from types import SimpleNamespace
+
 import numpy as np
 import pytest
 import torch
@@ -61,9 +66,40 @@ def _spmv(rp, ci, v, x, absval=False):
     return y
 
 
-def _check_properties(engine, a, pinned_products, nchunks=1):
+def _blocks(prod, hub_budget, rand_budget, nrand, seed):
+    """Row blocks [r0, r1) for the row-block oracle: the block starting at the row with
+    the most products, `nrand` blocks starting at product-weighted random rows, and the
+    matrix's last rows; each grows until it holds about `budget` products."""
+    n = len(prod)
+    cs = np.concatenate([[0], np.cumsum(prod, dtype=np.int64)])
+
+    def grow(r0, budget):
+        r1 = int(np.searchsorted(cs, cs[r0] + budget, side="right")) - 1
+        return (r0, min(n, max(r0 + 1, r1)))
+
+    out = [grow(int(np.argmax(prod)), hub_budget)]
+    rng = np.random.default_rng(seed)
+    for _ in range(nrand):
+        t = int(rng.integers(0, int(cs[-1])))
+        out.append(grow(int(np.searchsorted(cs, t, side="right")) - 1, rand_budget))
+    r0 = max(0, int(np.searchsorted(cs, cs[-1] - rand_budget, side="left")) - 1)
+    out.append((r0, n))
+    return out
+
+
+def _host_block(rp, ci, v, lo, hi):
+    """Rows [lo, hi) of a device CSR (row_ptr int64 with absolute offsets), on the host."""
+    rps = rp[lo:hi + 1].cpu().numpy()
+    s, e = int(rps[0]), int(rps[-1])
+    return SimpleNamespace(nrows=hi - lo, row_ptr=rps - s, col_idx=ci[s:e].cpu().numpy(),
+                           values=v[s:e].cpu().numpy())
+
+
+def _check_properties(engine, a, pinned_products, nchunks=1, ref_counts=None, blocks=()):
     """C = A·A in `nchunks` row ranges (bsp_spgemm_rowwise_range, the cost split of
-    bsp_partition_rows), each checked and freed before the next (cfg3's C is 285 GB)."""
+    bsp_partition_rows), each checked and freed before the next (cfg3's C is 285 GB).
+    ref_counts: the reference's per-row output counts; blocks: row blocks compared
+    bit-exactly with the reference's spgemm_rowwise on the same rows."""
     dev = torch.device("cuda")
     rpA = torch.from_numpy(a.row_ptr).to(dev)
     ciA = torch.from_numpy(a.col_idx).to(dev)
@@ -71,12 +107,19 @@ def _check_properties(engine, a, pinned_products, nchunks=1):
     torch.cuda.synchronize()  # the engine runs on its own stream
     A = engine.view_torch(a.nrows, a.ncols, rpA, ciA, vA)
     assert engine.spgemm_products(A, A) == pinned_products
-    cnt = torch.from_numpy(engine.spgemm_symbolic(A, A)).to(dev)
+    sym = engine.spgemm_symbolic(A, A)
+    if ref_counts is not None:
+        bad = np.flatnonzero(sym != ref_counts)
+        assert bad.size == 0, f"symbolic counts differ from the reference at rows {bad[:8]}"
+    cnt = torch.from_numpy(sym).to(dev)
     g = torch.Generator(device=dev).manual_seed(2507)
     x = torch.rand(a.ncols, dtype=torch.float64, device=dev, generator=g)
     z = _spmv(rpA, ciA, vA, _spmv(rpA, ciA, vA, x))
     bounds = ([0, a.nrows] if nchunks == 1
               else [int(b) for b in engine.partition_rows(A, A, nchunks)])
+    # blocks must not straddle a chunk boundary
+    blocks = [(b0, min(b1, min(x for x in bounds if x > b0))) for b0, b1 in blocks]
+    checked = []
     total = 0
     for r0, r1 in zip(bounds[:-1], bounds[1:]):
         Cd = (engine.spgemm_rowwise(A, A) if nchunks == 1
@@ -96,6 +139,14 @@ def _check_properties(engine, a, pinned_products, nchunks=1):
             assert int(rp[0]) == 0 and int(rp[-1]) == nnz
             assert bool(((rp[1:] - rp[:-1]) >= 0).all())
             assert torch.equal(rp[1:] - rp[:-1], cnt[r0:r1])
+            # row blocks of this range against the reference, bit for bit
+            for b0, b1 in blocks:
+                if b0 < r0 or b1 > r1:
+                    continue
+                got = _host_block(rp, ci, v, b0 - r0, b1 - r0)
+                want = O.ref_spgemm_rowwise(a, a, b0, b1)
+                assert_csr_identical(got, want, f"rows [{b0},{b1}) vs the reference")
+                checked.append((b0, b1))
             # sortedness, chunk by chunk (a chunk boundary inside a row is
             # checked by overlapping chunks by one entry)
             for s in range(0, nnz, CHUNK):
@@ -117,7 +168,14 @@ def _check_properties(engine, a, pinned_products, nchunks=1):
             Cd.free()
             torch.cuda.synchronize()
             torch.cuda.empty_cache()
+    assert len(checked) == len(blocks)
     return total
+
+
+def _rows_products(a):
+    """Intermediate products per row of A·A (row_upper_bound, spgemm.hpp:31-36)."""
+    cs = np.concatenate([[0], np.cumsum(np.diff(a.row_ptr)[a.col_idx], dtype=np.int64)])
+    return cs[a.row_ptr[1:]] - cs[a.row_ptr[:-1]]
 
 
 def test_cfg2_full_rowwise_and_clusterwise_bit_exact(engine):
@@ -131,22 +189,44 @@ def test_cfg2_full_rowwise_and_clusterwise_bit_exact(engine):
     assert_csr_identical(engine.spgemm_clusterwise(Ac, A).download(), o, "cfg2 full cluster-wise")
 
 
-def test_cfg4_full_properties(engine):
-    """27-point stencil 128^3 (n = 2097152, randomly permuted), C = A·A."""
+def test_cfg4_full_bit_exact_vs_reference(engine):
+    """27-point stencil 128^3 (n = 2097152, randomly permuted): the whole C = A·A
+    (1.49e9 products) bit-for-bit against the unmodified reference, row-wise and
+    cluster-wise (hierarchical clusters; cluster_spgemm.hpp:103-171 keeps the
+    row-wise order, so the cluster path's C is the same bits)."""
     a = B.make_config(4)
-    p = int(np.sum(np.diff(a.row_ptr)[a.col_idx]))  # sum over A's entries of B's row lengths
-    _check_properties(engine, a, p)
+    want = O.ref_spgemm_rowwise(a, a)
+    assert want.col_idx.size == 254840104
+    A = engine.upload(a)
+    assert_csr_identical(engine.spgemm_rowwise(A, A).download(), want, "cfg4 full row-wise")
+    asg = engine.hierarchical_clusters(a)
+    Ac = engine.build_csr_cluster(A, asg)
+    assert_csr_identical(engine.spgemm_clusterwise(Ac, A).download(), want,
+                         "cfg4 full cluster-wise")
+    p = int(np.sum(np.diff(a.row_ptr)[a.col_idx]))
+    assert engine.spgemm_products(A, A) == p == 1489355288
 
 
-def test_cfg5_full_properties(engine):
-    """R-MAT 22 ef 8 (the bench workload): 11,943,554,182 products, 138 GB of C."""
+def test_cfg5_full_vs_reference(engine):
+    """R-MAT 22 ef 8 (the bench workload): 11,943,554,182 products, 138 GB of C.
+    Every row count vs the reference's spgemm_symbolic; the hub block, three random
+    blocks and the last rows (offsets ~1.15e10) of the full C bit-exact."""
     a = B.make_config(5)
-    assert _check_properties(engine, a, 11943554182) == 11522129996
+    ref_counts = O.ref_spgemm_symbolic(a, a)
+    assert int(ref_counts.sum()) == 11522129996
+    blocks = _blocks(_rows_products(a), 1.5e8, 4e7, 3, seed=5)
+    assert _check_properties(engine, a, 11943554182, ref_counts=ref_counts,
+                             blocks=blocks) == 11522129996
 
 
-def test_cfg3_full_properties_row_chunks(engine):
-    """R-MAT 20 ef 16 (n = 1048576): C (~285 GB) exceeds HBM, so it is produced and
-    checked in 4 row ranges of equal product cost, as the e2e path and cfg3 runs do."""
+def test_cfg3_full_vs_reference_row_chunks(engine):
+    """R-MAT 20 ef 16 (n = 1048576): C (~285 GB) exceeds HBM, so it is produced in 4
+    row ranges of equal product cost.  Every row count vs the reference's
+    spgemm_symbolic; the block at the row with the most products (22M products, dense
+    windows), three random blocks and the last rows bit-exact."""
     a = B.make_config(3)
     p = int(np.sum(np.diff(a.row_ptr)[a.col_idx]))
-    _check_properties(engine, a, p, nchunks=4)
+    ref_counts = O.ref_spgemm_symbolic(a, a)
+    blocks = _blocks(_rows_products(a), 1.2e8, 4e7, 3, seed=3)
+    total = _check_properties(engine, a, p, nchunks=4, ref_counts=ref_counts, blocks=blocks)
+    assert total == int(ref_counts.sum())
