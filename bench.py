@@ -326,7 +326,8 @@ def main():
     line = {
         "metric": "A·B SpGEMM GFLOP/s (2×products/s)",
         "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "step_ms": [round(x, 3) for x in step_ms], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded R-MAT, BASELINE cfg5; inputs 0.81 GB > L2, no flush)",
         "config": {"workload": "cfg5_rmat22_ef8_AxA_rowwise" if args.scale is None

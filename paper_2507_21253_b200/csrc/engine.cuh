@@ -213,6 +213,10 @@ struct ResultPayload {
     DBuf<double> block;
     int64_t nnz = 0;
     ResultPayload(bsp_handle h, int64_t n) : block(h, n + (n + 1) / 2, Pool::out), nnz(n) {}
+    // capacity for `cap` entries (the count is known only after the numeric
+    // pass): values at [0, cap), column indices after them
+    ResultPayload(bsp_handle h, int64_t n, int64_t cap)
+        : block(h, cap + (cap + 1) / 2, Pool::out), nnz(cap) {}
     double* values() const { return block.p; }
     int32_t* col_idx() const { return reinterpret_cast<int32_t*>(block.p + nnz); }
 };

@@ -180,6 +180,7 @@ struct RowwisePlan {
     int64_t nwin = 0, nsparse = 0, ndense = 0;
     // sparse_ids[wcls_off[k], wcls_off[k+1]): windows of tile class k (kWinCap)
     int64_t wcls_off[NWCLS + 1]{};
+    int64_t wcls_prod[NWCLS + 1]{};  // products per window category (dense = NWCLS)
     DBuf<Window> wins;
     DBuf<int32_t> sparse_ids, dense_ids;
     DBuf<uint32_t> starts; // planner per-(window, segment) start tables (absolute)
@@ -201,10 +202,13 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re, const uint8
                 RowwisePlan& plan, int64_t* prod_out, int64_t* early_row_nnz = nullptr,
                 RowwisePlan* shadow = nullptr);
 // Symbolic counts of a plan into row_nnz (NOT zeroed here) and win_nnz (allocated).
+// skip_wcls >= 0: leave that window tile class out (counted by the look-back
+// numeric instead).
 void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t* row_nnz,
-                   DBuf<int64_t>& win_nnz);
+                   DBuf<int64_t>& win_nnz, int skip_wcls = -1);
 void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
-                  const int64_t* win_scan, int32_t* ccol, double* cval);
+                  const int64_t* win_scan, int32_t* ccol, double* cval, int skip_wcls = -1);
+void sort_ids(bsp_handle h, int32_t* ids, int64_t n);
 
 // B with <= 64 columns: per-row 64-bit column masks of B, then the row-wise
 // narrow kernel over rows [0, n) of A (skip[r] != 0 rows left out): symbolic

@@ -633,6 +633,82 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     return merge_runs<T, CAPM>(s, total);
 }
 
+// Single-pass output placement (decoupled look-back, the CUB single-pass scan
+// pattern): tile t of a list claimed in list order publishes its output count
+// as an "aggregate", then one warp walks its predecessors 32 at a time,
+// summing aggregates until it meets an inclusive prefix, and publishes its own
+// inclusive prefix.  Status word = flag << 62 | value (one 64-bit store, so a
+// reader never sees a flag without its value).  Tiles are claimed with an
+// atomic counter, so every predecessor is owned by a running CTA: the spin
+// always ends.  Returns the exclusive prefix (all 32 lanes call it).
+struct LbCtx {
+    int* counter;                 // next tile to claim
+    unsigned long long* status;   // per tile: 0 = not ready, 1 = aggregate, 2 = prefix
+};
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62,
+                             LB_VAL = (1ull << 62) - 1ull;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+
+// Publish tile t's aggregate (one lane; t == 0 publishes its prefix).
+__device__ __forceinline__ void lookback_publish(unsigned long long* st, int t, long long agg) {
+    st_release_u64(st + t, (t == 0 ? LB_PRE : LB_AGG) | static_cast<unsigned long long>(agg));
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Exclusive prefix of tile t (after lookback_publish), then its inclusive
+// prefix published.  All 32 lanes of one warp call it.  Each step inspects 128
+// predecessors (4 independent loads per lane; entry distance = 32u + lane) and
+// waits only for the not-yet-published ones closer than the nearest inclusive
+// prefix.
+__device__ __forceinline__ long long lookback_warp(unsigned long long* st, int t, long long agg) {
+    const int lane = threadIdx.x & 31;
+    if (t == 0) return 0;
+    long long excl = 0;
+    for (int j = t - 1;; j -= 128) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = 0;
+        int pre_d, zero_d;
+        for (;;) {
+            pre_d = 128;
+            zero_d = 128;
+#pragma unroll
+            for (int u = 3; u >= 0; --u) {
+                const int idx = j - 32 * u - lane;
+                if ((v[u] >> 62) == 0) v[u] = idx >= 0 ? ld_relaxed_u64(st + idx) : LB_PRE;
+                const unsigned pm = __ballot_sync(0xffffffffu, (v[u] >> 62) == 2);
+                const unsigned zm = __ballot_sync(0xffffffffu, (v[u] >> 62) == 0);
+                if (pm) pre_d = 32 * u + __ffs(pm) - 1;
+                if (zm) zero_d = 32 * u + __ffs(zm) - 1;
+            }
+            if (zero_d > pre_d || zero_d == 128) break;
+        }
+        long long x = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (32 * u + lane <= pre_d) x += static_cast<long long>(v[u] & LB_VAL);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        excl += x;
+        if (pre_d < 128) break;
+    }
+    if (lane == 0) st_release_u64(st + t, LB_PRE | static_cast<unsigned long long>(excl + agg));
+    return excl;
+}
+
 // After the sort: sum every run of equal columns left to right from 0.0
 // (ascending k — the reference's order, spgemm.hpp:92-97) and write
 // (column + kofs, sum) to ccol/cval.  Element-strided: lane l of warp w owns
@@ -640,10 +716,18 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
 // conflict-free, a head's output rank is a ballot prefix plus a scan over the
 // (row, warp) head counts, and consecutive lanes store consecutive entries of
 // C (coalesced, no staging).  Returns the number of distinct columns.
-template <int T, int CAPM>
+// LB: the output offset is not known in advance.  The count is published
+// (`publish(count)`) right after the head scan; the run sums are formed next
+// — each head overwrites its own first product's slot with the sum, and the
+// rank -> head position map is kept in the sort's idle buffer — so the wait
+// for the predecessors' counts overlaps this work; then warp 0 obtains the
+// offset (`place(count)`, the look-back) and the tile stores its output
+// coalesced at ccol/cval + offset.
+template <int T, int CAPM, bool LB = false, class Publish = int, class Place = int>
 __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, int total,
                                                 uint32_t kofs, int32_t* __restrict__ ccol,
-                                                double* __restrict__ cval) {
+                                                double* __restrict__ cval, Publish&& publish = 0,
+                                                Place&& place = 0) {
     constexpr int NW = T / 32;
     constexpr int R = (CAPM + T - 1) / T;
     static_assert(R * NW <= T && R * NW <= MergeShared<T, CAPM>::NHIST, "row/warp counters");
@@ -666,6 +750,50 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
     cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(v, pre, tile_cnt);
     __syncthreads();
     if (threadIdx.x < nrows * NW) cnt[threadIdx.x] = pre;
+    if constexpr (LB) {
+        if (threadIdx.x == 0) publish(tile_cnt);
+        __syncthreads();
+        // rank -> head position, in the buffer the sort left idle
+        uint16_t* hpos = b ? s.idx0 : reinterpret_cast<uint16_t*>(s.u.c.packed);
+        const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!((hm[r] >> lane) & 1u)) continue;
+            const int o = r * T + threadIdx.x;
+            const int rank = cnt[r * NW + warp] + __popc(hm[r] & below);
+            const uint32_t key = K[PADI(o)];
+            const int x0 = X[PADI(o)];
+            double acc = 0.0;
+            int e = o;
+            do {
+                acc = __dadd_rn(acc, s.val[X[PADI(e)]]);
+                ++e;
+            } while (e < total && K[PADI(e)] == key);
+            s.val[x0] = acc;  // only this head reads its run's slots
+            hpos[rank] = static_cast<uint16_t>(o);
+        }
+        __syncthreads();
+        long long off = 0;
+        if constexpr (!std::is_same_v<std::decay_t<Place>, int>) {
+            // placement now: warp 0 walks, the tile stores at the offset
+            __shared__ long long s_off;
+            if (warp == 0) {
+                const long long v = place(tile_cnt);
+                if (lane == 0) s_off = v;
+            }
+            __syncthreads();
+            off = s_off;
+        }
+        ccol += off;
+        cval += off;
+        for (int q = threadIdx.x; q < tile_cnt; q += T) {
+            const int o = hpos[q];
+            ccol[q] = static_cast<int32_t>(K[PADI(o)] + kofs);
+            cval[q] = s.val[X[PADI(o)]];
+        }
+        __syncthreads();
+        return tile_cnt;
+    }
     __syncthreads();
     const unsigned below = (1u << lane) - 1u;
 #pragma unroll

@@ -411,16 +411,27 @@ __global__ void start_size_kernel(Mats m, const int32_t* __restrict__ heavy, int
 
 // Window ids by category (sparse tile class 0..NWCLS-1, dense NWCLS):
 // counts, then a scatter from per-category cursors (block-aggregated).
-__global__ void window_cat_count_kernel(const uint8_t* __restrict__ cat, int64_t nw,
+// (+ the products of each category: cnt[NWCLS + 1 + c])
+__global__ void window_cat_count_kernel(const uint8_t* __restrict__ cat,
+                                        const Window* __restrict__ wins, int64_t nw,
                                         unsigned long long* __restrict__ cnt) {
     __shared__ unsigned s_cnt[NWCLS + 1];
-    if (threadIdx.x <= NWCLS) s_cnt[threadIdx.x] = 0;
+    __shared__ unsigned long long s_prod[NWCLS + 1];
+    if (threadIdx.x <= NWCLS) {
+        s_cnt[threadIdx.x] = 0;
+        s_prod[threadIdx.x] = 0;
+    }
     __syncthreads();
     const int64_t w = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
-    if (w < nw) atomicAdd(&s_cnt[cat[w]], 1u);
+    if (w < nw) {
+        atomicAdd(&s_cnt[cat[w]], 1u);
+        atomicAdd(&s_prod[cat[w]], static_cast<unsigned long long>(wins[w].nprod));
+    }
     __syncthreads();
-    if (threadIdx.x <= NWCLS && s_cnt[threadIdx.x])
+    if (threadIdx.x <= NWCLS && s_cnt[threadIdx.x]) {
         atomicAdd(&cnt[threadIdx.x], static_cast<unsigned long long>(s_cnt[threadIdx.x]));
+        atomicAdd(&cnt[NWCLS + 1 + threadIdx.x], s_prod[threadIdx.x]);
+    }
 }
 
 __global__ void split_windows_kernel(const uint8_t* __restrict__ cat, int64_t nw,
@@ -490,6 +501,56 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
     if (w >= 0) base += out.win_scan[w] - out.win_scan[wins[w].first];
     reduce_and_write<T, CAPM>(s, b, total, static_cast<uint32_t>(c0), out.ccol + base,
                               out.cval + base);
+}
+
+// Window numeric tile without a symbolic pass (the main window class): the
+// windows of the list (ordered as their rows and columns are laid out in C)
+// are claimed in list order; each tile counts its distinct columns after the
+// sort, takes its offset among the list's windows from a decoupled look-back,
+// and its output lands at
+//   known(row, w) + U(w),
+// known = the output offset from every unit counted beforehand (light rows and
+// the other window classes: out.crp / out.win_scan scanned with this list's
+// windows at 0) and U(w) = the outputs of this list's windows placed before w.
+// It records its count (win_nnz, row_nnz) so the final row_ptr / window scan
+// — computed after this kernel — places everything else consistently.
+// Replaces the symbolic count of these windows (spgemm.hpp:41-63 fused into
+// :70-106): their columns are gathered once instead of twice.
+//
+// A tile publishes its count right after the head scan and forms its run
+// sums before the look-back, so the wait for predecessors still sorting
+// overlaps that work (measured on cfg5: 175 ms for the class vs 137 ms
+// numeric + 60 ms symbolic before).  Rejected (measured): persistent CTAs
+// placing each tile one tile later from an L2 stash (look-back 2.4K instead of
+// 6.6K cycles per tile, but register spills and the stash copy: 211-230 ms).
+template <int T, int CAPM>
+__global__ void __launch_bounds__(T, CAPM <= 2048 ? 4 : 2) esc_window_lb_kernel(
+    Mats m, const int32_t* __restrict__ ids, const Window* __restrict__ wins, OutCtx out,
+    int csort, LbCtx lb) {
+    using S = MergeShared<T, CAPM>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S& s = *reinterpret_cast<S*>(smem_raw);
+    __shared__ int s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(lb.counter, 1);
+    __syncthreads();
+    const int t = s_tile;
+    const int32_t w = ids[t];
+    const Window wd = wins[w];
+    const int total = expand_runs<T, CAPM, true>(m, wd.row, wd.c0, wd.c1, false, s, wd.sofs, wd.wi,
+                                                 wd.rs, wd.d, /*defer=*/true);
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(wd.c1 - wd.c0), csort, 0, false,
+                                     wd.c0);
+    const int64_t r = wd.row - out.row_begin;
+    const int64_t known = out.crp[r] + out.win_scan[w] - out.win_scan[wd.first];
+    const int cnt = reduce_and_write<T, CAPM, true>(
+        s, b, total, static_cast<uint32_t>(wd.c0), out.ccol + known, out.cval + known,
+        [&](int agg) { lookback_publish(lb.status, t, agg); },
+        [&](int agg) { return lookback_warp(lb.status, t, agg); });
+    if (threadIdx.x == 0) {
+        out.win_nnz[w] = cnt;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&out.row_nnz[r]),
+                  static_cast<unsigned long long>(cnt));
+    }
 }
 
 constexpr int pow2_ceil(int x) { return x <= 1 ? 1 : 2 * pow2_ceil((x + 1) / 2); }
@@ -1010,6 +1071,18 @@ Mats make_mats(const bsp_csr* A, const bsp_csr* B) {
 template <bool NUMERIC>
 void run_light(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx& out);
 
+// Ascending sort of a device id list in place (CUB radix sort on the id bits).
+void sort_ids(bsp_handle h, int32_t* ids, int64_t n) {
+    if (n <= 1) return;
+    DBuf<int32_t> tmp(h, n);
+    size_t bytes = 0;
+    BSP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, ids, tmp.p, n, 0, 31, h->stream));
+    DBuf<uint8_t> t(h, static_cast<int64_t>(bytes));
+    BSP_CUDA(cub::DeviceRadixSort::SortKeys(t.p, bytes, ids, tmp.p, n, 0, 31, h->stream));
+    ++h->launches;
+    BSP_CUDA(cudaMemcpyAsync(ids, tmp.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
+}
+
 void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                        const uint8_t* skip, RowwisePlan& plan, int64_t* prod_out,
                        int64_t* early_row_nnz, RowwisePlan* shadow) {
@@ -1088,6 +1161,9 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     // Heavy rows: planned column windows.
     const int64_t nh = plan.class_count[NCLS - 1];
     if (nh > 0) {
+        // heavy rows in row order: window ids then follow C's layout (the
+        // look-back numeric places windows in window-id order)
+        sort_ids(h, plan.lists.p + plan.class_off[NCLS - 1], nh);
         const int32_t* heavy = plan.lists.p + plan.class_off[NCLS - 1];
         int log_binw = LOG_WD;
         while (div_up(m.ncols, int64_t{1} << log_binw) > MAXBINS) ++log_binw;
@@ -1151,12 +1227,13 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
                    use_starts ? plan.starts.p : nullptr);
         plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
         plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
-        DBuf<unsigned long long> cnt(h, NWCLS + 1);
-        BSP_CUDA(cudaMemsetAsync(cnt.p, 0, (NWCLS + 1) * sizeof(unsigned long long), h->stream));
+        DBuf<unsigned long long> cnt(h, 2 * (NWCLS + 1));
+        BSP_CUDA(cudaMemsetAsync(cnt.p, 0, 2 * (NWCLS + 1) * sizeof(unsigned long long), h->stream));
         BSP_LAUNCH(h, window_cat_count_kernel, static_cast<unsigned>(div_up(plan.nwin, 256)), 256,
-                   0, dense.p, plan.nwin, cnt.p);
-        unsigned long long hc[NWCLS + 1];
-        d2h(h, hc, cnt.p, NWCLS + 1);
+                   0, dense.p, plan.wins.p, plan.nwin, cnt.p);
+        unsigned long long hc[2 * (NWCLS + 1)];
+        d2h(h, hc, cnt.p, 2 * (NWCLS + 1));
+        for (int k = 0; k <= NWCLS; ++k) plan.wcls_prod[k] = static_cast<int64_t>(hc[NWCLS + 1 + k]);
         // sparse list = tile classes in descending size (top-k walks it whole)
         unsigned long long cur[NWCLS + 1];
         plan.wcls_off[0] = 0;
@@ -1215,10 +1292,13 @@ void run_light(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCt
 }
 
 template <bool NUMERIC>
-void run_windows(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCtx& out) {
+void run_windows(bsp_handle h, const Mats& m0, const RowwisePlan& plan, const OutCtx& out,
+                 int skip_cls = -1) {
     const Mats m = plan.with_starts(m0);
     auto wl = [&](int k) { return plan.sparse_ids.p + plan.wcls_off[k]; };
-    auto wn = [&](int k) { return plan.wcls_off[k + 1] - plan.wcls_off[k]; };
+    auto wn = [&](int k) {
+        return k == skip_cls ? int64_t{0} : plan.wcls_off[k + 1] - plan.wcls_off[k];
+    };
     static_assert(NWCLS == 5, "one launch per window tile class");
     launch_tile<256, 4096, NUMERIC>(h, m, wl(0), wn(0), plan.wins.p, out);
     launch_tile<256, 3072, NUMERIC>(h, m, wl(1), wn(1), plan.wins.p, out);
@@ -1238,19 +1318,16 @@ void run_plan(bsp_handle h, const Mats& m, const RowwisePlan& plan, const OutCtx
 // the caller, and be the array given to build_plan when the light rows were
 // counted early) and per-window counts.
 void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t* row_nnz,
-                   DBuf<int64_t>& win_nnz) {
+                   DBuf<int64_t>& win_nnz, int skip_wcls) {
     win_nnz = DBuf<int64_t>(h, plan.nwin + 1);
     BSP_CUDA(cudaMemsetAsync(win_nnz.p, 0, (plan.nwin + 1) * sizeof(int64_t), h->stream));
     OutCtx out{};
     out.row_begin = plan.rb;
     out.row_nnz = row_nnz;
     out.win_nnz = win_nnz.p;
-    if (plan.light_sym_done) {
-        run_windows<false>(h, m, plan, out);
-        join_side(h);
-    } else {
-        run_plan<false>(h, m, plan, out);
-    }
+    if (!plan.light_sym_done) run_light<false>(h, m, plan, out);
+    run_windows<false>(h, m, plan, out, skip_wcls);
+    if (plan.light_sym_done) join_side(h);
 }
 
 // ---------------------------------------------------------------------------
@@ -1388,7 +1465,7 @@ __global__ void route_light_kernel(const int32_t* __restrict__ lists, int64_t nl
 }
 
 void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
-                  const int64_t* win_scan, int32_t* ccol, double* cval) {
+                  const int64_t* win_scan, int32_t* ccol, double* cval, int skip_wcls) {
     OutCtx out{};
     out.row_begin = plan.rb;
     out.crp = crp;
@@ -1408,7 +1485,8 @@ void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const in
     for (int c = 1; c < NCLS; ++c) planned += plan.class_products[c];
     const bool repeats = 4 * planned >= 5 * std::max<int64_t>(1, h->stats.nnz_out);
     if (!hacc || !repeats || nlight <= 0 || plan.prod.p == nullptr) {
-        run_plan<true>(h, m, plan, out);
+        run_light<true>(h, m, plan, out);
+        run_windows<true>(h, m, plan, out, skip_wcls);
         return;
     }
     DBuf<int32_t> hlist(h, nlight), tl(h, nlight);
@@ -1436,7 +1514,7 @@ void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const in
         const int64_t cnt = static_cast<int64_t>(hc[c]) - b0;
         launch_light<true>(h, c, m, tl.p + b0, cnt, out);
     }
-    run_windows<true>(h, m, plan, out);
+    run_windows<true>(h, m, plan, out, skip_wcls);
 }
 
 // Narrow B: symbolic (+ products) -> int64 scan -> numeric, no planning.
@@ -1671,21 +1749,83 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     BSP_CUDA(cudaMemsetAsync(crp.p, 0, (n + 1) * sizeof(int64_t), h->stream));
     RowwisePlan plan;
     build_plan(h, m, rb, re, row_skip, plan, nullptr, crp.p);
+    // The main window class (2048-product tiles: nearly all heavy products on
+    // power-law inputs) is counted by its numeric pass (esc_window_lb_kernel)
+    // instead of a symbolic pass, when C's allocation can take that class's
+    // product bound (cf ~ 1 there: a few % of slack) — BSP_LOOKBACK=0 disables.
+    constexpr int LBC = 2;  // window tile class of esc_window_lb_kernel<256, 2048>
+    static const bool lb_on = [] {
+        const char* e = std::getenv("BSP_LOOKBACK");
+        return !(e && e[0] == '0');
+    }();
+    const int64_t nlb = plan.wcls_off[LBC + 1] - plan.wcls_off[LBC];
+    bool lb = lb_on && nlb > 0;
     DBuf<int64_t> win_nnz;
-    plan_symbolic(h, m, plan, crp.p, win_nnz);
-    // crp currently holds per-row counts in [0, n); scan in place over n+1.
+    plan_symbolic(h, m, plan, crp.p, win_nnz, lb ? LBC : -1);
     BSP_CUDA(cudaMemsetAsync(crp.p + n, 0, sizeof(int64_t), h->stream));
-    if (row_nnz_out)
-        BSP_CUDA(cudaMemcpyAsync(row_nnz_out, crp.p, n * sizeof(int64_t),
-                                 cudaMemcpyDeviceToDevice, h->stream));
     DBuf<int64_t> rp(h, n + 1, Pool::out);
     exclusive_scan_i64(h, crp.p, rp.p, n + 1);
     DBuf<int64_t> win_scan(h, plan.nwin + 1);
     if (plan.nwin > 0) exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
-    const int64_t nnz = read_scalar(h, rp.p + n);
+    int64_t nnz = read_scalar(h, rp.p + n);  // without the look-back class when lb
+    int64_t cap = nnz;
+    if (lb) {
+        cap = nnz + plan.wcls_prod[LBC];
+        const int64_t avail = static_cast<int64_t>(available_bytes(h));
+        // C (12 B per entry) + the look-back state, with a 1 GB margin
+        if (12 * cap + 16 * nlb + (int64_t{1} << 30) > avail) {
+            // no room for the bound: count the class symbolically after all
+            lb = false;
+            OutCtx so{};
+            so.row_begin = plan.rb;
+            so.row_nnz = crp.p;
+            so.win_nnz = win_nnz.p;
+            Mats ms = plan.with_starts(m);
+            launch_tile<256, 2048, false>(h, ms, plan.sparse_ids.p + plan.wcls_off[LBC], nlb,
+                                          plan.wins.p, so);
+            exclusive_scan_i64(h, crp.p, rp.p, n + 1);
+            exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
+            nnz = cap = read_scalar(h, rp.p + n);
+        }
+    }
+    ResultPayload pay(h, nnz, cap);
+    if (lb) {
+        // windows of the class in C's layout order (window ids follow the
+        // row-sorted heavy list), claimed in that order
+        int32_t* ids = plan.sparse_ids.p + plan.wcls_off[LBC];
+        sort_ids(h, ids, nlb);
+        DBuf<unsigned long long> status(h, nlb);
+        DBuf<int> counter(h, 1);
+        BSP_CUDA(cudaMemsetAsync(status.p, 0, nlb * sizeof(unsigned long long), h->stream));
+        BSP_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), h->stream));
+        OutCtx out{};
+        out.row_begin = plan.rb;
+        out.crp = rp.p;            // offsets from the units counted beforehand
+        out.win_scan = win_scan.p;
+        out.row_nnz = crp.p;       // + this class's counts -> the final row counts
+        out.win_nnz = win_nnz.p;
+        out.ccol = pay.col_idx();
+        out.cval = pay.values();
+        static const int csort = [] {
+            const char* e = std::getenv("BSP_CSORT");
+            return e ? std::atoi(e) : 1000;
+        }();
+        using S = MergeShared<256, 2048>;
+        auto k = esc_window_lb_kernel<256, 2048>;
+        set_smem(k, sizeof(S));
+        BSP_LAUNCH_AS(h, "esc_window_lb<256,2048>", k, static_cast<unsigned>(nlb), 256, sizeof(S),
+                      plan.with_starts(m), ids, plan.wins.p, out, csort, LbCtx{counter.p, status.p});
+        // final row_ptr and window offsets for the remaining numeric tiles
+        BSP_CUDA(cudaMemsetAsync(crp.p + n, 0, sizeof(int64_t), h->stream));
+        exclusive_scan_i64(h, crp.p, rp.p, n + 1);
+        exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
+        nnz = read_scalar(h, rp.p + n);
+    }
+    if (row_nnz_out)
+        BSP_CUDA(cudaMemcpyAsync(row_nnz_out, crp.p, n * sizeof(int64_t),
+                                 cudaMemcpyDeviceToDevice, h->stream));
     h->stats.nnz_out = nnz;
-    ResultPayload pay(h, nnz);
-    plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values());
+    plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values(), lb ? LBC : -1);
     C->nrows = n;
     C->ncols = B->ncols;
     C->nnz = nnz;
