@@ -121,7 +121,8 @@ typedef struct {
                              most 128/512/1024/2048/3072/4096 products; 7 heavy), [8]
                              sparse windows, [9] dense windows, [10] cluster tiles */
     int32_t kernels_launched;
-    int32_t chunks;       /* row chunks (1 unless C exceeded the budget) */
+    int32_t chunks;       /* row chunks: bsp_spgemm_rowwise_host splits A's rows when C
+                             exceeds the device budget (half the free memory); 1 otherwise */
 } bsp_exec_stats;
 
 /* ------------------------------------------------------------------ */

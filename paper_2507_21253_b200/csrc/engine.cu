@@ -1,6 +1,9 @@
 // Handle, memory and transfer entry points of the C ABI, plus device-wide
 // scan helpers and the device transpose (reference csr.hpp:115-135).
 #include "engine.cuh"
+#include "esc.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -107,47 +110,31 @@ __global__ void col_count_kernel(const int32_t* __restrict__ col, int64_t nnz,
         atomicAdd(&cnt[col[p]], 1);
 }
 
-// Transpose, step 2: one warp per source row writes its entries at
-// deterministic positions.  pos(i,p) = t_row_ptr[c] + #{entries (i',c) with
-// i' < i}; computed from an atomic cursor would be nondeterministic, so the
-// destination rank is found by a counting pass over rows in order: we use a
-// per-column cursor that is advanced row by row in a second kernel below.
-__global__ void transpose_scatter_kernel(const int64_t* __restrict__ rp,
-                                         const int32_t* __restrict__ col,
-                                         const double* __restrict__ val, int64_t nrows,
-                                         int64_t* __restrict__ cursor,
-                                         int32_t* __restrict__ t_col, double* __restrict__ t_val) {
-    for (int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; i < nrows;
-         i += int64_t{gridDim.x} * blockDim.x) {
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-            const int32_t c = col[p];
-            const int64_t pos = atomicAdd(reinterpret_cast<unsigned long long*>(&cursor[c]), 1ull);
-            t_col[pos] = static_cast<int32_t>(i);
-            if (val) t_val[pos] = val[p];
+// Transpose, step 2: the row of every entry (a warp per source row).
+__global__ void entry_rows_kernel(const int64_t* __restrict__ rp, int64_t nrows,
+                                  int32_t* __restrict__ row_of, int32_t* __restrict__ iota) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = int64_t{gridDim.x} * (blockDim.x >> 5);
+    for (int64_t i = blockIdx.x * int64_t{blockDim.x >> 5} + (threadIdx.x >> 5); i < nrows; i += nw)
+        for (int64_t p = rp[i] + lane; p < rp[i + 1]; p += 32) {
+            row_of[p] = static_cast<int32_t>(i);
+            iota[p] = static_cast<int32_t>(p);
         }
-    }
 }
 
-// Rows of the transpose are then sorted by (row index) with their values;
-// each row of A^T is short on average, so one thread per row does an
-// insertion sort (long rows use a warp-cooperative odd-even pass).
-__global__ void sort_rows_kernel(const int64_t* __restrict__ rp, int64_t nrows,
-                                 int32_t* __restrict__ col, double* __restrict__ val) {
-    for (int64_t r = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; r < nrows;
-         r += int64_t{gridDim.x} * blockDim.x) {
-        const int64_t b = rp[r], e = rp[r + 1];
-        for (int64_t p = b + 1; p < e; ++p) {
-            const int32_t kc = col[p];
-            const double kv = val ? val[p] : 0.0;
-            int64_t q = p - 1;
-            while (q >= b && col[q] > kc) {
-                col[q + 1] = col[q];
-                if (val) val[q + 1] = val[q];
-                --q;
-            }
-            col[q + 1] = kc;
-            if (val) val[q + 1] = kv;
-        }
+// Transpose, step 3: after a STABLE radix sort of the entries by column
+// (entries enter in row-major order, so equal columns keep ascending rows),
+// gather the transposed entries: deterministic, rows of A^T sorted, no
+// per-row sort (a hub column costs no more than any other).
+__global__ void transpose_gather_kernel(const int32_t* __restrict__ perm, int64_t nnz,
+                                        const int32_t* __restrict__ row_of,
+                                        const double* __restrict__ val,
+                                        int32_t* __restrict__ t_col, double* __restrict__ t_val) {
+    for (int64_t q = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; q < nnz;
+         q += int64_t{gridDim.x} * blockDim.x) {
+        const int32_t p = perm[q];
+        t_col[q] = row_of[p];
+        if (val) t_val[q] = val[p];
     }
 }
 
@@ -451,18 +438,23 @@ int bsp_transpose(bsp_handle h, const bsp_csr* A, bsp_csr* out) {
         BSP_LAUNCH(h, col_count_kernel, grid, 256, 0, A->col_idx, nnz, cnt.p);
         DBuf<int64_t> rp(h, n + 1, Pool::out);
         exclusive_scan_i32_to_i64(h, cnt.p, rp.p, n + 1);
-        DBuf<int64_t> cursor(h, n + 1);
-        BSP_CUDA(cudaMemcpyAsync(cursor.p, rp.p, (n + 1) * sizeof(int64_t),
-                                 cudaMemcpyDeviceToDevice, h->stream));
+        require(nnz < (int64_t{1} << 31), "transpose: nnz must be < 2^31");
+        DBuf<int32_t> row_of(h, nnz), iota(h, nnz), perm(h, nnz), keys(h, nnz);
+        const int rgrid = static_cast<int>(
+            std::min<int64_t>(div_up(std::max<int64_t>(A->nrows, 1), 8), h->sm_count * 16));
+        BSP_LAUNCH(h, entry_rows_kernel, rgrid, 256, 0, A->row_ptr, A->nrows, row_of.p, iota.p);
+        const int bits = std::max(1, bit_length(static_cast<uint32_t>(std::max<int64_t>(n - 1, 1))));
+        size_t tmp = 0;
+        BSP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, A->col_idx, keys.p, iota.p, perm.p,
+                                                 nnz, 0, bits, h->stream));
+        DBuf<uint8_t> t(h, static_cast<int64_t>(tmp));
+        BSP_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, A->col_idx, keys.p, iota.p, perm.p, nnz,
+                                                 0, bits, h->stream));
+        ++h->launches;
         DBuf<int32_t> tc(h, nnz, Pool::out);
         DBuf<double> tv(h, nnz, Pool::out);
-        const int rgrid = static_cast<int>(
-            std::min<int64_t>(div_up(std::max<int64_t>(A->nrows, 1), 256), h->sm_count * 16));
-        BSP_LAUNCH(h, transpose_scatter_kernel, rgrid, 256, 0, A->row_ptr, A->col_idx, A->values,
-                   A->nrows, cursor.p, tc.p, tv.p);
-        const int sgrid = static_cast<int>(
-            std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 256), h->sm_count * 16));
-        BSP_LAUNCH(h, sort_rows_kernel, sgrid, 256, 0, rp.p, n, tc.p, tv.p);
+        BSP_LAUNCH(h, transpose_gather_kernel, grid, 256, 0, perm.p, nnz, row_of.p, A->values, tc.p,
+                   A->values ? tv.p : nullptr);
         out->nrows = n;
         out->ncols = A->nrows;
         out->nnz = nnz;

@@ -185,6 +185,17 @@ struct RowwisePlan {
     DBuf<int32_t> sparse_ids, dense_ids;
     DBuf<uint32_t> starts; // planner per-(window, segment) start tables (absolute)
     bool light_sym_done = false;  // light rows counted on the side stream
+    // Set while that side-stream work is not yet joined into the main stream:
+    // the destructor joins it before the plan's buffers are freed on the main
+    // stream, so an error between build_plan and plan_symbolic cannot free
+    // memory the side stream still reads.
+    mutable bsp_handle side_h = nullptr;
+    RowwisePlan() = default;
+    RowwisePlan(const RowwisePlan&) = delete;
+    RowwisePlan& operator=(const RowwisePlan&) = delete;
+    ~RowwisePlan() {
+        if (side_h) cudaStreamWaitEvent(side_h->stream, side_h->ev_join, 0);
+    }
     // Matrices as seen by the window kernels (start tables attached).
     Mats with_starts(const Mats& m) const {
         Mats r = m;

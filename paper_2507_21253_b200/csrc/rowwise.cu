@@ -41,6 +41,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 namespace bsp {
 
@@ -56,13 +57,15 @@ namespace {
 __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restrict__ prod,
                                 uint8_t* __restrict__ cls, const uint8_t* __restrict__ skip,
                                 int64_t* __restrict__ class_count,
-                                int64_t* __restrict__ class_products, int shadow) {
+                                int64_t* __restrict__ class_products, int shadow,
+                                unsigned long long* __restrict__ max_prod) {
     // shadow: skipped rows get their own classes NCLS + c (a second plan)
-    __shared__ unsigned long long s_cnt[2 * NCLS], s_prod[2 * NCLS];
+    __shared__ unsigned long long s_cnt[2 * NCLS], s_prod[2 * NCLS], s_max;
     if (threadIdx.x < 2 * NCLS) {
         s_cnt[threadIdx.x] = 0;
         s_prod[threadIdx.x] = 0;
     }
+    if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = int64_t{gridDim.x} * (blockDim.x >> 5);
@@ -88,9 +91,11 @@ __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restri
             cls[r] = static_cast<uint8_t>(c);
             atomicAdd(&s_cnt[c], 1ull);
             atomicAdd(&s_prod[c], static_cast<unsigned long long>(P));
+            atomicMax(&s_max, static_cast<unsigned long long>(P));
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0 && max_prod) atomicMax(max_prod, s_max);
     if (threadIdx.x < (shadow ? 2 * NCLS : NCLS)) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&class_count[threadIdx.x]), s_cnt[threadIdx.x]);
         atomicAdd(reinterpret_cast<unsigned long long*>(&class_products[threadIdx.x]),
@@ -1095,15 +1100,19 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     }
     const int ncl = shadow ? 2 * NCLS : NCLS;  // shadow: skipped rows' own classes
     DBuf<uint8_t> cls(h, n);
-    DBuf<int64_t> counters(h, 2 * ncl);
-    BSP_CUDA(cudaMemsetAsync(counters.p, 0, 2 * ncl * sizeof(int64_t), h->stream));
+    DBuf<int64_t> counters(h, 2 * ncl + 1);
+    BSP_CUDA(cudaMemsetAsync(counters.p, 0, (2 * ncl + 1) * sizeof(int64_t), h->stream));
     const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 8),
                                                         int64_t{h->sm_count} * 8));
     BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, rb, n, prod_out, cls.p, skip, counters.p,
-               counters.p + ncl, shadow ? 1 : 0);
-    int64_t hc[4 * NCLS];
-    d2h(h, hc, counters.p, 2 * ncl);
+               counters.p + ncl, shadow ? 1 : 0,
+               reinterpret_cast<unsigned long long*>(counters.p + 2 * ncl));
+    int64_t hc[4 * NCLS + 1];
+    d2h(h, hc, counters.p, 2 * ncl + 1);
     sync(h);
+    // the heavy-row planner keeps per-row product prefixes in 32 bits
+    require(hc[2 * ncl] < (int64_t{1} << 31) - 1,
+            "spgemm: a row with >= 2^31 intermediate products is not supported (split A's row)");
     if (shadow) {  // rows of the skip mask, planned apart (light rows only)
         require(hc[NCLS + NCLS - 1] == 0, "build_plan: shadow rows must be light");
         shadow->rb = rb;
@@ -1157,6 +1166,7 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         out.row_nnz = early_row_nnz;
         run_light<false>(h, m, plan, out);
         plan.light_sym_done = true;
+        plan.side_h = h;
     }
     // Heavy rows: planned column windows.
     const int64_t nh = plan.class_count[NCLS - 1];
@@ -1327,7 +1337,10 @@ void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t
     out.win_nnz = win_nnz.p;
     if (!plan.light_sym_done) run_light<false>(h, m, plan, out);
     run_windows<false>(h, m, plan, out, skip_wcls);
-    if (plan.light_sym_done) join_side(h);
+    if (plan.light_sym_done) {
+        join_side(h);
+        plan.side_h = nullptr;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1788,6 +1801,14 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
             nnz = cap = read_scalar(h, rp.p + n);
         }
     }
+    {
+        const int64_t avail = static_cast<int64_t>(available_bytes(h));
+        if (12 * cap > avail)
+            throw oom_error("spgemm_rowwise: C needs " + std::to_string(12 * cap >> 20) +
+                            " MiB, more than the " + std::to_string(avail >> 20) +
+                            " MiB of free device memory; use the host-output call "
+                            "(bsp_spgemm_rowwise_host chunks rows) or row ranges");
+    }
     ResultPayload pay(h, nnz, cap);
     if (lb) {
         // windows of the class in C's layout order (window ids follow the
@@ -1863,7 +1884,7 @@ int bsp_spgemm_products(bsp_handle h, const bsp_csr* A, const bsp_csr* B,
         const int grid = static_cast<int>(std::min<int64_t>(
             div_up(std::max<int64_t>(n, 1), 8), int64_t{h->sm_count} * 8));
         BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, 0, n, prod, cls.p, nullptr, counters.p,
-                   counters.p + NCLS, 0);
+                   counters.p + NCLS, 0, nullptr);
         int64_t hc[2 * NCLS];
         d2h(h, hc, counters.p, 2 * NCLS);
         sync(h);
@@ -1906,6 +1927,14 @@ int bsp_spgemm_rowwise_range(bsp_handle h, const bsp_csr* A, const bsp_csr* B, i
     });
 }
 
+// The reference-shaped call (spgemm.hpp:70: host CSR in, host CSR out).  When
+// C's bound (12 B per intermediate product) exceeds the device budget —
+// cfg3's C is ~285 GB, more than HBM — the exact per-row counts are taken
+// first (bsp_spgemm_symbolic), the host C is allocated exactly, and A is cut
+// into row chunks whose exact C fits the budget; each chunk is multiplied
+// (rowwise_multiply on the row range) and downloaded into its place.  Budget:
+// half of the device bytes available after the uploads (BSP_CHUNK_BYTES
+// overrides, for tests).
 int bsp_spgemm_rowwise_host(bsp_handle h, const bsp_host_csr* A, const bsp_host_csr* B,
                             bsp_host_csr* C) {
     return guarded([&] {
@@ -1916,25 +1945,85 @@ int bsp_spgemm_rowwise_host(bsp_handle h, const bsp_host_csr* A, const bsp_host_
         auto check = [](int rc) {
             if (rc != BSP_OK) throw std::runtime_error(bsp_last_error());
         };
+        struct Frees {
+            bsp_handle h;
+            bsp_csr *a, *b, *c;
+            bool alias;
+            ~Frees() {
+                bsp_csr_free(h, c);
+                bsp_csr_free(h, a);
+                if (!alias) bsp_csr_free(h, b);
+            }
+        };
         check(bsp_csr_upload(h, A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values, &dA));
         const bool alias = (A == B) || (A->row_ptr == B->row_ptr && A->col_idx == B->col_idx &&
                                         A->values == B->values);
+        Frees fr{h, &dA, &dB, &dC, alias};
         if (!alias)
             check(bsp_csr_upload(h, B->nrows, B->ncols, B->row_ptr, B->col_idx, B->values, &dB));
-        int rc = bsp_spgemm_rowwise(h, &dA, alias ? &dA : &dB, &dC);
-        if (rc == BSP_OK) {
+        const bsp_csr* pB = alias ? &dA : &dB;
+        const int64_t n = A->nrows;
+        int64_t products = 0;
+        check(bsp_spgemm_products(h, &dA, pB, nullptr, &products));
+        const char* fe = std::getenv("BSP_CHUNK_BYTES");  // per call (tests set it)
+        const int64_t forced = fe ? std::atoll(fe) : int64_t{0};
+        const int64_t budget =
+            forced > 0 ? forced : static_cast<int64_t>(available_bytes(h)) / 2;
+        if (12 * products + 8 * (n + 1) <= budget) {
+            // one multiply (the bound fits)
+            check(bsp_spgemm_rowwise(h, &dA, pB, &dC));
             C->nrows = dC.nrows;
             C->ncols = dC.ncols;
             C->nnz = dC.nnz;
             C->row_ptr = host_malloc<int64_t>(dC.nrows + 1);
             C->col_idx = host_malloc<int32_t>(dC.nnz);
             C->values = host_malloc<double>(dC.nnz);
-            rc = bsp_csr_download(h, &dC, C->row_ptr, C->col_idx, C->values);
+            check(bsp_csr_download(h, &dC, C->row_ptr, C->col_idx, C->values));
+            return;
         }
-        bsp_csr_free(h, &dC);
-        bsp_csr_free(h, &dA);
-        if (!alias) bsp_csr_free(h, &dB);
-        check(rc);
+        // exact counts -> exact host C -> row chunks of <= budget bytes
+        std::vector<int64_t> rp(n + 1, 0);
+        {
+            DBuf<int64_t> cnt(h, std::max<int64_t>(n, 1));
+            check(bsp_spgemm_symbolic(h, &dA, pB, cnt.p));
+            d2h(h, rp.data() + 1, cnt.p, n);
+            sync(h);
+        }
+        for (int64_t i = 0; i < n; ++i) rp[i + 1] += rp[i];
+        const int64_t nnz = rp[n];
+        int64_t* hrp = host_malloc<int64_t>(n + 1);
+        int32_t* hci = host_malloc<int32_t>(nnz);
+        double* hv = host_malloc<double>(nnz);
+        std::memcpy(hrp, rp.data(), (n + 1) * sizeof(int64_t));
+        C->nrows = n;
+        C->ncols = B->ncols;
+        C->nnz = nnz;
+        C->row_ptr = hrp;
+        C->col_idx = hci;
+        C->values = hv;
+        int32_t chunks = 0;
+        int64_t products_done = 0;
+        for (int64_t r0 = 0; r0 < n;) {
+            int64_t r1 = r0 + 1;
+            while (r1 < n && 12 * (rp[r1 + 1] - rp[r0]) + 8 * (r1 + 1 - r0) <= budget) ++r1;
+            rowwise_multiply(h, &dA, pB, r0, r1, &dC, nullptr, nullptr);
+            products_done += h->stats.products;
+            require(dC.nnz == rp[r1] - rp[r0], "spgemm_rowwise_host: chunk count mismatch");
+            if (dC.nnz > 0) {
+                BSP_CUDA(cudaMemcpyAsync(hci + rp[r0], dC.col_idx, dC.nnz * sizeof(int32_t),
+                                         cudaMemcpyDeviceToHost, h->stream));
+                BSP_CUDA(cudaMemcpyAsync(hv + rp[r0], dC.values, dC.nnz * sizeof(double),
+                                         cudaMemcpyDeviceToHost, h->stream));
+            }
+            sync(h);
+            bsp_csr_free(h, &dC);
+            dC = bsp_csr{};
+            ++chunks;
+            r0 = r1;
+        }
+        h->stats.products = products_done;
+        h->stats.nnz_out = nnz;
+        h->stats.chunks = chunks;
     });
 }
 

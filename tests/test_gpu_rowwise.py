@@ -147,6 +147,25 @@ def test_host_buffer_entry_point(engine):
     assert_csr_identical(c, O.spgemm_rowwise(a, a), "host entry")
 
 
+def test_host_entry_point_chunks_rows_when_c_exceeds_budget(engine, monkeypatch):
+    """When C's bound exceeds the device budget (cfg3: ~285 GB), the reference-shaped
+    host call splits A's rows into chunks itself (exact counts first, each chunk's C
+    downloaded into place).  A small forced budget exercises that path: same bits as
+    the oracle, several chunks reported, heavy (windowed) rows included."""
+    a = B.make_config(5, 14)
+    want = O.spgemm_rowwise(a, a)
+    monkeypatch.setenv("BSP_CHUNK_BYTES", str(4 << 20))
+    c = engine.spgemm_rowwise_host(a, a)
+    st = engine.exec_stats()
+    assert st["chunks"] > 4, st
+    assert st["nnz_out"] == want.col_idx.size
+    assert_csr_identical(c, want, "chunked host entry")
+    monkeypatch.delenv("BSP_CHUNK_BYTES")
+    c1 = engine.spgemm_rowwise_host(a, a)
+    assert engine.exec_stats()["chunks"] == 1
+    assert_csr_identical(c1, want, "unchunked host entry")
+
+
 def test_heavy_rows_over_empty_b_rows(engine):
     """Heavy rows (windowed) whose segments include empty B rows — the shape
     of A x frontier operands: every start-table entry must still be filled."""
@@ -293,3 +312,14 @@ def test_hash_accumulator_output_bound(engine, nout):
     engine.profile(False)
     assert_csr_identical(c, O.spgemm_rowwise(a, b), f"{nout} outputs")
     assert "hashacc_kernel" in prof  # rows with fewer outputs are routed in every case
+
+
+@pytest.mark.parametrize("cfg,scale", [(5, 14), (2, 512), (4, 16)])
+def test_device_transpose_matches_host(engine, cfg, scale):
+    """bsp_transpose (csr.hpp:115-135): a stable radix sort of the entries by column,
+    so rows of A^T come out sorted and identical to the host counting-sort transpose,
+    hub columns (R-MAT) and unsymmetric patterns (cfg2) included."""
+    a = B.make_config(cfg, scale)
+    want = B.transpose(a)
+    got = engine.transpose(engine.upload(a)).download()
+    assert_csr_identical(got, want, f"transpose cfg{cfg}")
