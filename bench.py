@@ -111,53 +111,127 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-def cpu_reference_sample(a, stride: int, offset: int, threads: int):
-    """Reference row-wise SpGEMM (oracle/_ref) on the strided row sample
-    {offset, offset+stride, ...} of A against the full B = A.  Returns
-    (seconds, products in the sample)."""
+# The workload (BASELINE cfg5), shared by both arms.  The reference arm builds
+# its input with the oracle's C restatement of the generator (oracle/gen.c,
+# pinned bit-for-bit to the product's in tests/test_oracle.py), so that
+# process never loads the product library.
+CFG5 = dict(scale=22, ef=8, a=0.45, b=0.22, c=0.22, seed=5)
+PINNED_NNZ_C = {22: 11522129996}  # nnz(C) of cfg5, pinned by tests/test_gpu_fullsize.py
+
+
+def workload_config(n, nnz_a, products, nnz_c, world, scale):
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    return {"workload": "cfg5_rmat22_ef8_AxA_rowwise" if scale is None
+            else f"rmat{scale}_ef8_AxA_rowwise",
+            "n": n, "nnz_a": nnz_a, "products": products, "nnz_c": nnz_c,
+            "parallelism": f"row-shard x{world}", "l2": "inputs larger than L2"}
+
+
+def row_products(a):
+    """Intermediate products per row of A·A (row_upper_bound, spgemm.hpp:31-36)."""
+    cs = np.concatenate([[0], np.cumsum(np.diff(a.row_ptr)[a.col_idx], dtype=np.int64)])
+    return cs[a.row_ptr[1:]] - cs[a.row_ptr[:-1]]
+
+
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def sub_rows(a, rows):
+    """The rows `rows` of A as a CSR (the reference-side sample operand)."""
     import oracle as O
 
-    rows = np.arange(offset, a.nrows, stride, dtype=np.int64)
+    rows = np.asarray(rows, np.int64)
     lens = np.diff(a.row_ptr)[rows]
     rp = np.zeros(rows.size + 1, np.int64)
     rp[1:] = np.cumsum(lens)
-    idx = np.concatenate([np.arange(a.row_ptr[r], a.row_ptr[r + 1]) for r in rows]) \
-        if rows.size else np.zeros(0, np.int64)
-    sub = O.Csr(rows.size, a.ncols, rp, a.col_idx[idx], a.values[idx])
-    blen = np.diff(a.row_ptr)
-    products = int(blen[sub.col_idx].sum())
-    t0 = time.perf_counter()
-    O.ref_spgemm_rowwise(sub, a, threads=threads)
-    return time.perf_counter() - t0, products
+    idx = (np.concatenate([np.arange(a.row_ptr[r], a.row_ptr[r + 1]) for r in rows])
+           if rows.size else np.zeros(0, np.int64))
+    return O.Csr(rows.size, a.ncols, rp, a.col_idx[idx], a.values[idx])
 
 
-def run_reference(args, a, rank: int):
+def ref_rowwise_samples(a, stride, offsets, threads):
+    """The unmodified reference's spgemm_rowwise (oracle/_ref, OpenMP on `threads`
+    cores) on strided row samples {o, o+stride, ...} of A against the full B = A.
+    Operands are converted to the reference's own types outside the timed call;
+    only spgemm_rowwise is timed.  Returns [(seconds, products)] per offset."""
     import oracle as O
 
-    cfg = {"workload": "cfg5_rmat22_ef8_AxA_rowwise", "matrix": "R-MAT s22 ef8 (0.45,0.22,0.22)",
-           "n": a.nrows, "nnz_a": a.nnz()}
+    bref = O.RefCsr(a)
+    blen = np.diff(a.row_ptr)
+    out = []
+    for off in offsets:
+        sub = sub_rows(a, np.arange(off, a.nrows, stride, dtype=np.int64))
+        aref = O.RefCsr(sub)
+        secs, _ = O.ref_time_rowwise(aref, bref, threads)
+        out.append((secs, int(blen[sub.col_idx].sum())))
+        del aref
+    return out
+
+
+def ref_clusterwise_sample(a, cluster_ptr, rows, stride, threads):
+    """The reference's row-wise and cluster-wise paths (bench.hpp:176-193) on the
+    same rows: every `stride`-th cluster of the assignment (its rows, in cluster
+    order), B = full A; build_csr_cluster outside the timing.  Returns (row-wise s,
+    cluster-wise s, products, clusters, rows)."""
+    import oracle as O
+
+    cp = np.asarray(cluster_ptr, np.int64)
+    sel = np.arange(0, cp.size - 1, stride)
+    lens = cp[sel + 1] - cp[sel]
+    sptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    srows = np.concatenate([rows[cp[c]:cp[c + 1]] for c in sel]).astype(np.int64)
+    sub = sub_rows(a, srows)  # sample rows, renumbered 0..R-1 in cluster order
+    bref = O.RefCsr(a)
+    aref = O.RefCsr(sub)
+    acl = O.RefCluster(aref, sptr, np.arange(srows.size, dtype=np.int32))
+    t_row, _ = O.ref_time_rowwise(aref, bref, threads)
+    t_cl, _ = O.ref_time_clusterwise(acl, bref, threads)
+    prods = int(np.diff(a.row_ptr)[sub.col_idx].sum())
+    return t_row, t_cl, prods, int(sel.size), int(srows.size)
+
+
+def run_reference(args, world: int):
+    """--impl reference: the reference's own CPU row-wise SpGEMM (oracle/_ref, the
+    unmodified headers) on the host cores, on this workload — each step a bounded
+    sample (1/stride of A's rows against the full B = A, a different offset per
+    step), the throughput being products / time over the timed steps."""
+    import oracle as O
+
     if not O.have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
+    scale = CFG5["scale"] if args.scale is None else args.scale
+    a = O.gen_rmat(scale, CFG5["ef"], CFG5["a"], CFG5["b"], CFG5["c"], CFG5["seed"])
+    products = int(row_products(a).sum())
+    nnz_c = PINNED_NNZ_C.get(scale)
+    if nnz_c is None:
+        nnz_c = int(O.ref_spgemm_symbolic(a, a).sum())
     threads = os.cpu_count() or 1
     stride = args.ref_stride
-    vals = []
-    secs, prods = 0.0, 0
-    for s in range(args.warmup + args.steps):
-        t, p = cpu_reference_sample(a, stride, s % stride, threads)
-        if s >= args.warmup:
-            vals.append(2.0 * p / t / 1e9)
-            secs += t
-            prods += p
+    res = ref_rowwise_samples(a, stride, [s % stride for s in range(args.warmup + args.steps)],
+                              threads)[args.warmup:]
+    secs = sum(t for t, _ in res)
+    prods = sum(p for _, p in res)
     value = 2.0 * prods / secs / 1e9
+    sample = (f"per step 1/{stride} of A's rows (i = s mod {stride}, step s) x full B = A; "
+              f"{prods} products in {secs:.2f} s over {args.steps} steps; only "
+              f"spgemm_rowwise timed; {cpu_model()}, {threads} threads")
     line = {
         "impl": "reference", "metric": "A·B SpGEMM GFLOP/s (2×products/s)", "value": value,
-        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT, BASELINE cfg5)",
-        "config": dict(cfg, sample=f"rows i = s mod {stride} per step (1/{stride} of rows)"),
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded R-MAT, BASELINE cfg5; inputs 0.81 GB > L2, no flush)",
+        "config": workload_config(a.nrows, int(a.row_ptr[-1]), products, nnz_c, world, args.scale),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                         "sample": f"1/{stride} strided row sample per step, B = full A"},
+                         "cpu": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -191,14 +265,15 @@ def main():
     if shared_gpu:
         local = 0
 
-    import paper_2507_21253_b200 as B
-
     if args.impl == "reference":
         if rank != 0:
             return
-        a = B.make_config(CFG, args.scale)
-        run_reference(args, a, rank)
+        os.environ.setdefault("OMP_PROC_BIND", "spread")
+        os.environ.setdefault("OMP_PLACES", "cores")
+        run_reference(args, world)
         return
+
+    import paper_2507_21253_b200 as B
 
     import torch
 
@@ -330,10 +405,7 @@ def main():
         "step_ms": [round(x, 3) for x in step_ms], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded R-MAT, BASELINE cfg5; inputs 0.81 GB > L2, no flush)",
-        "config": {"workload": "cfg5_rmat22_ef8_AxA_rowwise" if args.scale is None
-                   else f"rmat{args.scale}_ef8_AxA_rowwise",
-                   "n": n, "nnz_a": nnz, "products": total_products, "nnz_c": nnz_c,
-                   "parallelism": f"row-shard x{world}", "l2": "inputs larger than L2"},
+        "config": workload_config(n, nnz, total_products, nnz_c, world, args.scale),
         "gpu_launches": launches,
         "wall_ms_per_step": 1e3 * t_wall / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
@@ -352,12 +424,32 @@ def main():
         import oracle as O
 
         if O.have_ref():
-            secs, prods = cpu_reference_sample(a, args.cpu_stride, 0, os.cpu_count() or 1)
-            line["cpu_baseline"] = {
-                "value": 2.0 * prods / secs / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(),
-                "kind": "reference",
-                "sample": f"rows i = 0 mod {args.cpu_stride} (1/{args.cpu_stride} of rows), "
-                          f"{prods} products, {secs:.2f} s; B = full A"}
+            threads = os.cpu_count() or 1
+            (secs, prods), = ref_rowwise_samples(a, args.cpu_stride, [0], threads)
+            cb = {"value": 2.0 * prods / secs / 1e9, "unit": "GFLOP/s", "cores": threads,
+                  "kind": "reference", "cpu": cpu_model(),
+                  "sample": f"rows i = 0 mod {args.cpu_stride} (1/{args.cpu_stride} of rows) x "
+                            f"full B = A, {prods} products, {secs:.2f} s; only the reference's "
+                            f"spgemm_rowwise timed"}
+            # the reference's cluster-wise path beside it (bench.hpp:185-193), on the
+            # rows of every cpu_stride-th cluster of the hierarchical clustering
+            # (clusters from the GPU top-k candidates + the reference's merge rule)
+            try:
+                t0 = time.perf_counter()
+                asg = eng.hierarchical_clusters(a)
+                t_clu = time.perf_counter() - t0
+                t_row, t_cl, cp, ncl, nrw = ref_clusterwise_sample(
+                    a, asg.cluster_ptr, asg.rows, args.cpu_stride, threads)
+                cb["clusterwise"] = {
+                    "rowwise_value": 2.0 * cp / t_row / 1e9,
+                    "clusterwise_value": 2.0 * cp / t_cl / 1e9, "unit": "GFLOP/s",
+                    "sample": f"every {args.cpu_stride}-th cluster of {asg.nclusters} "
+                              f"(hierarchical, GPU clustering {t_clu:.1f} s): {ncl} clusters, "
+                              f"{nrw} rows, {cp} products; row-wise {t_row:.2f} s, "
+                              f"cluster-wise {t_cl:.2f} s on the same rows"}
+            except Exception as ex:  # reported, never fatal for the bench line
+                cb["clusterwise"] = {"error": str(ex)[:200]}
+            line["cpu_baseline"] = cb
         else:
             line["cpu_baseline"] = None
     print(json.dumps(line))
@@ -433,23 +525,20 @@ def run_tall_skinny(B, args, num_frontiers=10, batch=64, seed=0):
 
         if O.have_ref():
             stride = args.cpu_stride
-            rows = np.arange(0, a.nrows, stride, dtype=np.int64)
-            lens = np.diff(a.row_ptr)[rows]
-            rp = np.zeros(rows.size + 1, np.int64)
-            rp[1:] = np.cumsum(lens)
-            idx = np.concatenate([np.arange(a.row_ptr[r], a.row_ptr[r + 1]) for r in rows])
-            sub = O.Csr(rows.size, a.ncols, rp, a.col_idx[idx], a.values[idx])
+            sub = sub_rows(a, np.arange(0, a.nrows, stride, dtype=np.int64))
+            aref = O.RefCsr(sub)
             secs, prods = 0.0, 0
             for f in fs:
                 fh = f.download()
                 prods += int(np.diff(fh.row_ptr)[sub.col_idx].sum())
-                t0 = time.perf_counter()
-                O.ref_spgemm_rowwise(sub, O.Csr(fh.nrows, fh.ncols, fh.row_ptr, fh.col_idx,
-                                                fh.values), threads=os.cpu_count() or 1)
-                secs += time.perf_counter() - t0
+                fref = O.RefCsr(O.Csr(fh.nrows, fh.ncols, fh.row_ptr, fh.col_idx, fh.values))
+                t, _ = O.ref_time_rowwise(aref, fref, os.cpu_count() or 1)
+                secs += t
             line["cpu_baseline"] = {"value": 2.0 * prods / secs / 1e9, "unit": "GFLOP/s",
                                     "cores": os.cpu_count(), "kind": "reference",
-                                    "sample": f"rows i = 0 mod {stride} of A x every frontier"}
+                                    "cpu": cpu_model(),
+                                    "sample": f"rows i = 0 mod {stride} of A x every frontier; "
+                                              f"only spgemm_rowwise timed"}
     for f in fs:
         f.free()
     print(json.dumps(line))

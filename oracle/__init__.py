@@ -87,6 +87,8 @@ def lib() -> C.CDLL:
         l.orc_merge_candidates.argtypes = [i64, vp, vp, vp, i64, dbl, i32, vp]
         l.orc_merge_candidates.restype = i64
         l.orc_free.argtypes = [vp]
+        l.orc_gen_rmat.argtypes = [i32, i32, dbl, dbl, dbl, u64, P(i64), P(P(i64)), P(P(i32)),
+                                   P(P(dbl))]
         _orc = l
     return _orc
 
@@ -125,6 +127,14 @@ def ref() -> C.CDLL:
         l.ref_generate_frontiers.argtypes = [i64, i64, vp, vp, i64, i64, u64, P(i64), P(i64),
                                              P(P(i64)), P(P(i64)), P(P(i32))]
         l.ref_free.argtypes = [vp]
+        l.ref_csr_new.argtypes = [i64, i64, vp, vp, vp]
+        l.ref_csr_new.restype = vp
+        l.ref_csr_delete.argtypes = [vp]
+        l.ref_time_rowwise.argtypes = [vp, vp, C.c_int, P(dbl), P(i64)]
+        l.ref_cluster_new.argtypes = [vp, i64, vp, vp]
+        l.ref_cluster_new.restype = vp
+        l.ref_cluster_delete.argtypes = [vp]
+        l.ref_time_clusterwise_prepared.argtypes = [vp, vp, C.c_int, P(dbl), P(i64)]
         _ref = l
     return _ref
 
@@ -477,3 +487,72 @@ def generate_frontiers(a, num_frontiers: int, batch: int, seed: int) -> list:
         rpt = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
         out.append(Csr(n, width, rpt, ss.astype(np.int32), np.ones(len(ss), np.float64)))
     return out
+
+
+# ------------------------------------------------------------ generator (gen.c)
+def gen_rmat(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int) -> Csr:
+    """The cfg3/cfg5 R-MAT recipe restated in C (gen.c), bit-identical to the
+    product's generator (tests/test_oracle.py) — bench.py's reference arm builds its
+    input with it, so that process never loads the product library."""
+    n = i64()
+    rp, ci, v = P(i64)(), P(i32)(), P(dbl)()
+    rc = lib().orc_gen_rmat(scale, edge_factor, a, b, c, seed, C.byref(n), C.byref(rp),
+                            C.byref(ci), C.byref(v))
+    if rc != 0:
+        raise ValueError("orc_gen_rmat: bad sizes or out of memory")
+    f = lib().orc_free
+    nn = n.value
+    row_ptr = _arr(rp, nn + 1, np.int64, f)
+    nnz = int(row_ptr[-1])
+    return Csr(nn, nn, row_ptr, _arr(ci, nnz, np.int32, f), _arr(v, nnz, np.float64, f))
+
+
+# ------------------------------------------------ reference timing (bench only)
+class RefCsr:
+    """The reference's own CsrMatrix (int32 offsets), built once outside any timed
+    region (ref_shim.cpp ref_csr_new)."""
+
+    def __init__(self, a):
+        arp, aci, av = _csr_args(a)
+        self.nrows, self.ncols = a.nrows, a.ncols
+        self.h = ref().ref_csr_new(a.nrows, a.ncols, _p(arp), _p(aci), _p(av))
+        if not self.h:
+            _ref_check(6)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().ref_csr_delete(self.h)
+            self.h = None
+
+
+class RefCluster:
+    """The reference's CsrClusterMatrix of a RefCsr and an assignment
+    (build_csr_cluster, cluster_format.hpp:130-186), built outside the timing."""
+
+    def __init__(self, a: RefCsr, cluster_ptr, rows):
+        cp = np.ascontiguousarray(cluster_ptr, np.int64)
+        rr = np.ascontiguousarray(rows, np.int32)
+        self.h = ref().ref_cluster_new(a.h, cp.size - 1, _p(cp), _p(rr))
+        if not self.h:
+            _ref_check(6)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().ref_cluster_delete(self.h)
+            self.h = None
+
+
+def ref_time_rowwise(a: RefCsr, b: RefCsr, threads: int = 0):
+    """Seconds of the reference's spgemm_rowwise(a, b) call alone (and nnz(C))."""
+    s, nnz = dbl(), i64()
+    _ref_check(ref().ref_time_rowwise(a.h, b.h, threads, C.byref(s), C.byref(nnz)))
+    return s.value, nnz.value
+
+
+def ref_time_clusterwise(ac: RefCluster, b: RefCsr, threads: int = 0):
+    """Seconds of the reference's spgemm_clusterwise(ac, b) call alone (and C's
+    value slots)."""
+    s, slots = dbl(), i64()
+    _ref_check(ref().ref_time_clusterwise_prepared(ac.h, b.h, threads, C.byref(s),
+                                                   C.byref(slots)))
+    return s.value, slots.value

@@ -49,6 +49,9 @@ int64_t orc_merge_candidates(int64_t nrows, const int64_t* rp, const int32_t* co
                              const orc_candidate* pairs, int64_t npairs, double jacc_th,
                              int32_t max_cluster, int32_t* cluster_of);
 void orc_free(void* p);
+/* gen.c: the seeded R-MAT recipe of cfg3/cfg5 (bench.py's reference arm input) */
+int orc_gen_rmat(int32_t scale, int32_t edge_factor, double a, double b, double c, uint64_t seed,
+                 int64_t* nrows_out, int64_t** rp_out, int32_t** ci_out, double** v_out);
 
 #ifdef __cplusplus
 }
