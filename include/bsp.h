@@ -197,6 +197,51 @@ int bsp_partition_rows(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int32_t
                        int64_t* bounds_out);
 
 /* ------------------------------------------------------------------ */
+/* multi-GPU (one process per GPU; NCCL over NVLink, loaded on demand)  */
+/* ------------------------------------------------------------------ */
+/* No reference counterpart: the reference has no distributed code
+ * (SPEC.md:563).  Rows of C are independent given B (spgemm.hpp:88-104), so
+ * A's rows are split by product cost (bsp_partition_rows), B is replicated,
+ * and each rank multiplies its row block with no communication; C stays
+ * sharded or is assembled on request. */
+#define BSP_NCCL_ID_BYTES 128
+typedef struct {
+    int64_t row_begin, row_end; /* this rank's rows of A (and of C) */
+    int64_t products_local;     /* intermediate products of this rank's rows */
+    int64_t nnz_local;          /* nnz of this rank's shard of C */
+    int64_t nnz_global;         /* nnz of the gathered C (gather=1 or one rank), else -1 */
+    double multiply_ms;         /* this rank's multiply (CUDA events, handle stream) */
+    double gather_ms;           /* the assembly of the global C (gather=1) */
+} bsp_shard_info;
+/* An ncclUniqueId (rank 0 creates it and ships it to the others, e.g. with
+ * torch.distributed). */
+int bsp_nccl_unique_id(void* id_out /* BSP_NCCL_ID_BYTES */);
+/* Give the handle its own NCCL communicator (on its device). */
+int bsp_comm_init(bsp_handle h, int nranks, int rank, const void* id /* BSP_NCCL_ID_BYTES */);
+int bsp_comm_destroy(bsp_handle h);
+int bsp_comm_rank(bsp_handle h, int* rank, int* nranks);
+/* Replicate a device CSR from `root` to every rank (NCCL broadcasts on the
+ * handle's stream; on the other ranks M is allocated by the library, owned=1).
+ * ms_out (nullable): the broadcast's time (CUDA events). */
+int bsp_csr_broadcast(bsp_handle h, bsp_csr* M, int root, double* ms_out);
+/* Global C from row shards held by every rank (concatenated in rank order):
+ * an all-gather of the shard sizes, then one broadcast per rank of its exact
+ * arrays (no padding; NCCL has no all-gather-v) and a row_ptr rebase. */
+int bsp_csr_allgather_rows(bsp_handle h, const bsp_csr* shard, bsp_csr* global);
+/* Row-sharded C = A*B: this rank's row block of C (gather = 0) or the global C
+ * on every rank (gather = 1).  A and B must be resident on every rank. */
+int bsp_spgemm_rowwise_sharded(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int gather,
+                               bsp_csr* C, bsp_shard_info* info /* nullable */);
+/* Cluster-wise shards: bounds[0..nparts] over clusters (CSR_Cluster order),
+ * split by the clusters' intermediate products, snapped to cluster boundaries. */
+int bsp_partition_clusters(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr* B,
+                           int32_t nparts, int64_t* bounds_out);
+/* Rows `rows` (device int32) of A as a new CSR (owned): a cluster shard's
+ * operand (its clusters' rows in cluster order). */
+int bsp_csr_select_rows(bsp_handle h, const bsp_csr* A, const int32_t* rows, int64_t n,
+                        bsp_csr* out);
+
+/* ------------------------------------------------------------------ */
 /* cluster-wise SpGEMM                                                 */
 /* ------------------------------------------------------------------ */
 /* reference: build_csr_cluster, cluster_format.hpp:130-186.  cluster_ptr/rows

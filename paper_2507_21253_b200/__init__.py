@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field
-from typing import Iterable, List, Optional, Sequence
+from typing import Tuple, Iterable, List, Optional, Sequence
 
 import numpy as np
 
@@ -332,6 +332,21 @@ class DeviceCsr:
     def nnz(self) -> int:
         return int(self.s.nnz)
 
+    def torch_views(self):
+        """Zero-copy torch views (row_ptr int64, col_idx int32, values float64) of
+        this device CSR's arrays (valid while it lives)."""
+        import torch
+
+        class _Cai:
+            def __init__(s_, ptr, n, ts):
+                s_.__cuda_array_interface__ = {"shape": (n,), "typestr": ts,
+                                               "data": (int(ptr or 0), False), "version": 3}
+
+        dev = f"cuda:{self.engine.device}"
+        return (torch.as_tensor(_Cai(self.s.row_ptr, self.nrows + 1, "<i8"), device=dev),
+                torch.as_tensor(_Cai(self.s.col_idx, self.nnz(), "<i4"), device=dev),
+                torch.as_tensor(_Cai(self.s.values, self.nnz(), "<f8"), device=dev))
+
     def download(self) -> CsrMatrix:
         n, nnz = self.nrows, self.nnz()
         rp = np.empty(n + 1, np.int64)
@@ -397,7 +412,8 @@ class DeviceCsrCluster:
         return out
 
     def free(self) -> None:
-        if self.s is not None:
+        # after Engine.close() the handle (its stream and pools) is gone: drop
+        if self.s is not None and self.engine.h:
             self.engine.lib.bsp_csr_cluster_free(self.engine.h, C.byref(self.s))
         self.s = None
 
@@ -508,6 +524,65 @@ class Engine:
         b = np.zeros(nparts + 1, np.int64)
         _check(self.lib.bsp_partition_rows(self.h, C.byref(A.s), C.byref(B.s), nparts, _ptr(b)))
         return b
+
+    # -- multi-GPU (one process per GPU, NCCL; include/bsp.h "multi-GPU") ----
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(L.BSP_NCCL_ID_BYTES)
+        _check(L.load().bsp_nccl_unique_id(buf))
+        return buf.raw
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
+        """Give this engine its own NCCL communicator (rank of nranks)."""
+        buf = C.create_string_buffer(bytes(uid), L.BSP_NCCL_ID_BYTES)
+        _check(self.lib.bsp_comm_init(self.h, nranks, rank, buf))
+
+    def comm_destroy(self) -> None:
+        _check(self.lib.bsp_comm_destroy(self.h))
+
+    def comm_rank(self) -> Tuple[int, int]:
+        r, n = C.c_int(), C.c_int()
+        _check(self.lib.bsp_comm_rank(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+    def broadcast(self, M: Optional[DeviceCsr], root: int = 0) -> Tuple[DeviceCsr, float]:
+        """Replicate a device CSR from `root` (NCCL); returns (matrix, ms)."""
+        s = M.s if M is not None else L.bsp_csr()
+        ms = C.c_double()
+        _check(self.lib.bsp_csr_broadcast(self.h, C.byref(s), root, C.byref(ms)))
+        return (M if M is not None else DeviceCsr(self, s)), float(ms.value)
+
+    def allgather_rows(self, shard: DeviceCsr) -> DeviceCsr:
+        s = L.bsp_csr()
+        _check(self.lib.bsp_csr_allgather_rows(self.h, C.byref(shard.s), C.byref(s)))
+        return DeviceCsr(self, s)
+
+    def spgemm_rowwise_sharded(self, A: DeviceCsr, B: DeviceCsr, gather: bool = False):
+        """Row-sharded C = A*B over the engine's communicator: (C, info) with C this
+        rank's row block, or the global C on every rank when gather=True."""
+        s = L.bsp_csr()
+        inf = L.bsp_shard_info()
+        _check(self.lib.bsp_spgemm_rowwise_sharded(self.h, C.byref(A.s), C.byref(B.s),
+                                                   1 if gather else 0, C.byref(s), C.byref(inf)))
+        info = {k: getattr(inf, k) for k, _ in L.bsp_shard_info._fields_}
+        return DeviceCsr(self, s), info
+
+    def partition_clusters(self, Ac: "DeviceCsrCluster", B: DeviceCsr, nparts: int) -> np.ndarray:
+        b = np.zeros(nparts + 1, np.int64)
+        _check(self.lib.bsp_partition_clusters(self.h, C.byref(Ac.s), C.byref(B.s), nparts,
+                                               _ptr(b)))
+        return b
+
+    def select_rows(self, A: DeviceCsr, rows: np.ndarray) -> DeviceCsr:
+        import torch
+
+        r = torch.from_numpy(np.ascontiguousarray(rows, np.int32)).to(f"cuda:{self.device}")
+        torch.cuda.synchronize(self.device)
+        s = L.bsp_csr()
+        _check(self.lib.bsp_csr_select_rows(self.h, C.byref(A.s), r.data_ptr(), int(r.numel()),
+                                            C.byref(s)))
+        self.synchronize()
+        return DeviceCsr(self, s)
 
     def spgemm_rowwise_host(self, a: CsrMatrix, b: CsrMatrix) -> CsrMatrix:
         ha, hb = a._host(), b._host()

@@ -50,6 +50,14 @@ class bsp_host_csr_cluster(C.Structure):
                 ("valid", P(u64)), ("row_map", P(i32))]
 
 
+class bsp_shard_info(C.Structure):
+    _fields_ = [("row_begin", i64), ("row_end", i64), ("products_local", i64),
+                ("nnz_local", i64), ("nnz_global", i64), ("multiply_ms", dbl), ("gather_ms", dbl)]
+
+
+BSP_NCCL_ID_BYTES = 128
+
+
 class bsp_access_stats(C.Structure):
     _fields_ = [("b_row_loads", u64), ("a_inner_iters", u64), ("placeholder_skips", u64)]
 
@@ -129,6 +137,16 @@ SIGNATURES = {
     "bsp_gen_hidden_clusters": (C.c_int, [i64, i32, i32, dbl, dbl, u64, u64, P(bsp_host_csr)]),
     "bsp_gen_rmat": (C.c_int, [i32, i32, dbl, dbl, dbl, u64, P(bsp_host_csr)]),
     "bsp_gen_stencil27": (C.c_int, [i32, i64, P(bsp_host_csr)]),
+    "bsp_nccl_unique_id": (C.c_int, [vp]),
+    "bsp_comm_init": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "bsp_comm_destroy": (C.c_int, [vp]),
+    "bsp_comm_rank": (C.c_int, [vp, P(C.c_int), P(C.c_int)]),
+    "bsp_csr_broadcast": (C.c_int, [vp, P(bsp_csr), C.c_int, P(dbl)]),
+    "bsp_csr_allgather_rows": (C.c_int, [vp, P(bsp_csr), P(bsp_csr)]),
+    "bsp_spgemm_rowwise_sharded": (C.c_int, [vp, P(bsp_csr), P(bsp_csr), C.c_int, P(bsp_csr),
+                                             P(bsp_shard_info)]),
+    "bsp_partition_clusters": (C.c_int, [vp, P(bsp_csr_cluster), P(bsp_csr), i32, vp]),
+    "bsp_csr_select_rows": (C.c_int, [vp, P(bsp_csr), vp, i64, P(bsp_csr)]),
 }
 
 _lib = None

@@ -656,7 +656,66 @@ void free_cluster(bsp_handle h, bsp_csr_cluster* m) {
 
 using namespace bsp;
 
+namespace bsp {
+namespace {
+// Intermediate products of each cluster (one warp per cluster): over its merged
+// columns p, (live members of p) x nnz(B row col[p]) — the sum of its member
+// rows' row_upper_bound (spgemm.hpp:31-36), placeholders not counted.
+__global__ void cluster_work_kernel(const int64_t* __restrict__ ccp, const int32_t* __restrict__ col,
+                                    const uint32_t* __restrict__ mask,
+                                    const int64_t* __restrict__ brp, int64_t ncl,
+                                    int64_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = int64_t{gridDim.x} * (blockDim.x >> 5);
+    for (int64_t c = blockIdx.x * int64_t{blockDim.x >> 5} + (threadIdx.x >> 5); c < ncl; c += nw) {
+        int64_t P = 0;
+        for (int64_t q = ccp[c] + lane; q < ccp[c + 1]; q += 32) {
+            const int32_t k = col[q];
+            P += static_cast<int64_t>(__popc(mask[q])) * (brp[k + 1] - brp[k]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) P += __shfl_xor_sync(0xffffffffu, P, o);
+        if (lane == 0) out[c] = P;
+    }
+}
+}  // namespace
+}  // namespace bsp
+
 extern "C" {
+
+// Cluster-boundary split for multi-GPU cluster-wise shards:
+// bounds[g] = the first cluster whose exclusive product prefix reaches
+// total*g/nparts; clusters are independent (cluster_spgemm.hpp:108-109), so a
+// shard is a contiguous run of clusters (CSR_Cluster order).
+int bsp_partition_clusters(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr* B,
+                           int32_t nparts, int64_t* bounds_out) {
+    return guarded([&] {
+        require(A != nullptr && B != nullptr && bounds_out != nullptr,
+                "partition_clusters: null argument");
+        require(nparts >= 1, "partition_clusters: nparts must be >= 1");
+        require(A->ncols == B->nrows, "partition_clusters: dimension mismatch");
+        BSP_CUDA(cudaSetDevice(h->device));
+        const int64_t ncl = A->nclusters;
+        std::vector<int64_t> pc(ncl);
+        if (ncl > 0) {
+            DBuf<int64_t> w(h, ncl);
+            BSP_LAUNCH(h, cluster_work_kernel, grid_for(h, ncl * 32, 256), 256, 0,
+                       A->cluster_col_ptr, A->col_idx, A->member_mask, B->row_ptr, ncl, w.p);
+            d2h(h, pc.data(), w.p, ncl);
+            sync(h);
+        }
+        std::vector<int64_t> pre(ncl + 1, 0);
+        for (int64_t c = 0; c < ncl; ++c) pre[c + 1] = pre[c] + pc[c];
+        bounds_out[0] = 0;
+        for (int32_t g = 1; g < nparts; ++g) {
+            const int64_t target =
+                static_cast<int64_t>((static_cast<__int128>(pre[ncl]) * g) / nparts);
+            const int64_t c = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+            bounds_out[g] = std::max(bounds_out[g - 1], std::min<int64_t>(c, ncl));
+        }
+        bounds_out[nparts] = ncl;
+    });
+}
 
 int bsp_csr_cluster_build(bsp_handle h, const bsp_csr* A, int64_t nclusters,
                           const int64_t* cluster_ptr, const int32_t* rows, bsp_csr_cluster* out) {
@@ -703,7 +762,10 @@ int bsp_csr_cluster_build(bsp_handle h, const bsp_csr* A, int64_t nclusters,
 }
 
 int bsp_csr_cluster_free(bsp_handle h, bsp_csr_cluster* m) {
-    return guarded([&] { free_cluster(h, m); });
+    return guarded([&] {
+        require(h != nullptr || m == nullptr || !m->owned, "csr_cluster_free: null handle");
+        free_cluster(h, m);
+    });
 }
 
 int bsp_csr_cluster_download(bsp_handle h, const bsp_csr_cluster* m, bsp_host_csr_cluster* o) {

@@ -26,6 +26,9 @@ struct cuda_error : std::runtime_error {
 struct oom_error : std::runtime_error {
     explicit oom_error(const std::string& w) : std::runtime_error(w) {}
 };
+struct nccl_error : std::runtime_error {
+    explicit nccl_error(const std::string& w) : std::runtime_error(w) {}
+};
 
 inline void require(bool cond, const std::string& msg) {
     if (!cond) throw contract_error(msg);
@@ -51,6 +54,9 @@ int guarded(F&& f) {
     } catch (const cuda_error& e) {
         set_last_error(std::string("cuda: ") + e.what());
         return BSP_ERR_CUDA;
+    } catch (const nccl_error& e) {
+        set_last_error(std::string("nccl: ") + e.what());
+        return BSP_ERR_NCCL;
     } catch (const std::bad_alloc&) {
         set_last_error("host out of memory");
         return BSP_ERR_OOM;

@@ -225,6 +225,7 @@ int bsp_destroy(bsp_handle h) {
     return guarded([&] {
         if (!h) return;
         cudaStreamSynchronize(h->stream);
+        if (h->comm) bsp_comm_destroy(h);
         if (h->own_stream) cudaStreamDestroy(h->stream);
         // pools with live allocations (results still held by the caller) are
         // released by the driver once those are freed
@@ -405,6 +406,7 @@ int bsp_stream_wait(bsp_handle waiter, bsp_handle signaler) {
 int bsp_csr_free(bsp_handle h, bsp_csr* m) {
     return guarded([&] {
         if (!m) return;
+        require(h != nullptr || !m->owned, "csr_free: null handle");
         if (m->owned) {
             dfree(h, m->row_ptr);
             if (m->owned != 2) dfree(h, m->col_idx);  // 2: col_idx inside the values block

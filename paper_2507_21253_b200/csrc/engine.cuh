@@ -41,6 +41,15 @@ struct bsp_handle_s {
     // (light-row symbolic during the heavy-row planner); fork/join events.
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // Multi-GPU (comm.cu): this rank's NCCL communicator (one process per GPU),
+    // created by bsp_comm_init; nullptr = single GPU.
+    void* comm = nullptr;
+    int comm_rank = 0, comm_size = 1;
+    // bsp_spgemm_rowwise_sharded's row split of the last (A, B) pair (the split
+    // needs every row's products: computed once, reused while A and B stay)
+    const void* part_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t part_nnz[2] = {0, 0};
+    std::vector<int64_t> part_bounds;
 };
 
 namespace bsp {
