@@ -119,7 +119,8 @@ typedef struct {
     int64_t nnz_out;      /* nnz(C) */
     int64_t units[16];    /* work units: [0..7] rows per class (0 empty; 1..6 light, at
                              most 128/512/1024/2048/3072/4096 products; 7 heavy), [8]
-                             sparse windows, [9] dense windows, [10] cluster tiles */
+                             sparse windows, [9] dense windows, [10] cluster tiles, [11]
+                             of which union tiles (each B entry sorted once per cluster) */
     int32_t kernels_launched;
     int32_t chunks;       /* row chunks: bsp_spgemm_rowwise_host splits A's rows when C
                              exceeds the device budget (half the free memory); 1 otherwise */

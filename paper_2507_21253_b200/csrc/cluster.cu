@@ -146,12 +146,18 @@ __global__ void cluster_to_csr_kernel(const int32_t* __restrict__ sizes,
 // ---------------------------------------------------------------------------
 // cluster products + routing
 // ---------------------------------------------------------------------------
-constexpr int NCC = 6;  // 0: row-wise classes, 1: <=512, 2: <=1024, 3: <=2048, 4: <=3072, 5: <=4096 products
-__constant__ int kClusterCap[NCC] = {0, 512, 1024, 2048, 3072, 4096};
+// 0: row-wise classes; 1..5: member-keyed tiles of <= 512 .. 4096 products;
+// 6, 7: union tiles of <= 1024 / 2048 distinct B entries (cluster_union_kernel)
+constexpr int NCC = 8;
+constexpr int NKC = 6;  // member-keyed classes 1..5 (+ 0)
+__constant__ int kClusterCap[NKC] = {0, 512, 1024, 2048, 3072, 4096};
+constexpr int UMAXK = 8;      // union tiles: members (accumulators in registers)
+constexpr int UMAXMC = 512;   // union tiles: merged columns
+constexpr int UMAXA = 1024;   // union tiles: A values staged (merged columns x members)
 
 __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
                                         uint8_t* __restrict__ ccls, uint8_t* __restrict__ row_skip,
-                                        unsigned long long* __restrict__ counts) {
+                                        unsigned long long* __restrict__ counts, int union_ok) {
     __shared__ unsigned s_cnt[NCC];
     if (threadIdx.x < NCC) s_cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -163,8 +169,9 @@ __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
         for (int64_t u = m.ccp[c]; u < m.ccp[c + 1]; ++u) {
             const int32_t k = m.ccol[u];
             const int64_t len = m.brp[k + 1] - m.brp[k];
-            P += static_cast<int64_t>(__popc(m.mask[u])) * len;
-            S += len;
+            const int live = __popc(m.mask[u]);
+            P += static_cast<int64_t>(live) * len;
+            if (live) S += len;  // B entries the cluster loads (once each)
         }
         // staged cluster tile: B rows of the cluster fit the stage, every
         // member fits one merge tile (otherwise the rows go to the row bins)
@@ -172,15 +179,18 @@ __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
         // tried — see DESIGN.md §4): classes by the cluster's total products
         int cl = 0;
         const bool keyfits = bit_length(static_cast<uint32_t>(K - 1)) + cbits <= 31;
-        (void)MC;
-        (void)S;
-        if (K >= 2 && K <= MAXK && keyfits && P > 0 && P <= kClusterCap[NCC - 1]) {
+        if (union_ok && K >= 2 && K <= UMAXK && MC <= UMAXMC && MC * K <= UMAXA && S > 0 &&
+            S <= 2048) {
+            // union tile: each B entry expanded and sorted once for the cluster
+            cl = S <= 1024 ? 6 : 7;
+        } else if (K >= 2 && K <= MAXK && keyfits && P > 0 && P <= kClusterCap[NKC - 1]) {
             cl = 1;
             while (P > kClusterCap[cl]) ++cl;
         }
         ccls[c] = static_cast<uint8_t>(cl);
         if (cl > 0)
-            for (int l = 0; l < K; ++l) row_skip[m.row_map[m.member_ptr[c] + l]] = 1;
+            for (int l = 0; l < K; ++l)
+                row_skip[m.row_map[m.member_ptr[c] + l]] = cl >= 6 ? 2 : 1;
         atomicAdd(&s_cnt[cl], 1u);
     }
     __syncthreads();
@@ -358,6 +368,485 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
     }
 }
 
+// ---------------------------------------------------------------------------
+// Union tile (K <= 8): the paper's B-row reuse taken to the sort.  Every B entry
+// of the cluster's merged columns is expanded ONCE (column key, b value, merged
+// column index) instead of once per live member, the entries are sorted by
+// column (stable: ties keep ascending k), and each run of one column is the
+// column's slot in the cluster's output union (the CSR_Cluster C columns,
+// cluster_spgemm.hpp:86-93).  The run's head then forms, for every live member
+// l, sum over the run's entries with l live of a[p][l] * b in run order =
+// ascending k from 0.0 — the member's row-wise value bit for bit
+// (cluster_spgemm.hpp:129-143) — and writes it at the member's rank of that
+// column: a per-member count of earlier union columns holding l (ballots per
+// member within a warp + a scan over (row, warp) of packed 16-bit counters).
+// Sort work drops from P (member products) to S (B entries loaded): cfg2's
+// clusters load each template column's B row once for 8 members.
+// ---------------------------------------------------------------------------
+template <int T, int CAPM>
+struct UnionShared {
+    MergeShared<T, CAPM> m;
+    uint16_t pidx[CAPM];     // merged column (local) of each expanded entry
+    double sa[UMAXA];        // the cluster's A values, [p * K + l]
+    uint32_t smask[UMAXMC];  // live members of merged column p
+    int16_t runp[T];         // merged column of each compacted run of the chunk
+    unsigned long long cnt[2][((CAPM + T - 1) / T) * (T / 32)];  // packed member counts
+    int64_t mbase[UMAXK];
+};
+
+template <int T, int CAPM>
+__global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
+    cluster_union_kernel(ClusterMats m, const int32_t* __restrict__ ids, int csort,
+                         const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
+                         double* __restrict__ oval) {
+    using U = UnionShared<T, CAPM>;
+    using S = MergeShared<T, CAPM>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    U& us = *reinterpret_cast<U*>(smem_raw);
+    S& s = us.m;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = T / 32;
+    constexpr int R = (CAPM + T - 1) / T;
+    const int32_t c = ids[blockIdx.x];
+    const int K = m.sizes[c];
+    const int64_t u0 = m.ccp[c], u1 = m.ccp[c + 1];
+    const int MC = static_cast<int>(u1 - u0);
+    const int64_t vbase = m.vptr[c];
+    if (tid < K) us.mbase[tid] = crp[m.row_map[m.member_ptr[c] + tid]];
+    for (int q = tid; q < MC * K; q += T) us.sa[q] = __ldg(m.aval + vbase + q);
+    for (int q = tid; q < MC; q += T) us.smask[q] = __ldg(m.mask + u0 + q);
+    auto& x = s.ex();
+    int total = 0, nruns = 0;
+    for (int64_t uc = u0; uc < u1; uc += T) {
+        const int64_t u = uc + tid;
+        int len = 0;
+        int64_t start = 0;
+        if (u < u1 && __ldg(m.mask + u) != 0u) {
+            const int32_t k = __ldg(m.ccol + u);
+            start = __ldg(m.brp + k);
+            len = static_cast<int>(__ldg(m.brp + k + 1) - start);
+        }
+        const int packed = len | ((len > 0) << 16);
+        int off, agg;
+        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        const int r = off >> 16;
+        if (len > 0) {
+            if (nruns + r < S::MAXRUNS)
+                s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
+            x.pstart[r] = start;
+            x.poff[r] = off & 0xffff;
+            us.runp[r] = static_cast<int16_t>(uc + tid - u0);
+        }
+        const int nr = agg >> 16, ct = agg & 0xffff;
+        if (tid == 0) x.poff[nr] = ct;
+        __syncthreads();
+        {
+            int e0, we, qa;
+            warp_slice(x.poff, nr, ct, NW, e0, we, qa);
+            for (; e0 < we; e0 += 32) {
+                const int q = warp_runs(x.poff, nr, e0, qa);
+                const int e = e0 + lane;
+                if (e < we) {
+                    const int64_t src = x.pstart[q] + (e - x.poff[q]);
+                    const int g = total + e;
+                    cp_async4(&s.key0[PADI(g)], m.bcol + src);
+                    cp_async8(&s.val[g], m.bval + src);
+                    us.pidx[g] = static_cast<uint16_t>(us.runp[q]);
+                }
+            }
+            cp_async_wait_all();
+        }
+        total += ct;
+        nruns += nr;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (nruns <= S::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
+        s.nruns = nruns;
+    }
+    __syncthreads();
+    // keys are absolute columns (kofs = 0: idx0 is set by the sort's prep)
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(m.ncols), csort, 0, false, 0);
+    const uint32_t* KS = s.key(b);
+    const uint16_t* X = s.idx(b);
+    uint32_t* umask = b ? s.key0 : s.u.m.key1;  // the buffer the sort left idle
+    // pass A: each head's member mask (OR over its run) and the per-(row, warp)
+    // head counts of every member (16-bit fields, members 0-3 and 4-7)
+    unsigned hm[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+        hm[rr] = 0u;
+        if (rr * T >= total) {  // block-uniform: rows past the tile's entries
+            if (lane == 0) us.cnt[0][rr * NW + warp] = us.cnt[1][rr * NW + warp] = 0ull;
+            continue;
+        }
+        const int o = rr * T + tid;
+        const bool h = o < total && (o == 0 || KS[PADI(o)] != KS[PADI(o - 1)]);
+        hm[rr] = __ballot_sync(0xffffffffu, h);
+        uint32_t M = 0;
+        if (h) {
+            const uint32_t key = KS[PADI(o)];
+            int e = o;
+            do {
+                M |= us.smask[us.pidx[X[PADI(e)]]];
+                ++e;
+            } while (e < total && KS[PADI(e)] == key);
+            umask[o] = M;
+        }
+        unsigned long long ca = 0, cb = 0;
+#pragma unroll
+        for (int l = 0; l < UMAXK; ++l) {
+            if (l >= K) break;
+            const unsigned bl = __ballot_sync(0xffffffffu, (M >> l) & 1u);
+            if (l < 4) ca |= static_cast<unsigned long long>(__popc(bl)) << (16 * l);
+            else cb |= static_cast<unsigned long long>(__popc(bl)) << (16 * (l - 4));
+        }
+        if (lane == 0) {
+            us.cnt[0][rr * NW + warp] = ca;
+            us.cnt[1][rr * NW + warp] = cb;
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the packed counters over (row, warp), in sorted order
+    constexpr int NC = R * NW;
+    static_assert(NC <= 64, "one warp scans the (row, warp) counters");
+    if (warp == 0) {
+        unsigned long long a0 = 2 * lane < NC ? us.cnt[0][2 * lane] : 0ull;
+        unsigned long long a1 = 2 * lane + 1 < NC ? us.cnt[0][2 * lane + 1] : 0ull;
+        unsigned long long b0 = 2 * lane < NC ? us.cnt[1][2 * lane] : 0ull;
+        unsigned long long b1 = 2 * lane + 1 < NC ? us.cnt[1][2 * lane + 1] : 0ull;
+        unsigned long long sa_ = a0 + a1, sb_ = b0 + b1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long ta = __shfl_up_sync(0xffffffffu, sa_, o);
+            const unsigned long long tb = __shfl_up_sync(0xffffffffu, sb_, o);
+            if (lane >= o) {
+                sa_ += ta;
+                sb_ += tb;
+            }
+        }
+        const unsigned long long ea = sa_ - (a0 + a1), eb = sb_ - (b0 + b1);  // exclusive
+        if (2 * lane < NC) {
+            us.cnt[0][2 * lane] = ea;
+            us.cnt[1][2 * lane] = eb;
+        }
+        if (2 * lane + 1 < NC) {
+            us.cnt[0][2 * lane + 1] = ea + a0;
+            us.cnt[1][2 * lane + 1] = eb + b0;
+        }
+    }
+    __syncthreads();
+    // pass B: per head, each live member's sum in run (= k) order, written at
+    // that member's rank of the column
+    const unsigned below = (1u << lane) - 1u;
+#pragma unroll 1
+    for (int rr = 0; rr < R; ++rr) {
+        if (rr * T >= total) break;
+        const int o = rr * T + tid;
+        const bool h = (hm[rr] >> lane) & 1u;
+        const uint32_t M = h ? umask[o] : 0u;
+        const unsigned long long pa = us.cnt[0][rr * NW + warp], pb = us.cnt[1][rr * NW + warp];
+        int pos[UMAXK];
+#pragma unroll
+        for (int l = 0; l < UMAXK; ++l) {
+            pos[l] = 0;
+            if (l >= K) continue;
+            const unsigned bl = __ballot_sync(0xffffffffu, (M >> l) & 1u);
+            const unsigned long long pw = l < 4 ? pa : pb;
+            pos[l] = static_cast<int>((pw >> (16 * (l & 3))) & 0xffffull) + __popc(bl & below);
+        }
+        if (!h) continue;
+        double acc[UMAXK];
+#pragma unroll
+        for (int l = 0; l < UMAXK; ++l) acc[l] = 0.0;
+        const uint32_t key = KS[PADI(o)];
+        int e = o;
+        do {
+            const int xe = X[PADI(e)];
+            const int p = us.pidx[xe];
+            const double bv = s.val[xe];
+            const uint32_t mp = us.smask[p];
+            const double* ap = us.sa + p * K;
+#pragma unroll
+            for (int l = 0; l < UMAXK; ++l)
+                if ((mp >> l) & 1u) acc[l] = __dadd_rn(acc[l], __dmul_rn(ap[l], bv));
+            ++e;
+        } while (e < total && KS[PADI(e)] == key);
+#pragma unroll
+        for (int l = 0; l < UMAXK; ++l) {
+            if (!((M >> l) & 1u)) continue;
+            const int64_t q = us.mbase[l] + pos[l];
+            ocol[q] = static_cast<int32_t>(key);
+            oval[q] = acc[l];
+        }
+    }
+}
+
+// Symbolic count of the union tiles' rows from the cluster's B rows, each loaded
+// once (the symbolic twin of cluster_union_kernel; replaces one row-wise hash
+// count per member, hash_accumulator.hpp:48-54 / spgemm.hpp:41-63): every B
+// entry of a live merged column is inserted once into a CTA-wide open-addressed
+// table whose slot also collects the live members (OR); member l's output count
+// is the number of slots holding l.
+template <int T, int HS>
+__global__ void __launch_bounds__(T) cluster_union_count_kernel(ClusterMats m,
+                                                               const int32_t* __restrict__ ids,
+                                                               int64_t* __restrict__ row_nnz) {
+    __shared__ int32_t keys[HS];
+    __shared__ uint32_t mem[HS];
+    __shared__ int s_cnt[UMAXK];
+    constexpr int LG = 31 - __builtin_clz(static_cast<unsigned>(HS));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = T / 32;
+    const int32_t c = ids[blockIdx.x];
+    const int K = m.sizes[c];
+    for (int i = tid; i < HS; i += T) {
+        keys[i] = -1;
+        mem[i] = 0u;
+    }
+    if (tid < UMAXK) s_cnt[tid] = 0;
+    __syncthreads();
+    const int64_t u0 = m.ccp[c], u1 = m.ccp[c + 1];
+    // a warp per merged column (its B row read coalesced), columns strided over warps
+    for (int64_t u = u0 + warp; u < u1; u += NW) {
+        const uint32_t mk = __ldg(m.mask + u);
+        if (!mk) continue;
+        const int32_t k = __ldg(m.ccol + u);
+        const int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
+        for (int64_t q = b0 + lane; q < b1; q += 32) {
+            const int32_t col = __ldg(m.bcol + q);
+            uint32_t slot = col_hash(static_cast<uint32_t>(col), LG);
+            for (;;) {
+                const int32_t prev = atomicCAS(&keys[slot], -1, col);
+                if (prev == -1 || prev == col) break;
+                slot = (slot + 1) & (HS - 1);
+            }
+            atomicOr(&mem[slot], mk);
+        }
+    }
+    __syncthreads();
+    int cnt[UMAXK];
+#pragma unroll
+    for (int l = 0; l < UMAXK; ++l) cnt[l] = 0;
+    for (int i = tid; i < HS; i += T) {
+        const uint32_t x = mem[i];
+#pragma unroll
+        for (int l = 0; l < UMAXK; ++l) cnt[l] += (x >> l) & 1u;
+    }
+#pragma unroll
+    for (int l = 0; l < UMAXK; ++l) {
+        int v = cnt[l];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(&s_cnt[l], v);
+    }
+    __syncthreads();
+    if (tid < K) row_nnz[m.row_map[m.member_ptr[c] + tid]] = s_cnt[tid];
+}
+
+template <int T, int CAPM>
+void launch_union(bsp_handle h, const ClusterMats& m, const int32_t* ids, int64_t n,
+                  const int64_t* crp, int32_t* ocol, double* oval) {
+    if (n <= 0) return;
+    using U = UnionShared<T, CAPM>;
+    auto k = cluster_union_kernel<T, CAPM>;
+    static const std::string nm =
+        "cluster_union<" + std::to_string(T) + "," + std::to_string(CAPM) + ">";
+    static const int csort = [] {
+        const char* e = std::getenv("BSP_CSORT");
+        return e ? std::atoi(e) : 1000;
+    }();
+    set_smem(k, sizeof(U));
+    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(U), m, ids, csort, crp,
+                  ocol, oval);
+}
+
+// ---------------------------------------------------------------------------
+// Duplicate-heavy clusters of two rows (cfg4 after RCM + hierarchical: stencil
+// rows of 729 products -> 125 columns, neighbours sharing most B rows): a warp
+// per cluster, the row-wise hash accumulator (rowwise.cu hashacc_kernel) with
+// one value slot per member.  Merged columns are walked in ascending k; each B
+// row is loaded ONCE, its columns inserted once into the warp's table, and
+// a[p][l] * b added for each live member l — a segment's columns are distinct,
+// so no two lanes collide and every (column, member) sum is formed in
+// ascending k from 0.0 (cluster_spgemm.hpp:129-143 = the row-wise order).
+// Then each member's columns are compacted and ranked and written as CSR.
+// Routed after the symbolic pass: K == 2, products >= 2 x outputs, <= 256
+// outputs per member (the table has 512 slots).
+// ---------------------------------------------------------------------------
+constexpr int CH_WARPS = 4, CH_HS = 512, CH_MAX = 256;
+struct ClusterHaccShared {
+    int32_t key[CH_WARPS][CH_HS];
+    uint32_t pres[CH_WARPS][CH_HS];  // live-member bits of each slot
+    double val[CH_WARPS][CH_HS][2];
+    uint16_t order[CH_WARPS][CH_HS];  // union rank -> compacted entry
+};
+
+__global__ void __launch_bounds__(CH_WARPS * 32)
+    cluster_hashacc_kernel(ClusterMats m, const int32_t* __restrict__ ids, int64_t n,
+                           const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
+                           double* __restrict__ oval) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ClusterHaccShared& s = *reinterpret_cast<ClusterHaccShared*>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t* keys = s.key[warp];
+    uint32_t* pres = s.pres[warp];
+    double(*vals)[2] = s.val[warp];
+    uint16_t* order = s.order[warp];
+    constexpr int LG = 31 - __builtin_clz(static_cast<unsigned>(CH_HS));
+    constexpr int PER = CH_HS / 32;  // union entries per lane (<= 2 x CH_MAX)
+    const unsigned below = (1u << lane) - 1u;
+    for (int64_t t = blockIdx.x * int64_t{CH_WARPS} + warp; t < n;
+         t += int64_t{gridDim.x} * CH_WARPS) {
+        const int32_t c = ids[t];
+        for (int i = lane; i < CH_HS; i += 32) {
+            keys[i] = -1;
+            pres[i] = 0u;
+        }
+        __syncwarp();
+        const int64_t u0 = m.ccp[c], u1 = m.ccp[c + 1], vb = m.vptr[c];
+        for (int64_t ub = u0; ub < u1; ub += 32) {
+            const int64_t u = ub + lane;
+            int64_t b0 = 0;
+            int len = 0;
+            uint32_t mk = 0;
+            double a0 = 0.0, a1 = 0.0;
+            if (u < u1) {
+                mk = __ldg(m.mask + u) & 3u;
+                if (mk) {
+                    const int32_t k = __ldg(m.ccol + u);
+                    b0 = __ldg(m.brp + k);
+                    len = static_cast<int>(__ldg(m.brp + k + 1) - b0);
+                    a0 = __ldg(m.aval + vb + (u - u0) * 2);
+                    a1 = __ldg(m.aval + vb + (u - u0) * 2 + 1);
+                }
+            }
+            unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+            while (ne) {
+                const int j = __ffs(ne) - 1;
+                ne &= ne - 1;
+                const int64_t bj = __shfl_sync(0xffffffffu, b0, j);
+                const int lj = __shfl_sync(0xffffffffu, len, j);
+                const uint32_t mj = __shfl_sync(0xffffffffu, mk, j);
+                const double aj0 = __shfl_sync(0xffffffffu, a0, j);
+                const double aj1 = __shfl_sync(0xffffffffu, a1, j);
+                for (int q = lane; q < lj; q += 32) {
+                    const int32_t col = __ldg(m.bcol + bj + q);
+                    const double bv = __ldg(m.bval + bj + q);
+                    uint32_t slot = col_hash(static_cast<uint32_t>(col), LG);
+                    for (;;) {
+                        const int32_t prev = atomicCAS(&keys[slot], -1, col);
+                        if (prev == -1 || prev == col) break;
+                        slot = (slot + 1) & (CH_HS - 1);
+                    }
+                    const uint32_t had = pres[slot];
+                    if (mj & 1u)
+                        vals[slot][0] =
+                            __dadd_rn((had & 1u) ? vals[slot][0] : 0.0, __dmul_rn(aj0, bv));
+                    if (mj & 2u)
+                        vals[slot][1] =
+                            __dadd_rn((had & 2u) ? vals[slot][1] : 0.0, __dmul_rn(aj1, bv));
+                    pres[slot] = had | mj;
+                }
+                __syncwarp();  // the next B row adds after this one (ascending k)
+            }
+        }
+        // compact the union's slots to the front (ascending slot order; a block
+        // of 32 slots is read before any position inside it is written)
+        int U = 0;
+        for (int i0 = 0; i0 < CH_HS; i0 += 32) {
+            const int32_t kk = keys[i0 + lane];
+            const uint32_t pp = pres[i0 + lane];
+            const double v0 = vals[i0 + lane][0], v1 = vals[i0 + lane][1];
+            const unsigned occ = __ballot_sync(0xffffffffu, kk >= 0);
+            __syncwarp();
+            if (kk >= 0) {
+                const int pos = U + __popc(occ & below);
+                keys[pos] = kk;
+                pres[pos] = pp;
+                vals[pos][0] = v0;
+                vals[pos][1] = v1;
+            }
+            U += __popc(occ);
+            __syncwarp();
+        }
+        // union rank of each entry (counting against the compacted keys,
+        // read as warp broadcasts), then order[rank] = entry
+        int32_t mk[PER];
+        int rk[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int e = u * 32 + lane;
+            mk[u] = e < U ? keys[e] : 0x7fffffff;
+            rk[u] = 0;
+        }
+        const int nu = (U + 31) >> 5;
+        for (int jj = 0; jj < U; ++jj) {
+            const int32_t kj = keys[jj];
+#pragma unroll
+            for (int u = 0; u < PER; ++u)
+                if (u < nu) rk[u] += kj < mk[u];
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u)
+            if (u * 32 + lane < U) order[rk[u]] = static_cast<uint16_t>(u * 32 + lane);
+        __syncwarp();
+        // each member's columns in ascending order: ballot prefix -> coalesced stores
+        const int64_t mb = m.member_ptr[c];
+        const int64_t base0 = crp[m.row_map[mb]], base1 = crp[m.row_map[mb + 1]];
+        int n0 = 0, n1 = 0;
+        for (int i0 = 0; i0 < U; i0 += 32) {
+            const int i = i0 + lane;
+            const int e = i < U ? order[i] : 0;
+            const uint32_t pm = i < U ? pres[e] : 0u;
+            const unsigned m0 = __ballot_sync(0xffffffffu, pm & 1u);
+            const unsigned m1 = __ballot_sync(0xffffffffu, (pm >> 1) & 1u);
+            if (pm & 1u) {
+                const int64_t q = base0 + n0 + __popc(m0 & below);
+                ocol[q] = keys[e];
+                oval[q] = vals[e][0];
+            }
+            if (pm & 2u) {
+                const int64_t q = base1 + n1 + __popc(m1 & below);
+                ocol[q] = keys[e];
+                oval[q] = vals[e][1];
+            }
+            n0 += __popc(m0);
+            n1 += __popc(m1);
+        }
+        __syncwarp();
+    }
+}
+
+// After the symbolic pass: clusters of two rows with products >= 2 x outputs and
+// <= CH_MAX outputs per member go to cluster_hashacc_kernel (hlist); the others
+// keep their class (tlists, per-class cursors).
+__global__ void route_cluster_kernel(ClusterMats m, const int32_t* __restrict__ lists,
+                                     const uint8_t* __restrict__ ccls, int64_t nlist,
+                                     const int64_t* __restrict__ crp,
+                                     unsigned long long* __restrict__ cursor,
+                                     int32_t* __restrict__ hlist, int32_t* __restrict__ tlists) {
+    const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (t >= nlist) return;
+    const int32_t c = lists[t];
+    const int64_t mb = m.member_ptr[c];
+    bool hash = false;
+    if (m.member_ptr[c + 1] - mb == 2) {
+        const int32_t r0 = m.row_map[mb], r1 = m.row_map[mb + 1];
+        const int64_t z0 = crp[r0 + 1] - crp[r0], z1 = crp[r1 + 1] - crp[r1];
+        int64_t P = 0;
+        for (int64_t u = m.ccp[c]; u < m.ccp[c + 1]; ++u) {
+            const int32_t k = m.ccol[u];
+            P += static_cast<int64_t>(__popc(m.mask[u])) * (m.brp[k + 1] - m.brp[k]);
+        }
+        hash = z0 <= CH_MAX && z1 <= CH_MAX && P >= 2 * (z0 + z1);
+    }
+    if (hash)
+        hlist[atomicAdd(&cursor[0], 1ull)] = c;
+    else
+        tlists[atomicAdd(&cursor[ccls[c]], 1ull)] = c;
+}
+
 template <int T, int CAPM>
 void launch_cluster(bsp_handle h, const ClusterMats& m, const int32_t* ids, int64_t n, int cbits,
                     const int64_t* crp, int32_t* ocol, double* oval) {
@@ -383,7 +872,9 @@ void launch_cluster(bsp_handle h, const ClusterMats& m, const int32_t* ids, int6
 void run_cluster_classes(bsp_handle h, const ClusterMats& m, const int32_t* lists,
                          const int64_t* off, const int64_t* cnt, int cbits, const int64_t* crp,
                          int32_t* ocol, double* oval) {
-    static_assert(NCC == 6, "one launch per cluster tile class");
+    static_assert(NCC == 8, "one launch per cluster tile class");
+    launch_union<256, 2048>(h, m, lists + off[7], cnt[7], crp, ocol, oval);
+    launch_union<128, 1024>(h, m, lists + off[6], cnt[6], crp, ocol, oval);
     launch_cluster<64, 512>(h, m, lists + off[1], cnt[1], cbits, crp, ocol, oval);
     launch_cluster<128, 1024>(h, m, lists + off[2], cnt[2], cbits, crp, ocol, oval);
     launch_cluster<256, 2048>(h, m, lists + off[3], cnt[3], cbits, crp, ocol, oval);
@@ -904,8 +1395,11 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         BSP_CUDA(cudaMemsetAsync(skip.p, 0, std::max<int64_t>(n, 1), h->stream));
         DBuf<unsigned long long> counts(h, NCC);
         BSP_CUDA(cudaMemsetAsync(counts.p, 0, NCC * sizeof(unsigned long long), h->stream));
+        // BSP_CLUSTER_UNION=0: member-keyed tiles only
+        const char* ue = std::getenv("BSP_CLUSTER_UNION");
+        const int union_ok = (ue && ue[0] == '0') ? 0 : 1;
         BSP_LAUNCH(h, cluster_products_kernel, grid_for(h, ncl, 256), 256, 0, cm, ncl, cbits, ccls.p,
-                   skip.p, counts.p);
+                   skip.p, counts.p, union_ok);
         unsigned long long hc[NCC];
         d2h(h, hc, counts.p, NCC);
         sync(h);
@@ -928,7 +1422,9 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         RowwisePlan plan;    // rows outside cluster tiles (incl. heavy windows)
         RowwisePlan plan_c;  // the cluster tiles' rows, for their symbolic counts
         build_plan(h, m, 0, n, skip.p, plan, nullptr, nullptr, &plan_c);
-        h->stats.units[10] = cnt[1] + cnt[2] + cnt[3] + cnt[4] + cnt[5];  // cluster tiles
+        for (int c = 0; c < NCLS; ++c) h->stats.products += plan_c.class_products[c];  // + cluster rows
+        h->stats.units[10] = acc;  // cluster tiles (member-keyed + union)
+        h->stats.units[11] = cnt[6] + cnt[7];  // of which union tiles
         DBuf<int64_t> row_nnz(h, n + 1);
         BSP_CUDA(cudaMemsetAsync(row_nnz.p, 0, (n + 1) * sizeof(int64_t), h->stream));
         // Symbolic: C's row structure does not depend on the clustering, so the
@@ -938,6 +1434,13 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
             DBuf<int64_t> wn_c;
             plan_symbolic(h, m, plan_c, row_nnz.p, wn_c);
         }
+        // the union tiles' rows: counted from each cluster's B rows loaded once
+        if (cnt[6] > 0)
+            BSP_LAUNCH_AS(h, "cluster_union_count<128,2048>", (cluster_union_count_kernel<128, 2048>),
+                          static_cast<unsigned>(cnt[6]), 128, 0, cm, lists.p + off[6], row_nnz.p);
+        if (cnt[7] > 0)
+            BSP_LAUNCH_AS(h, "cluster_union_count<256,4096>", (cluster_union_count_kernel<256, 4096>),
+                          static_cast<unsigned>(cnt[7]), 256, 0, cm, lists.p + off[7], row_nnz.p);
         DBuf<int64_t> win_nnz;
         plan_symbolic(h, m, plan, row_nnz.p, win_nnz);
         DBuf<int64_t> rp(h, n + 1, Pool::out);
@@ -947,7 +1450,40 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         const int64_t nnz = read_scalar(h, rp.p + n);
         h->stats.nnz_out = nnz;
         ResultPayload pay(h, nnz);
-        run_cluster_classes(h, cm, lists.p, off, cnt, cbits, rp.p, pay.col_idx(), pay.values());
+        // duplicate-heavy two-row clusters -> the cluster hash accumulator
+        // (only when columns repeat overall: compression factor >= 1.25, as
+        // the row-wise routing; BSP_HACC=0 disables)
+        const char* he = std::getenv("BSP_HACC");
+        const bool repeats = 4 * h->stats.products >= 5 * std::max<int64_t>(1, nnz);
+        if (acc > 0 && repeats && !(he && he[0] == '0')) {
+            DBuf<int32_t> hl(h, acc), tl(h, acc);
+            DBuf<unsigned long long> cur(h, NCC);
+            std::vector<unsigned long long> cu(NCC, 0);
+            for (int c = 1; c < NCC; ++c) cu[c] = static_cast<unsigned long long>(off[c] - off[1]);
+            h2d(h, cur.p, cu.data(), NCC);
+            BSP_LAUNCH(h, route_cluster_kernel, static_cast<unsigned>(div_up(acc, 256)), 256, 0, cm,
+                       lists.p + off[1], ccls.p, acc, rp.p, cur.p, hl.p, tl.p);
+            unsigned long long hc2[NCC];
+            d2h(h, hc2, cur.p, NCC);
+            sync(h);
+            const int64_t nh = static_cast<int64_t>(hc2[0]);
+            int64_t off2[NCC], cnt2[NCC];
+            for (int c = 0; c < NCC; ++c) {
+                off2[c] = c == 0 ? 0 : off[c] - off[1];
+                cnt2[c] = c == 0 ? 0 : static_cast<int64_t>(hc2[c]) - off2[c];
+            }
+            if (nh > 0) {
+                set_smem(cluster_hashacc_kernel, sizeof(ClusterHaccShared));
+                const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+                    1, std::min<int64_t>(div_up(nh, CH_WARPS), int64_t{h->sm_count} * 32)));
+                BSP_LAUNCH(h, cluster_hashacc_kernel, grid, CH_WARPS * 32, sizeof(ClusterHaccShared),
+                           cm, hl.p, nh, rp.p, pay.col_idx(), pay.values());
+            }
+            h->stats.units[12] = nh;
+            run_cluster_classes(h, cm, tl.p, off2, cnt2, cbits, rp.p, pay.col_idx(), pay.values());
+        } else {
+            run_cluster_classes(h, cm, lists.p, off, cnt, cbits, rp.p, pay.col_idx(), pay.values());
+        }
         plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values());
         C->nrows = n;
         C->ncols = B->ncols;

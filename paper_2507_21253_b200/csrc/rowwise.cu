@@ -86,7 +86,9 @@ __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restri
                 c = 1;
                 while (c < NCLS - 1 && P > kClassCap[c]) ++c;
             }
-            if (skip && skip[r]) c = (shadow && c > 0) ? NCLS + c : 0;
+            // skip 1: planned apart in the shadow plan; 2: counted elsewhere
+            // (cluster union tiles count their own rows)
+            if (skip && skip[r]) c = (shadow && c > 0 && skip[r] == 1) ? NCLS + c : 0;
             if (prod) prod[r] = P;
             cls[r] = static_cast<uint8_t>(c);
             atomicAdd(&s_cnt[c], 1ull);
