@@ -9,6 +9,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 
@@ -154,6 +155,26 @@ __global__ void readback_kernel(const unsigned char* __restrict__ src,
 }
 }  // namespace
 
+namespace {
+thread_local std::chrono::steady_clock::time_point g_sync_ret{};
+thread_local bool g_sync_set = false;
+}  // namespace
+bool gap_log_enabled() {
+    static const bool on = std::getenv("BSP_GAP_LOG") != nullptr;
+    return on;
+}
+void gap_mark_sync() {
+    g_sync_ret = std::chrono::steady_clock::now();
+    g_sync_set = true;
+}
+void gap_check_launch(const char* name) {
+    if (!g_sync_set) return;
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - g_sync_ret).count();
+    g_sync_set = false;
+    if (ms > 1.0) std::fprintf(stderr, "[gap] %.2f ms host time before %s\n", ms, name);
+}
+
 void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes) {
     if (!h->rb_host) {
         BSP_CUDA(cudaHostAlloc(&h->rb_host, kReadbackBytes, cudaHostAllocMapped));
@@ -163,6 +184,7 @@ void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes) {
                static_cast<unsigned char*>(h->rb_dev), bytes);
     BSP_CUDA(cudaStreamSynchronize(h->stream));
     std::memcpy(dst, h->rb_host, bytes);
+    if (gap_log_enabled()) gap_mark_sync();
 }
 
 size_t available_bytes(bsp_handle h) {
@@ -226,6 +248,10 @@ int bsp_destroy(bsp_handle h) {
         if (!h) return;
         cudaStreamSynchronize(h->stream);
         if (h->comm) bsp_comm_destroy(h);
+        if (h->keep_starts) {
+            cudaFreeAsync(h->keep_starts, h->stream);
+            cudaStreamSynchronize(h->stream);
+        }
         if (h->own_stream) cudaStreamDestroy(h->stream);
         // pools with live allocations (results still held by the caller) are
         // released by the driver once those are freed

@@ -47,6 +47,12 @@ struct bsp_handle_s {
     int comm_rank = 0, comm_size = 1;
     // bsp_spgemm_rowwise_sharded's row split of the last (A, B) pair (the split
     // needs every row's products: computed once, reused while A and B stay)
+    // Start tables of the heavy-row planner (the largest scratch buffer, GBs on
+    // cfg5), kept across multiplies and grown on demand: a fresh multi-GB pool
+    // allocation now and then had to map new memory (a 30-80 ms host stall
+    // between two kernels of a multiply).
+    void* keep_starts = nullptr;
+    size_t keep_starts_bytes = 0;
     const void* part_key[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t part_nnz[2] = {0, 0};
     std::vector<int64_t> part_bounds;
@@ -69,6 +75,7 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define BSP_LAUNCH_AS(h, name, kernel, grid, block, smem, ...)                         \
     do {                                                                               \
         if ((grid) > 0) {                                                              \
+            if (::bsp::gap_log_enabled()) ::bsp::gap_check_launch(name);               \
             const int prof_slot_ = ::bsp::prof_begin(h);                               \
             kernel<<<(grid), (block), (smem), (h)->stream>>>(__VA_ARGS__);             \
             ::bsp::cuda_check(cudaGetLastError(), name);                               \
@@ -141,20 +148,30 @@ struct DBuf {
         : h(hh), p(dalloc<T>(hh, nn, pool)), n(nn) {}
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : h(o.h), p(o.p), n(o.n) { o.p = nullptr; }
+    // non-owning view of a buffer that outlives this object (handle caches)
+    static DBuf borrow(T* q, int64_t nn) {
+        DBuf d;
+        d.p = q;
+        d.n = nn;
+        d.own = false;
+        return d;
+    }
+    DBuf(DBuf&& o) noexcept : h(o.h), p(o.p), n(o.n), own(o.own) { o.p = nullptr; }
     DBuf& operator=(DBuf&& o) noexcept {
         reset();
         h = o.h;
         p = o.p;
         n = o.n;
+        own = o.own;
         o.p = nullptr;
         return *this;
     }
     ~DBuf() { reset(); }
     void reset() {
-        if (p) dfree(h, p);
+        if (p && own) dfree(h, p);
         p = nullptr;
     }
+    bool own = true;
     T* release() {
         T* q = p;
         p = nullptr;
@@ -184,7 +201,15 @@ void h2d(bsp_handle h, T* dst, const T* src, int64_t n) {
     if (n <= 0) return;
     BSP_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, h->stream));
 }
-inline void sync(bsp_handle h) { BSP_CUDA(cudaStreamSynchronize(h->stream)); }
+// BSP_GAP_LOG=1: log host time between a synchronisation's return and the next
+// engine launch when it exceeds 1 ms (diagnoses GPU idle gaps inside a multiply).
+bool gap_log_enabled();
+void gap_mark_sync();
+void gap_check_launch(const char* name);
+inline void sync(bsp_handle h) {
+    BSP_CUDA(cudaStreamSynchronize(h->stream));
+    if (gap_log_enabled()) gap_mark_sync();
+}
 
 template <typename T>
 T read_scalar(bsp_handle h, const T* dptr) {

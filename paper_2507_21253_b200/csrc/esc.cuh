@@ -185,6 +185,7 @@ struct RowwisePlan {
     DBuf<int32_t> sparse_ids, dense_ids;
     DBuf<uint32_t> starts; // planner per-(window, segment) start tables (absolute)
     bool light_sym_done = false;  // light rows counted on the side stream
+    bool keep_tables = false;     // start tables in the handle's kept buffer
     // Set while that side-stream work is not yet joined into the main stream:
     // the destructor joins it before the plan's buffers are freed on the main
     // stream, so an error between build_plan and plan_symbolic cannot free

@@ -1222,14 +1222,31 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         // repeat: cfg3).  Rows in scan order that fit get a table, the rest
         // binary-search.
         constexpr int64_t EB = sizeof(uint32_t);
-        const int64_t avail = static_cast<int64_t>(available_bytes(h));
+        // the kept table buffer counts as available to the tables
+        const int64_t avail = static_cast<int64_t>(available_bytes(h)) +
+                              (plan.keep_tables ? static_cast<int64_t>(h->keep_starts_bytes) : 0);
         const int64_t spare = avail - 12 * h->stats.products - (int64_t{2} << 30);
         const int64_t floor_entries = std::min<int64_t>(int64_t{1} << 30, avail / (16 * EB));
         const int64_t budget = std::min<int64_t>(
             hv[1], std::max<int64_t>(floor_entries,
                                      std::min<int64_t>(int64_t{1} << 31, spare / EB)));
         const bool use_starts = budget > 0 && m.bnnz < (int64_t{1} << 32);
-        if (use_starts) plan.starts = DBuf<uint32_t>(h, budget);
+        if (use_starts) {
+            if (plan.keep_tables) {
+                const size_t bytes = static_cast<size_t>(budget) * sizeof(uint32_t);
+                if (bytes > h->keep_starts_bytes) {
+                    if (h->keep_starts) dfree(h, h->keep_starts);
+                    h->keep_starts = nullptr;
+                    h->keep_starts_bytes = 0;
+                    const size_t want = bytes + bytes / 8;  // headroom for the next call
+                    h->keep_starts = dalloc<unsigned char>(h, static_cast<int64_t>(want));
+                    h->keep_starts_bytes = want;
+                }
+                plan.starts = DBuf<uint32_t>::borrow(static_cast<uint32_t*>(h->keep_starts), budget);
+            } else {
+                plan.starts = DBuf<uint32_t>(h, budget);
+            }
+        }
         plan.wins = DBuf<Window>(h, plan.nwin);
         DBuf<uint8_t> dense(h, plan.nwin);
         set_smem(plan_write_kernel, sizeof(PlanWriteShared));
@@ -1763,6 +1780,7 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     DBuf<int64_t> crp(h, n + 1);
     BSP_CUDA(cudaMemsetAsync(crp.p, 0, (n + 1) * sizeof(int64_t), h->stream));
     RowwisePlan plan;
+    plan.keep_tables = true;
     build_plan(h, m, rb, re, row_skip, plan, nullptr, crp.p);
     // The main window class (2048-product tiles: nearly all heavy products on
     // power-law inputs) is counted by its numeric pass (esc_window_lb_kernel)
@@ -1784,9 +1802,9 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     if (plan.nwin > 0) exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
     int64_t nnz = read_scalar(h, rp.p + n);  // without the look-back class when lb
     int64_t cap = nnz;
+    const int64_t avail = static_cast<int64_t>(available_bytes(h));
     if (lb) {
         cap = nnz + plan.wcls_prod[LBC];
-        const int64_t avail = static_cast<int64_t>(available_bytes(h));
         // C (12 B per entry) + the look-back state, with a 1 GB margin
         if (12 * cap + 16 * nlb + (int64_t{1} << 30) > avail) {
             // no room for the bound: count the class symbolically after all
@@ -1804,7 +1822,6 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
         }
     }
     {
-        const int64_t avail = static_cast<int64_t>(available_bytes(h));
         if (12 * cap > avail)
             throw oom_error("spgemm_rowwise: C needs " + std::to_string(12 * cap >> 20) +
                             " MiB, more than the " + std::to_string(avail >> 20) +
