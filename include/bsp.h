@@ -332,6 +332,20 @@ int bsp_permute_rows(const bsp_host_csr* A, const int32_t* perm, bsp_host_csr* o
 /* reference: transpose (csr.hpp:115-135), host form */
 int bsp_transpose_host(const bsp_host_csr* A, bsp_host_csr* out);
 void bsp_host_csr_free(bsp_host_csr* m);
+
+/* ------------------------------------------------------------------ */
+/* file IO (host; reference matrix_market.hpp)                          */
+/* ------------------------------------------------------------------ */
+/* load_matrix_market (matrix_market.hpp:42-119) + coo_to_csr (csr.hpp:92-113):
+ * coordinate real/integer/pattern, general/symmetric; 1-based -> 0-based;
+ * symmetric files expanded; duplicates summed; BSP_ERR_IO "path:line: msg". */
+int bsp_load_matrix_market(const char* path, bsp_host_csr* out);
+/* write_matrix_market (:122-137): "coordinate real general", %.17g values. */
+int bsp_write_matrix_market(const bsp_host_csr* A, const char* path);
+/* load_permutation (:141-166; ReorderSpec::file, reorder.hpp:185-192): one
+ * integer per line, perm[k] on line k; length and bijectivity checked. */
+int bsp_load_permutation(const char* path, int64_t nrows, int32_t* perm_out);
+int bsp_write_permutation(const int32_t* perm, int64_t n, const char* path);
 void bsp_host_free_plain(void* p);
 
 /* ------------------------------------------------------------------ */

@@ -127,6 +127,10 @@ def ref() -> C.CDLL:
         l.ref_generate_frontiers.argtypes = [i64, i64, vp, vp, i64, i64, u64, P(i64), P(i64),
                                              P(P(i64)), P(P(i64)), P(P(i32))]
         l.ref_free.argtypes = [vp]
+        l.ref_load_matrix_market.argtypes = [C.c_char_p, P(i64), P(i64), P(i64), P(P(i64)),
+                                             P(P(i32)), P(P(dbl))]
+        l.ref_load_permutation.argtypes = [C.c_char_p, i64, vp]
+        l.ref_write_matrix_market.argtypes = [i64, i64, vp, vp, vp, C.c_char_p]
         l.ref_csr_new.argtypes = [i64, i64, vp, vp, vp]
         l.ref_csr_new.restype = vp
         l.ref_csr_delete.argtypes = [vp]
@@ -556,3 +560,26 @@ def ref_time_clusterwise(ac: RefCluster, b: RefCsr, threads: int = 0):
     _ref_check(ref().ref_time_clusterwise_prepared(ac.h, b.h, threads, C.byref(s),
                                                    C.byref(slots)))
     return s.value, slots.value
+
+
+def ref_load_matrix_market(path) -> Csr:
+    """The reference's load_matrix_market + coo_to_csr (matrix_market.hpp:42-119)."""
+    nr, nc, nz = i64(), i64(), i64()
+    crp, cci, cv = P(i64)(), P(i32)(), P(dbl)()
+    _ref_check(ref().ref_load_matrix_market(str(path).encode(), C.byref(nr), C.byref(nc),
+                                            C.byref(nz), C.byref(crp), C.byref(cci), C.byref(cv)))
+    f = ref().ref_free
+    return Csr(nr.value, nc.value, _arr(crp, nr.value + 1, np.int64, f),
+               _arr(cci, nz.value, np.int32, f), _arr(cv, nz.value, np.float64, f))
+
+
+def ref_load_permutation(path, nrows: int) -> np.ndarray:
+    out = np.zeros(nrows, np.int32)
+    _ref_check(ref().ref_load_permutation(str(path).encode(), nrows, _p(out)))
+    return out
+
+
+def ref_write_matrix_market(a, path) -> None:
+    arp, aci, av = _csr_args(a)
+    _ref_check(ref().ref_write_matrix_market(a.nrows, a.ncols, _p(arp), _p(aci), _p(av),
+                                             str(path).encode()))

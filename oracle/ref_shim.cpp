@@ -247,6 +247,34 @@ int ref_time_clusterwise_prepared(const void* ac, const void* b, int num_threads
     });
 }
 
+// Matrix Market / permutation files through the reference's own readers
+// (matrix_market.hpp), for the IO parity tests.
+int ref_load_matrix_market(const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz,
+                           int64_t** crp, int32_t** cci, double** cv) {
+    return guard([&] {
+        CsrMatrix a = coo_to_csr(load_matrix_market(path));
+        std::vector<int64_t> rp(a.row_ptr.begin(), a.row_ptr.end());
+        *nrows = a.nrows;
+        *ncols = a.ncols;
+        *nnz = a.nnz();
+        *crp = dup(rp);
+        *cci = dup(a.col_idx);
+        *cv = dup(a.values);
+    });
+}
+
+int ref_load_permutation(const char* path, int64_t nrows, int32_t* perm) {
+    return guard([&] {
+        const Permutation p = load_permutation(path, static_cast<index_t>(nrows));
+        std::memcpy(perm, p.perm.data(), p.perm.size() * sizeof(int32_t));
+    });
+}
+
+int ref_write_matrix_market(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
+                            const double* v, const char* path) {
+    return guard([&] { write_matrix_market(make(nrows, ncols, rp, ci, v), path); });
+}
+
 int ref_build_cluster_dims(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
                            int64_t nclusters, const int64_t* cptr, const int32_t* crows,
                            int64_t* colslots, int64_t* slots, int64_t* placeholders,

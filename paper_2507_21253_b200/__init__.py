@@ -35,7 +35,9 @@ __all__ = [
     "reorder_degree", "reorder_rcm", "bandwidth", "transpose", "generate_frontiers", "binarize",
     "permute_symmetric",
     "permute_rows", "coo_to_csr", "csr_equal_canonical", "gen_er", "gen_hidden_clusters",
-    "gen_rmat", "gen_stencil27", "make_config", "CONFIGS",
+    "gen_rmat", "gen_stencil27", "make_config", "CONFIGS", "load_matrix_market",
+    "write_matrix_market", "load_permutation", "write_permutation", "ReorderSpec",
+    "make_permutation",
 ]
 
 
@@ -888,6 +890,63 @@ def permute_rows(a: CsrMatrix, p: Permutation) -> CsrMatrix:
     ha, out = a._host(), L.bsp_host_csr()
     _check(L.load().bsp_permute_rows(C.byref(ha), _ptr(p.perm), C.byref(out)))
     return CsrMatrix._adopt(out)
+
+
+# ---------------------------------------------------------------------------
+# file IO and reorder specs (reference matrix_market.hpp, reorder.hpp:183-192)
+# ---------------------------------------------------------------------------
+def load_matrix_market(path: str) -> CsrMatrix:
+    """reference load_matrix_market + coo_to_csr (matrix_market.hpp:42-119)."""
+    out = L.bsp_host_csr()
+    _check(L.load().bsp_load_matrix_market(str(path).encode(), C.byref(out)))
+    return CsrMatrix._adopt(out)
+
+
+def write_matrix_market(a: CsrMatrix, path: str) -> None:
+    """reference write_matrix_market (matrix_market.hpp:122-137)."""
+    ha = a._host()
+    _check(L.load().bsp_write_matrix_market(C.byref(ha), str(path).encode()))
+
+
+def load_permutation(path: str, nrows: int) -> Permutation:
+    """reference load_permutation (matrix_market.hpp:141-166)."""
+    p = np.zeros(nrows, np.int32)
+    _check(L.load().bsp_load_permutation(str(path).encode(), nrows, _ptr(p)))
+    return Permutation.from_perm(p)
+
+
+def write_permutation(p: Permutation, path: str) -> None:
+    """reference write_permutation (matrix_market.hpp:168-173)."""
+    perm = np.ascontiguousarray(p.perm, np.int32)
+    _check(L.load().bsp_write_permutation(_ptr(perm), perm.size, str(path).encode()))
+
+
+@dataclass
+class ReorderSpec:
+    """reference ReorderSpec (reorder.hpp:183-192): original, random (seed),
+    degree, rcm, or an external permutation file (graph / hypergraph
+    partitioning orders)."""
+    method: str = "original"
+    seed: int = 0
+    path: str = ""
+
+    def name(self) -> str:  # reference reorder_name (bench.hpp:51-59)
+        return f"file:{self.path}" if self.method == "file" else self.method
+
+
+def make_permutation(spec: ReorderSpec, a: CsrMatrix) -> Permutation:
+    """reference detail::make_permutation (bench.hpp:119-127)."""
+    if spec.method == "original":
+        return Permutation.identity(a.nrows)
+    if spec.method == "random":
+        return reorder_random(a.nrows, spec.seed)
+    if spec.method == "degree":
+        return reorder_degree(a)
+    if spec.method == "rcm":
+        return reorder_rcm(a)
+    if spec.method == "file":
+        return load_permutation(spec.path, a.nrows)
+    raise ContractError(f"unknown reorder method '{spec.method}'")
 
 
 # ---------------------------------------------------------------------------

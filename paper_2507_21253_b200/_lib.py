@@ -137,6 +137,10 @@ SIGNATURES = {
     "bsp_gen_hidden_clusters": (C.c_int, [i64, i32, i32, dbl, dbl, u64, u64, P(bsp_host_csr)]),
     "bsp_gen_rmat": (C.c_int, [i32, i32, dbl, dbl, dbl, u64, P(bsp_host_csr)]),
     "bsp_gen_stencil27": (C.c_int, [i32, i64, P(bsp_host_csr)]),
+    "bsp_load_matrix_market": (C.c_int, [C.c_char_p, P(bsp_host_csr)]),
+    "bsp_write_matrix_market": (C.c_int, [P(bsp_host_csr), C.c_char_p]),
+    "bsp_load_permutation": (C.c_int, [C.c_char_p, i64, vp]),
+    "bsp_write_permutation": (C.c_int, [vp, i64, C.c_char_p]),
     "bsp_nccl_unique_id": (C.c_int, [vp]),
     "bsp_comm_init": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "bsp_comm_destroy": (C.c_int, [vp]),
