@@ -15,6 +15,8 @@
 #include "bsp.h"
 
 #include <cstdint>
+#include <limits>
+#include <type_traits>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -100,10 +102,14 @@ Csr spgemm_rowwise(const Csr& a, const Csr& b, int /*num_threads*/ = 0,
     return detail::download<Csr>(e, dc);
 }
 
-// reference spgemm.hpp:41-63 (per-row exact output counts).
+// reference spgemm.hpp:41-63 (per-row exact output counts), in the matrix's
+// own index type (cspgemm::index_t for the reference's CsrMatrix); a row's count
+// always fits (< 2^31 outputs per row).
 template <class Csr>
-std::vector<int64_t> spgemm_symbolic(const Csr& a, const Csr& b, int /*num_threads*/ = 0,
-                                     Engine& e = default_engine()) {
+auto spgemm_symbolic(const Csr& a, const Csr& b, int /*num_threads*/ = 0,
+                     Engine& e = default_engine())
+    -> std::vector<typename std::decay<decltype(a.row_ptr[0])>::type> {
+    using Idx = typename std::decay<decltype(a.row_ptr[0])>::type;
     if (a.ncols != b.nrows) throw contract_error("spgemm: dimension mismatch (a.ncols != b.nrows)");
     bsp_csr da = detail::upload(e, a), db = detail::upload(e, b);
     // counts land in a device buffer owned by a CSR-shaped scratch
@@ -119,8 +125,7 @@ std::vector<int64_t> spgemm_symbolic(const Csr& a, const Csr& b, int /*num_threa
     bsp_csr_free(e.get(), &db);
     bsp_csr_free(e.get(), &da);
     check(rc);
-    counts.resize(static_cast<size_t>(a.nrows));
-    return counts;
+    return std::vector<Idx>(counts.begin(), counts.begin() + a.nrows);
 }
 
 // reference cluster_spgemm.hpp:186-189 with the CSR_Cluster built on the
@@ -147,6 +152,134 @@ Csr spgemm_clusterwise(const Csr& a, const Assignment& asg, const Csr& b, int /*
     bsp_csr_free(e.get(), &da);
     check(rc);
     return detail::download<Csr>(e, dc);
+}
+
+namespace detail {
+
+template <class Csr>
+bsp_host_csr host_view(const Csr& a, std::vector<int64_t>& rp) {
+    rp.assign(a.row_ptr.begin(), a.row_ptr.end());
+    bsp_host_csr h{};
+    h.nrows = a.nrows;
+    h.ncols = a.ncols;
+    h.nnz = rp.empty() ? 0 : rp.back();
+    h.row_ptr = rp.data();
+    h.col_idx = const_cast<int32_t*>(reinterpret_cast<const int32_t*>(a.col_idx.data()));
+    h.values = const_cast<double*>(a.values.data());
+    return h;
+}
+
+// A flattened assignment (library-malloc'ed) into the caller's type, which
+// has `clusters` (a vector of member vectors), like cspgemm::ClusterAssignment.
+template <class Assignment>
+Assignment adopt_assignment(int64_t nc, int64_t* ptr, int32_t* rows) {
+    Assignment asg;
+    asg.clusters.resize(static_cast<size_t>(nc));
+    for (int64_t c = 0; c < nc; ++c)
+        asg.clusters[c].assign(rows + ptr[c], rows + ptr[c + 1]);
+    bsp_host_free_plain(ptr);
+    bsp_host_free_plain(rows);
+    return asg;
+}
+
+template <class Perm>
+Perm adopt_perm(std::vector<int32_t>& p) {
+    return Perm::from_perm({p.begin(), p.end()});
+}
+
+}  // namespace detail
+
+// reference spgemm_topk (spgemm.hpp:144-206): the candidate list element for
+// element (order, scores bitwise).  Pair: the caller's pair type with members
+// i, j, score (cspgemm::CandidatePair), default bsp_candidate.
+template <class Pair = bsp_candidate, class Csr>
+std::vector<Pair> spgemm_topk(const Csr& a, const Csr& a_t, int topk, double jacc_th,
+                              int /*num_threads*/ = 0, Engine& e = default_engine()) {
+    if (a.ncols != a_t.nrows) throw contract_error("spgemm_topk: dimension mismatch");
+    bsp_csr da = detail::upload(e, a), dt = detail::upload(e, a_t);
+    bsp_candidate* pairs = nullptr;
+    int64_t n = 0;
+    const int rc = bsp_spgemm_topk(e.get(), &da, &dt, topk, jacc_th, &pairs, &n);
+    bsp_csr_free(e.get(), &dt);
+    bsp_csr_free(e.get(), &da);
+    check(rc);
+    std::vector<Pair> out(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+        out[k].i = pairs[k].i;
+        out[k].j = pairs[k].j;
+        out[k].score = pairs[k].score;
+    }
+    bsp_host_free_plain(pairs);
+    return out;
+}
+
+// reference hierarchical_clusters (clustering.hpp:109-185): GPU top-k
+// candidates + the reference's merge rule; the assignment is identical.
+// Params: any type with jacc_th and max_cluster_th (cspgemm::ClusterParams).
+template <class Assignment, class Csr, class Params>
+Assignment hierarchical_clusters(const Csr& a, const Params& prm, int /*num_threads*/ = 0,
+                                 Engine& e = default_engine()) {
+    std::vector<int64_t> rp;
+    bsp_host_csr h = detail::host_view(a, rp);
+    int64_t nc = 0, *ptr = nullptr;
+    int32_t* rows = nullptr;
+    check(bsp_hierarchical_clusters(e.get(), &h, prm.jacc_th, prm.max_cluster_th, 0, 64, 32, 1,
+                                    &nc, &ptr, &rows));
+    return detail::adopt_assignment<Assignment>(nc, ptr, rows);
+}
+
+// reference variable_length_clusters (clustering.hpp:76-93) / fixed (:59-69).
+template <class Assignment, class Csr, class Params>
+Assignment variable_length_clusters(const Csr& a, const Params& prm) {
+    std::vector<int64_t> rp;
+    bsp_host_csr h = detail::host_view(a, rp);
+    int64_t nc = 0, *ptr = nullptr;
+    int32_t* rows = nullptr;
+    check(bsp_variable_length_clusters(&h, prm.jacc_th, prm.max_cluster_th, &nc, &ptr, &rows));
+    return detail::adopt_assignment<Assignment>(nc, ptr, rows);
+}
+
+template <class Assignment>
+Assignment fixed_length_clusters(int64_t nrows, int k) {
+    int64_t nc = 0, *ptr = nullptr;
+    int32_t* rows = nullptr;
+    check(bsp_fixed_length_clusters(nrows, k, &nc, &ptr, &rows));
+    return detail::adopt_assignment<Assignment>(nc, ptr, rows);
+}
+
+// reference reorder_rcm / reorder_degree / reorder_random (reorder.hpp:20-181)
+// and load_permutation (matrix_market.hpp:141-166); Perm has from_perm
+// (cspgemm::Permutation).
+template <class Perm, class Csr>
+Perm reorder_rcm(const Csr& a) {
+    std::vector<int64_t> rp;
+    bsp_host_csr h = detail::host_view(a, rp);
+    std::vector<int32_t> p(static_cast<size_t>(a.nrows));
+    check(bsp_reorder_rcm(&h, p.data()));
+    return detail::adopt_perm<Perm>(p);
+}
+
+template <class Perm, class Csr>
+Perm reorder_degree(const Csr& a) {
+    std::vector<int64_t> rp;
+    bsp_host_csr h = detail::host_view(a, rp);
+    std::vector<int32_t> p(static_cast<size_t>(a.nrows));
+    check(bsp_reorder_degree(&h, p.data()));
+    return detail::adopt_perm<Perm>(p);
+}
+
+template <class Perm>
+Perm reorder_random(int64_t n, uint64_t seed) {
+    std::vector<int32_t> p(static_cast<size_t>(n));
+    check(bsp_reorder_random(n, seed, p.data()));
+    return detail::adopt_perm<Perm>(p);
+}
+
+template <class Perm>
+Perm load_permutation(const std::string& path, int64_t nrows) {
+    std::vector<int32_t> p(static_cast<size_t>(nrows));
+    check(bsp_load_permutation(path.c_str(), nrows, p.data()));
+    return detail::adopt_perm<Perm>(p);
 }
 
 }  // namespace bsp_gpu

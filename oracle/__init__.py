@@ -131,6 +131,10 @@ def ref() -> C.CDLL:
                                              P(P(i32)), P(P(dbl))]
         l.ref_load_permutation.argtypes = [C.c_char_p, i64, vp]
         l.ref_write_matrix_market.argtypes = [i64, i64, vp, vp, vp, C.c_char_p]
+        l.ref_fmt_double.argtypes = [dbl, C.c_char_p, C.c_int]
+        l.ref_bench_csv_row.argtypes = [C.c_char_p, C.c_int, C.c_int, u64, C.c_char_p, C.c_int,
+                                        dbl, C.c_int, C.c_int, C.c_int, C.c_int, u64, C.c_int,
+                                        C.c_int, C.c_int, vp, vp, dbl, dbl, C.c_char_p, C.c_int]
         l.ref_csr_new.argtypes = [i64, i64, vp, vp, vp]
         l.ref_csr_new.restype = vp
         l.ref_csr_delete.argtypes = [vp]
@@ -583,3 +587,25 @@ def ref_write_matrix_market(a, path) -> None:
     arp, aci, av = _csr_args(a)
     _ref_check(ref().ref_write_matrix_market(a.nrows, a.ncols, _p(arp), _p(aci), _p(av),
                                              str(path).encode()))
+
+
+def ref_fmt_double(v: float) -> str:
+    """std::to_chars(double) as the reference's CSV writer uses it."""
+    buf = C.create_string_buffer(64)
+    _ref_check(ref().ref_fmt_double(v, buf, 64))
+    return buf.value.decode()
+
+
+def ref_bench_csv_row(matrix, workload, reorder_method, reorder_seed, reorder_path,
+                      cluster_method, jacc_th, max_cluster, fixed_len, nf, fb, fseed, reps,
+                      threads, warmup, d9, u6, ratio, amort):
+    """(row, header) as the reference's bench_csv_row / bench_csv_header print them."""
+    d = np.ascontiguousarray(d9, np.float64)
+    u = np.ascontiguousarray(u6, np.uint64)
+    buf = C.create_string_buffer(1 << 12)
+    _ref_check(ref().ref_bench_csv_row(str(matrix).encode(), workload, reorder_method, reorder_seed,
+                                       str(reorder_path).encode(), cluster_method, jacc_th,
+                                       max_cluster, fixed_len, nf, fb, fseed, reps, threads,
+                                       warmup, _p(d), _p(u), ratio, amort, buf, 1 << 12))
+    row, header = buf.value.decode().split("\n")
+    return row, header

@@ -5,6 +5,9 @@
 // the reference's own CPU path (cpu_baseline kind "reference").  Nothing in
 // the product links this library.
 #include "cspgemm/cspgemm.hpp"
+#include "cspgemm/bench.hpp"
+
+#include <charconv>
 
 #include <cstdlib>
 #include <cstring>
@@ -273,6 +276,60 @@ int ref_load_permutation(const char* path, int64_t nrows, int32_t* perm) {
 int ref_write_matrix_market(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,
                             const double* v, const char* path) {
     return guard([&] { write_matrix_market(make(nrows, ncols, rp, ci, v), path); });
+}
+
+// The reference's CSV report row (bench.hpp:260-290) from plain fields, and its
+// double formatting (std::to_chars), for the harness parity tests.
+int ref_fmt_double(double v, char* out, int cap) {
+    return guard([&] {
+        const auto r = std::to_chars(out, out + cap - 1, v);
+        *r.ptr = 0;
+    });
+}
+
+int ref_bench_csv_row(const char* matrix, int workload, int reorder_method, uint64_t reorder_seed,
+                      const char* reorder_path, int cluster_method, double jacc_th,
+                      int max_cluster, int fixed_len, int nf, int fb, uint64_t fseed, int reps,
+                      int threads, int warmup, const double* d9, const uint64_t* u6,
+                      double ratio, double amort, char* out, int cap) {
+    return guard([&] {
+        BenchReport r;
+        r.config.matrix_path = matrix;
+        r.config.workload = workload == 0 ? Workload::a_squared : Workload::tall_skinny;
+        r.config.reorder.method = static_cast<ReorderSpec::Method>(reorder_method);
+        r.config.reorder.seed = reorder_seed;
+        r.config.reorder.path = reorder_path;
+        r.config.clustering.method = static_cast<ClusteringSpec::Method>(cluster_method);
+        r.config.clustering.params.jacc_th = jacc_th;
+        r.config.clustering.params.max_cluster_th = max_cluster;
+        r.config.clustering.params.fixed_len = fixed_len;
+        r.config.num_frontiers = nf;
+        r.config.frontier_batch = fb;
+        r.config.frontier_seed = fseed;
+        r.config.repetitions = reps;
+        r.config.threads = threads;
+        r.config.warmup = warmup != 0;
+        r.reorder_seconds = d9[0];
+        r.cluster_build_seconds = d9[1];
+        r.baseline_mean_s = d9[2];
+        r.baseline_min_s = d9[3];
+        r.baseline_max_s = d9[4];
+        r.variant_mean_s = d9[5];
+        r.variant_min_s = d9[6];
+        r.variant_max_s = d9[7];
+        r.speedup_vs_baseline = d9[8];
+        r.footprint.csr_bytes = u6[0];
+        r.footprint.cluster_bytes = u6[1];
+        r.footprint.ratio = ratio;
+        r.baseline_access.b_row_loads = u6[2];
+        r.access.b_row_loads = u6[3];
+        r.access.a_inner_iters = u6[4];
+        r.access.placeholder_skips = u6[5];
+        r.amortization_iters = amort;
+        const std::string row = bench_csv_row(r) + "\n" + bench_csv_header();
+        if (static_cast<int>(row.size()) >= cap) throw std::runtime_error("buffer too small");
+        std::memcpy(out, row.c_str(), row.size() + 1);
+    });
 }
 
 int ref_build_cluster_dims(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* ci,

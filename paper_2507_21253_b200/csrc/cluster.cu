@@ -24,7 +24,20 @@ namespace bsp {
 
 namespace {
 
-constexpr int MAXK = 32;  // cluster size limit of the device format (member_mask is 32-bit)
+constexpr int MAXK = 32;     // clusters the cluster kernels take (member_mask is 32-bit)
+constexpr int MAXK_FMT = 1024;  // cluster size limit of the device format: larger
+                                // clusters keep valid bits only (member_mask 0) and
+                                // are multiplied through the row view
+
+// Live members of merged column u (slot base = value_ptr + (u - u0) * K):
+// the 32-bit member mask for K <= 32, else the valid bits.
+__device__ __forceinline__ int live_count(const uint32_t* mask, const unsigned long long* valid,
+                                          int64_t u, int64_t slot0, int K) {
+    if (K <= MAXK) return __popc(mask[u]);
+    int n = 0;
+    for (int l = 0; l < K; ++l) n += static_cast<int>((valid[(slot0 + l) >> 6] >> ((slot0 + l) & 63)) & 1ull);
+    return n;
+}
 
 struct ClusterMats {
     const int32_t* __restrict__ sizes;
@@ -60,6 +73,7 @@ __global__ void build_cluster_kernel(const int64_t* __restrict__ rp, const int32
     const int64_t nwarps = (int64_t{gridDim.x} * blockDim.x) >> 5;
     for (int64_t c = warp; c < ncl; c += nwarps) {
         const int K = static_cast<int>(mptr[c + 1] - mptr[c]);
+        if (K > 32) continue;  // build_cluster_big_kernel
         int64_t cur = 0, end = 0;
         if (lane < K) {
             const int32_t r = rows[mptr[c] + lane];
@@ -93,6 +107,76 @@ __global__ void build_cluster_kernel(const int64_t* __restrict__ rp, const int32
     }
 }
 
+
+// Clusters of more than 32 rows (up to MAXK_FMT): lane holds members lane + 32 j;
+// the same K-way merge, each step taking the minimum over all members.  Kept
+// apart so the common kernel above stays lean; launched only when such
+// clusters exist.
+template <int MODE>
+__global__ void build_cluster_big_kernel(const int64_t* __restrict__ rp,
+                                         const int32_t* __restrict__ col,
+                                         const double* __restrict__ val, int64_t ncl,
+                                         const int64_t* __restrict__ mptr,
+                                         const int32_t* __restrict__ rows,
+                                         int64_t* __restrict__ ucount,
+                                         const int64_t* __restrict__ ccp,
+                                         const int64_t* __restrict__ vptr,
+                                         int32_t* __restrict__ ocol, double* __restrict__ oval,
+                                         unsigned long long* __restrict__ valid,
+                                         uint32_t* __restrict__ omask) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t{blockDim.x} + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t{gridDim.x} * blockDim.x) >> 5;
+    for (int64_t c = warp; c < ncl; c += nwarps) {
+        const int K = static_cast<int>(mptr[c + 1] - mptr[c]);
+        if (K <= 32) continue;
+        {
+            // big clusters (warp-uniform): lane holds members lane + 32 j; the
+            // same K-way merge, each step taking the minimum over all members
+            constexpr int MB = MAXK_FMT / 32;
+            int64_t bc[MB], be[MB];
+#pragma unroll
+            for (int j = 0; j < MB; ++j) {
+                const int l = lane + 32 * j;
+                bc[j] = be[j] = 0;
+                if (l < K) {
+                    const int32_t r = rows[mptr[c] + l];
+                    bc[j] = rp[r];
+                    be[j] = rp[r + 1];
+                }
+            }
+            int64_t u = 0;
+            const int64_t cbase = MODE ? ccp[c] : 0;
+            const int64_t vbase = MODE ? vptr[c] : 0;
+            for (;;) {
+                int32_t mine = INT32_MAX;
+#pragma unroll
+                for (int j = 0; j < MB; ++j)
+                    if (bc[j] < be[j]) mine = min(mine, col[bc[j]]);
+                const int32_t mn = __reduce_min_sync(0xffffffffu, mine);
+                if (mn == INT32_MAX) break;
+                if (MODE && lane == 0) {
+                    ocol[cbase + u] = mn;
+                    omask[cbase + u] = 0u;  // members beyond 32: valid bits only
+                }
+#pragma unroll
+                for (int j = 0; j < MB; ++j) {
+                    if (bc[j] < be[j] && col[bc[j]] == mn) {
+                        if (MODE) {
+                            const int64_t slot = vbase + u * K + lane + 32 * j;
+                            oval[slot] = val[bc[j]];
+                            atomicOr(&valid[slot >> 6], 1ull << (slot & 63));
+                        }
+                        ++bc[j];
+                    }
+                }
+                ++u;
+            }
+            if (!MODE && lane == 0) ucount[c] = u;
+        }
+    }
+}
+
 __global__ void value_ptr_kernel(const int64_t* __restrict__ ucount, const int64_t* __restrict__ mptr,
                                  int64_t ncl, int64_t* __restrict__ slots,
                                  int32_t* __restrict__ sizes) {
@@ -113,6 +197,7 @@ __global__ void cluster_to_csr_kernel(const int32_t* __restrict__ sizes,
                                       const int64_t* __restrict__ vptr,
                                       const double* __restrict__ vals,
                                       const uint32_t* __restrict__ mask,
+                                      const unsigned long long* __restrict__ valid,
                                       const int32_t* __restrict__ row_map, int64_t ncl,
                                       int64_t* __restrict__ row_nnz, const int64_t* __restrict__ crp,
                                       int32_t* __restrict__ ocol, double* __restrict__ oval) {
@@ -128,7 +213,15 @@ __global__ void cluster_to_csr_kernel(const int32_t* __restrict__ sizes,
             int64_t cnt = 0;
             for (int64_t ub = u0; ub < u1; ub += 32) {
                 const int64_t u = ub + lane;
-                const bool has = u < u1 && ((mask[u] >> l) & 1u);
+                bool has = false;
+                if (u < u1) {
+                    if (K <= MAXK) {
+                        has = (mask[u] >> l) & 1u;
+                    } else {
+                        const int64_t slot = vptr[c] + (u - u0) * K + l;
+                        has = (valid[slot >> 6] >> (slot & 63)) & 1ull;
+                    }
+                }
                 const uint32_t b = __ballot_sync(0xffffffffu, has);
                 if (MODE && has) {
                     const int64_t o = pos + __popc(b & ((1u << lane) - 1u));
@@ -887,6 +980,8 @@ __global__ void cluster_stats_kernel(const int32_t* __restrict__ sizes,
                                      const int64_t* __restrict__ ccp,
                                      const int32_t* __restrict__ ccol,
                                      const uint32_t* __restrict__ mask,
+                                     const unsigned long long* __restrict__ valid,
+                                     const int64_t* __restrict__ vptr,
                                      const int64_t* __restrict__ brp, int64_t ncl,
                                      unsigned long long* __restrict__ out) {
     unsigned long long loads = 0, iters = 0, skips = 0;
@@ -899,7 +994,8 @@ __global__ void cluster_stats_kernel(const int32_t* __restrict__ sizes,
             if (bn == 0) continue;
             ++loads;
             iters += static_cast<unsigned long long>(K * bn);
-            skips += static_cast<unsigned long long>((K - __popc(mask[u])) * bn);
+            skips += static_cast<unsigned long long>(
+                (K - live_count(mask, valid, u, vptr[c] + (u - ccp[c]) * K, K)) * bn);
         }
     }
     atomicAdd(&out[0], loads);
@@ -1049,6 +1145,8 @@ void build_cluster_device(bsp_handle h, const bsp_csr* A, int64_t ncl, int64_t* 
     const int g = grid_for(h, ncl * 32, 256);
     BSP_LAUNCH(h, build_cluster_kernel<0>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl, mptr,
                rows, ucount.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    BSP_LAUNCH(h, build_cluster_big_kernel<0>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl,
+               mptr, rows, ucount.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
     DBuf<int64_t> ccp(h, ncl + 1, Pool::out);
     exclusive_scan_i64(h, ucount.p, ccp.p, ncl + 1);
     DBuf<int64_t> slots(h, ncl + 1);
@@ -1072,6 +1170,9 @@ void build_cluster_device(bsp_handle h, const bsp_csr* A, int64_t ncl, int64_t* 
     BSP_CUDA(cudaMemsetAsync(valid.p, 0, std::max<int64_t>(nwords, 1) * sizeof(uint64_t), h->stream));
     BSP_LAUNCH(h, build_cluster_kernel<1>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl, mptr,
                rows, nullptr, ccp.p, vptr.p, ocol.p, oval.p,
+               reinterpret_cast<unsigned long long*>(valid.p), omask.p);
+    BSP_LAUNCH(h, build_cluster_big_kernel<1>, g, 256, 0, A->row_ptr, A->col_idx, A->values, ncl,
+               mptr, rows, nullptr, ccp.p, vptr.p, ocol.p, oval.p,
                reinterpret_cast<unsigned long long*>(valid.p), omask.p);
     out->nclusters = ncl;
     out->nrows = A->nrows;
@@ -1116,7 +1217,8 @@ void cluster_to_csr_device(bsp_handle h, const bsp_csr_cluster* m, bsp_csr* out)
     const int g = grid_for(h, m->nclusters * 32, 256);
     BSP_LAUNCH(h, cluster_to_csr_kernel<0>, g, 256, 0, m->cluster_sizes, m->member_ptr,
                m->cluster_col_ptr, m->col_idx, m->value_ptr, m->values, m->member_mask,
-               m->row_map, m->nclusters, cnt.p, nullptr, nullptr, nullptr);
+               reinterpret_cast<const unsigned long long*>(m->valid), m->row_map, m->nclusters,
+               cnt.p, nullptr, nullptr, nullptr);
     DBuf<int64_t> rp(h, n + 1, Pool::out);
     exclusive_scan_i64(h, cnt.p, rp.p, n + 1);
     const int64_t nnz = read_scalar(h, rp.p + n);
@@ -1124,7 +1226,8 @@ void cluster_to_csr_device(bsp_handle h, const bsp_csr_cluster* m, bsp_csr* out)
     DBuf<double> v(h, nnz, Pool::out);
     BSP_LAUNCH(h, cluster_to_csr_kernel<1>, g, 256, 0, m->cluster_sizes, m->member_ptr,
                m->cluster_col_ptr, m->col_idx, m->value_ptr, m->values, m->member_mask,
-               m->row_map, m->nclusters, nullptr, rp.p, ci.p, v.p);
+               reinterpret_cast<const unsigned long long*>(m->valid), m->row_map, m->nclusters,
+               nullptr, rp.p, ci.p, v.p);
     out->nrows = n;
     out->ncols = m->ncols;
     out->nnz = nnz;
@@ -1154,6 +1257,9 @@ namespace {
 // rows' row_upper_bound (spgemm.hpp:31-36), placeholders not counted.
 __global__ void cluster_work_kernel(const int64_t* __restrict__ ccp, const int32_t* __restrict__ col,
                                     const uint32_t* __restrict__ mask,
+                                    const unsigned long long* __restrict__ valid,
+                                    const int64_t* __restrict__ vptr,
+                                    const int32_t* __restrict__ sizes,
                                     const int64_t* __restrict__ brp, int64_t ncl,
                                     int64_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
@@ -1162,7 +1268,9 @@ __global__ void cluster_work_kernel(const int64_t* __restrict__ ccp, const int32
         int64_t P = 0;
         for (int64_t q = ccp[c] + lane; q < ccp[c + 1]; q += 32) {
             const int32_t k = col[q];
-            P += static_cast<int64_t>(__popc(mask[q])) * (brp[k + 1] - brp[k]);
+            const int K = sizes[c];
+            P += static_cast<int64_t>(live_count(mask, valid, q, vptr[c] + (q - ccp[c]) * K, K)) *
+                 (brp[k + 1] - brp[k]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) P += __shfl_xor_sync(0xffffffffu, P, o);
@@ -1191,7 +1299,9 @@ int bsp_partition_clusters(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         if (ncl > 0) {
             DBuf<int64_t> w(h, ncl);
             BSP_LAUNCH(h, cluster_work_kernel, grid_for(h, ncl * 32, 256), 256, 0,
-                       A->cluster_col_ptr, A->col_idx, A->member_mask, B->row_ptr, ncl, w.p);
+                       A->cluster_col_ptr, A->col_idx, A->member_mask,
+                       reinterpret_cast<const unsigned long long*>(A->valid), A->value_ptr,
+                       A->cluster_sizes, B->row_ptr, ncl, w.p);
             d2h(h, pc.data(), w.p, ncl);
             sync(h);
         }
@@ -1222,8 +1332,8 @@ int bsp_csr_cluster_build(bsp_handle h, const bsp_csr* A, int64_t nclusters,
         for (int64_t c = 0; c < nclusters; ++c) {
             const int64_t b = cluster_ptr[c], e = cluster_ptr[c + 1];
             require(e > b, "cluster assignment: empty cluster");
-            require(e - b <= MAXK, "cluster assignment: cluster larger than 32 rows is not "
-                                   "supported by the device format");
+            require(e - b <= MAXK_FMT, "cluster assignment: clusters of more than 1024 rows "
+                                       "are not supported by the device format");
             for (int64_t q = b; q < e; ++q) {
                 const int32_t r = rows[q];
                 require(r >= 0 && r < n, "cluster assignment: row index out of range");
@@ -1523,7 +1633,8 @@ int bsp_cluster_access_stats(bsp_handle h, const bsp_csr_cluster* A, const bsp_c
         DBuf<unsigned long long> acc(h, 3);
         BSP_CUDA(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), h->stream));
         BSP_LAUNCH(h, cluster_stats_kernel, grid_for(h, A->nclusters, 256), 256, 0,
-                   A->cluster_sizes, A->cluster_col_ptr, A->col_idx, A->member_mask, B->row_ptr,
+                   A->cluster_sizes, A->cluster_col_ptr, A->col_idx, A->member_mask,
+                   reinterpret_cast<const unsigned long long*>(A->valid), A->value_ptr, B->row_ptr,
                    A->nclusters, acc.p);
         unsigned long long r[3];
         d2h(h, r, acc.p, 3);

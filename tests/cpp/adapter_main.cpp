@@ -43,7 +43,33 @@ int main(int argc, char** argv) {
     } catch (const std::invalid_argument&) {
         threw = true;
     }
-    std::printf("rowwise %s clusterwise %s contract %s\n", row_ok ? "PASS" : "FAIL",
-                cw_ok ? "PASS" : "FAIL", threw ? "PASS" : "FAIL");
-    return (row_ok && cw_ok && threw) ? 0 : 1;
+    // the rest of the mirror: symbolic in the reference's index type, top-k
+    // element for element, clustering / reorder identical
+    const std::vector<index_t> sym = bsp_gpu::spgemm_symbolic(a, a);
+    const bool sym_ok = sym == spgemm_symbolic(a, a);
+    const CsrMatrix at = transpose(binarize(a));
+    const auto tk_ref = spgemm_topk(binarize(a), at, 7, 0.3);
+    const auto tk_gpu = bsp_gpu::spgemm_topk<CandidatePair>(binarize(a), at, 7, 0.3);
+    bool tk_ok = tk_ref.size() == tk_gpu.size();
+    for (size_t k = 0; tk_ok && k < tk_ref.size(); ++k)
+        tk_ok = tk_ref[k].i == tk_gpu[k].i && tk_ref[k].j == tk_gpu[k].j &&
+                std::memcmp(&tk_ref[k].score, &tk_gpu[k].score, sizeof(double)) == 0;
+    const ClusterParams prm{};
+    const bool hier_ok =
+        bsp_gpu::hierarchical_clusters<ClusterAssignment>(a, prm).clusters == asg.clusters;
+    const bool var_ok = bsp_gpu::variable_length_clusters<ClusterAssignment>(a, prm).clusters ==
+                        variable_length_clusters(a, prm).clusters;
+    const bool fix_ok =
+        bsp_gpu::fixed_length_clusters<ClusterAssignment>(a.nrows, 4).clusters ==
+        fixed_length_clusters(a.nrows, 4).clusters;
+    const bool ord_ok = bsp_gpu::reorder_rcm<Permutation>(a).perm == reorder_rcm(a).perm &&
+                        bsp_gpu::reorder_degree<Permutation>(a).perm == reorder_degree(a).perm &&
+                        bsp_gpu::reorder_random<Permutation>(a.nrows, 11).perm ==
+                            reorder_random(a.nrows, 11).perm;
+    const bool rest_ok = sym_ok && tk_ok && hier_ok && var_ok && fix_ok && ord_ok;
+    std::printf("rowwise %s clusterwise %s contract %s mirror %s (sym %d topk %d hier %d var %d "
+                "fixed %d reorder %d)\n",
+                row_ok ? "PASS" : "FAIL", cw_ok ? "PASS" : "FAIL", threw ? "PASS" : "FAIL",
+                rest_ok ? "PASS" : "FAIL", sym_ok, tk_ok, hier_ok, var_ok, fix_ok, ord_ok);
+    return (row_ok && cw_ok && threw && rest_ok) ? 0 : 1;
 }

@@ -33,4 +33,4 @@ def test_adapter_matches_reference_on_gpu():
         pytest.skip("adapter binary not built (build it in the container: it needs the reference headers)")
     r = subprocess.run([str(BIN), "run"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "rowwise PASS clusterwise PASS contract PASS" in r.stdout
+    assert "rowwise PASS clusterwise PASS contract PASS mirror PASS" in r.stdout

@@ -193,3 +193,33 @@ def test_clusterwise_narrow_b_large_clusters(engine, k, ncols):
     res = engine.spgemm_clusterwise(Ac, Bd, want_cluster=True)
     cc = res[0] if isinstance(res, tuple) else res
     assert_csr_identical(cc.download(), O.spgemm_rowwise(a, b), "narrow, CSR_Cluster requested")
+
+
+@pytest.mark.parametrize("k", [33, 64, 200])
+def test_clusters_beyond_32_members(engine, k):
+    """fixed_length_clusters(n, k) with k > 32 (the reference accepts any k,
+    clustering.hpp:59-69): the device CSR_Cluster holds them (valid bits; the
+    32-bit member masks only serve the cluster kernels), the format equals the
+    oracle's, cluster-wise C equals row-wise bit for bit (those clusters run
+    through the row view), cluster_to_csr round-trips, access stats are exact,
+    and the cluster split covers them."""
+    a = random_csr(420, 420, 0.03, 900 + k)
+    asg = B.fixed_length_clusters(a.nrows, k)
+    A = engine.upload(a)
+    Ac = engine.build_csr_cluster(A, asg)
+    got = Ac.download()
+    ref = O.build_csr_cluster(a, asg.cluster_ptr, asg.rows)
+    for key in ("cluster_sizes", "cluster_col_ptr", "col_idx", "value_ptr", "row_map", "valid"):
+        assert np.array_equal(got[key], ref[key]), key
+    assert np.array_equal(got["values"].view(np.uint64), ref["values"].view(np.uint64))
+    assert B.csr_equal_canonical(engine.cluster_to_csr(Ac).download(), a, 0.0)
+    want, _, st = O.spgemm_clusterwise(a, asg.cluster_ptr, asg.rows, a)
+    assert_csr_identical(engine.spgemm_clusterwise(Ac, A).download(), O.spgemm_rowwise(a, a),
+                         f"k={k}")
+    s = engine.cluster_access_stats(Ac, A)
+    assert (s.b_row_loads, s.a_inner_iters, s.placeholder_skips) == tuple(st)
+    b = engine.partition_clusters(Ac, A, 3)
+    assert b[0] == 0 and b[-1] == asg.nclusters
+    big = random_csr(1100, 50, 0.05, 7)
+    with pytest.raises(B.ContractError):  # the format's limit: 1024 rows per cluster
+        engine.build_csr_cluster(engine.upload(big), B.fixed_length_clusters(big.nrows, 1025))
