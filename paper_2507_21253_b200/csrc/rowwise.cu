@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(PLAN_T, 5) plan_write_kernel(
     const int32_t* __restrict__ nwin, const int64_t* __restrict__ doff,
     const uint2* __restrict__ desc, const int64_t* __restrict__ win_off, Window* __restrict__ wins,
     uint8_t* __restrict__ win_cat, const int64_t* __restrict__ start_off, int64_t start_budget,
-    uint32_t* __restrict__ starts) {
+    uint32_t* __restrict__ starts, int bs_x4) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PlanWriteShared& s = *reinterpret_cast<PlanWriteShared*>(smem_raw);
     const int32_t hrow = blockIdx.x;
@@ -348,10 +348,34 @@ __global__ void __launch_bounds__(PLAN_T, 5) plan_write_kernel(
         win_cat[off + k] = static_cast<uint8_t>(cat);
     }
     if (sofs < 0) return;
-    __syncthreads();  // wc0/wpre dead: the union becomes the staging area
     const int lane = threadIdx.x & 31;
     const int d = static_cast<int>(m.arp[row + 1] - m.arp[row]);
     const int64_t tsz = int64_t{wtot + 1} * d;
+    // Rows with few windows: each interior boundary of each segment is a
+    // binary search for the window's first column in that B row —
+    // (windows - 1) x segments x log2(segment length) loads instead of
+    // streaming every product's column a second time.
+    {
+        const int64_t P = s.u.w.wpre[wtot];
+        const int lg = 1 + bit_length(static_cast<uint32_t>(P / ::max(d, 1)));
+        if (int64_t{wtot - 1} * d * lg * 4 < P * bs_x4) {
+            uint32_t* tab = starts + sofs;
+            const int64_t rs = m.arp[row];
+            for (int64_t t = threadIdx.x; t < tsz; t += PLAN_T) {
+                const int w = static_cast<int>(t / d), p = static_cast<int>(t - int64_t{w} * d);
+                const int32_t k = __ldg(m.acol + rs + p);
+                const int64_t b0 = __ldg(m.brp + k), b1 = __ldg(m.brp + k + 1);
+                int64_t e = b0;
+                if (w == wtot) e = b1;
+                else if (w > 0)
+                    e = lower_bound_col(m.bcol, b0, b1,
+                                        static_cast<int32_t>(s.u.w.wc0[w] & ~DENSE_BIT));
+                tab[t] = static_cast<uint32_t>(e);
+            }
+            return;
+        }
+    }
+    __syncthreads();  // wc0/wpre dead: the union becomes the staging area
     const bool staged = tsz <= STAGE;
     uint32_t* tab = staged ? s.u.stage : starts + sofs;
     // entries are absolute B offsets (segment start b0 + element index)
@@ -1249,11 +1273,19 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         }
         plan.wins = DBuf<Window>(h, plan.nwin);
         DBuf<uint8_t> dense(h, plan.nwin);
+        // start tables by binary search where (windows - 1) x segments x log2(len)
+        // < products x BSP_BS_X4 / 4 (0 disables).  Measured on cfg5: plan_write
+        // 35.5 ms streaming only, 25.4 ms at 2 (28.2 / 28.7 / 28.8 / 40.3 / 59.7 ms
+        // at 1 / 3 / 4 / 8 / 16).
+        static const int bs_x4 = [] {
+            const char* e = std::getenv("BSP_BS_X4");
+            return e ? std::atoi(e) : 2;
+        }();
         set_smem(plan_write_kernel, sizeof(PlanWriteShared));
         BSP_LAUNCH(h, plan_write_kernel, static_cast<unsigned>(nh), PLAN_T,
                    sizeof(PlanWriteShared), m, heavy, nbins, log_binw, nwin.p, doff.p, desc.p,
                    woff.p, plan.wins.p, dense.p, use_starts ? soff.p : nullptr, budget,
-                   use_starts ? plan.starts.p : nullptr);
+                   use_starts ? plan.starts.p : nullptr, bs_x4);
         plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
         plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
         DBuf<unsigned long long> cnt(h, 2 * (NWCLS + 1));
