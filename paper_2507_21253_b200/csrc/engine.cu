@@ -175,6 +175,10 @@ void gap_check_launch(const char* name) {
     if (ms > 1.0) std::fprintf(stderr, "[gap] %.2f ms host time before %s\n", ms, name);
 }
 
+void gap_slow_call(const char* what, double ms) {
+    if (ms > 1.0) std::fprintf(stderr, "[slow] %.2f ms in %s\n", ms, what);
+}
+
 void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes) {
     if (!h->rb_host) {
         BSP_CUDA(cudaHostAlloc(&h->rb_host, kReadbackBytes, cudaHostAllocMapped));
@@ -189,7 +193,11 @@ void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes) {
 
 size_t available_bytes(bsp_handle h) {
     size_t free_b = 0, total_b = 0;
+    const auto t0 = std::chrono::steady_clock::now();
     BSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (gap_log_enabled())
+        gap_slow_call("cudaMemGetInfo", std::chrono::duration<double, std::milli>(
+                                            std::chrono::steady_clock::now() - t0).count());
     for (cudaMemPool_t pool : {h->scratch_pool, h->out_pool}) {
         uint64_t reserved = 0, used = 0;
         BSP_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -116,16 +117,29 @@ inline void join_side(bsp_handle h) {
     cuda_check(cudaStreamWaitEvent(h->stream, h->ev_join, 0), "cudaStreamWaitEvent");
 }
 
+// BSP_GAP_LOG=1: log host time between a synchronisation's return and the next
+// engine launch when it exceeds 1 ms (diagnoses GPU idle gaps inside a multiply).
+bool gap_log_enabled();
+void gap_mark_sync();
+void gap_check_launch(const char* name);
+
 // Stream-ordered device allocation from one of the handle's pools.
 enum class Pool { scratch, out };
 
+void gap_slow_call(const char* what, double ms);
 template <typename T>
 T* dalloc(bsp_handle h, int64_t n, Pool pool = Pool::scratch) {
     void* p = nullptr;
     const size_t bytes = static_cast<size_t>(n > 0 ? n : 1) * sizeof(T);
+    const bool lg = gap_log_enabled();
+    const auto t0 = lg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
     cuda_check(cudaMallocFromPoolAsync(&p, bytes, pool == Pool::out ? h->out_pool : h->scratch_pool,
                                        h->stream),
                "cudaMallocFromPoolAsync");
+    if (lg)
+        gap_slow_call("cudaMallocFromPoolAsync",
+                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                          .count());
     return static_cast<T*>(p);
 }
 
@@ -201,11 +215,6 @@ void h2d(bsp_handle h, T* dst, const T* src, int64_t n) {
     if (n <= 0) return;
     BSP_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, h->stream));
 }
-// BSP_GAP_LOG=1: log host time between a synchronisation's return and the next
-// engine launch when it exceeds 1 ms (diagnoses GPU idle gaps inside a multiply).
-bool gap_log_enabled();
-void gap_mark_sync();
-void gap_check_launch(const char* name);
 inline void sync(bsp_handle h) {
     BSP_CUDA(cudaStreamSynchronize(h->stream));
     if (gap_log_enabled()) gap_mark_sync();

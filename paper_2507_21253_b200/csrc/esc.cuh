@@ -186,6 +186,11 @@ struct RowwisePlan {
     DBuf<uint32_t> starts; // planner per-(window, segment) start tables (absolute)
     bool light_sym_done = false;  // light rows counted on the side stream
     bool keep_tables = false;     // start tables in the handle's kept buffer
+    // Free device bytes sampled at the start of the multiply (-1: query when
+    // needed).  cudaMemGetInfo waits on the driver while nvidia-smi polls it
+    // (measured: up to 65 ms); sampled before the first synchronisation, that
+    // wait overlaps the previous multiply's kernels instead of idling the GPU.
+    int64_t avail_hint = -1;
     // Set while that side-stream work is not yet joined into the main stream:
     // the destructor joins it before the plan's buffers are freed on the main
     // stream, so an error between build_plan and plan_symbolic cannot free
@@ -233,8 +238,13 @@ void narrow64_rows(bsp_handle h, const Mats& m, const unsigned long long* mask, 
 
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
+    const bool lg = gap_log_enabled();
+    const auto t0 = lg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
     BSP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes)));
+    if (lg)
+        gap_slow_call("cudaFuncSetAttribute", std::chrono::duration<double, std::milli>(
+                                                  std::chrono::steady_clock::now() - t0).count());
 }
 
 }  // namespace bsp

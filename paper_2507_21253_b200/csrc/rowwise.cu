@@ -1247,8 +1247,9 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         // binary-search.
         constexpr int64_t EB = sizeof(uint32_t);
         // the kept table buffer counts as available to the tables
-        const int64_t avail = static_cast<int64_t>(available_bytes(h)) +
-                              (plan.keep_tables ? static_cast<int64_t>(h->keep_starts_bytes) : 0);
+        const int64_t avail =
+            (plan.avail_hint >= 0 ? plan.avail_hint : static_cast<int64_t>(available_bytes(h))) +
+            (plan.keep_tables ? static_cast<int64_t>(h->keep_starts_bytes) : 0);
         const int64_t spare = avail - 12 * h->stats.products - (int64_t{2} << 30);
         const int64_t floor_entries = std::min<int64_t>(int64_t{1} << 30, avail / (16 * EB));
         const int64_t budget = std::min<int64_t>(
@@ -1813,6 +1814,7 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     BSP_CUDA(cudaMemsetAsync(crp.p, 0, (n + 1) * sizeof(int64_t), h->stream));
     RowwisePlan plan;
     plan.keep_tables = true;
+    plan.avail_hint = static_cast<int64_t>(available_bytes(h));  // before any sync (see esc.cuh)
     build_plan(h, m, rb, re, row_skip, plan, nullptr, crp.p);
     // The main window class (2048-product tiles: nearly all heavy products on
     // power-law inputs) is counted by its numeric pass (esc_window_lb_kernel)
@@ -1834,7 +1836,9 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     if (plan.nwin > 0) exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
     int64_t nnz = read_scalar(h, rp.p + n);  // without the look-back class when lb
     int64_t cap = nnz;
-    const int64_t avail = static_cast<int64_t>(available_bytes(h));
+    // the planner's allocations since the sample are small next to C; C's own
+    // allocation still fails cleanly (BSP_ERR_OOM) if memory was taken meanwhile
+    const int64_t avail = plan.avail_hint;
     if (lb) {
         cap = nnz + plan.wcls_prod[LBC];
         // C (12 B per entry) + the look-back state, with a 1 GB margin
