@@ -532,7 +532,6 @@ def run_tall_skinny(B, args, num_frontiers=10, batch=64, seed=0):
         "clusterwise": {"value": 2.0 * products / (ms_cl * 1e-3) / 1e9, "ms_per_step": ms_cl,
                         "clusters": asg.nclusters},
         "gpu_launches": launches,
-        "b_broadcast_ms": round(bcast_ms, 3) if engine_comm else None,
         "roofline": {"bound": "hbm", "achieved": bal / (ms_row * 1e-3) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": bal / (ms_row * 1e-3) / 1e9 / peak,
                      "traffic": None, "bytes_alg_per_step": bal, "peak_source": peak_kind,

@@ -35,3 +35,14 @@ def test_two_rank_bench_matches_one_rank():
     assert two["config"]["products"] == one["config"]["products"]
     assert two["e2e"]["d2h_bytes_per_step"] >= one["e2e"]["d2h_bytes_per_step"]
     assert two["e2e"]["chunks"] == 4
+
+
+def test_tall_skinny_workload_runs():
+    """bench.py --workload ts (A x BFS frontiers) at a small scale."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--workload", "ts", "--steps", "1",
+           "--warmup", "3", "--scale", "12", "--no-cpu"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["value"] > 0 and line["clusterwise"]["value"] > 0
+    assert line["config"]["frontiers"] >= 1
