@@ -251,9 +251,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16)
-    ap.add_argument("--workload", default="a2", choices=["a2", "ts"],
+    ap.add_argument("--workload", default="a2", choices=["a2", "ts", "cfg2", "cfg4"],
                     help="a2: C = A*A (headline); ts: A x 10 BFS frontiers of 64 sources "
-                         "(square x tall-skinny, SURVEY 8(f)-1)")
+                         "(square x tall-skinny, SURVEY 8(f)-1); cfg2 / cfg4: row-wise vs "
+                         "cluster-wise on the clustered configs (BASELINE targets)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -281,6 +282,10 @@ def main():
     if args.workload == "ts":
         if rank == 0:
             run_tall_skinny(B, args)
+        return
+    if args.workload in ("cfg2", "cfg4"):
+        if rank == 0:
+            run_clustered(B, args)
         return
     dist = None
     if world > 1:
@@ -559,6 +564,93 @@ def run_tall_skinny(B, args, num_frontiers=10, batch=64, seed=0):
                                               f"only spgemm_rowwise timed"}
     for f in fs:
         f.free()
+    print(json.dumps(line))
+
+
+def run_clustered(B, args):
+    """BASELINE's cluster-wise comparisons: cfg2 = row-wise vs cluster-wise
+    on the permuted hidden-cluster matrix (hierarchical clustering; the row-wise line is the
+    value); cfg4 = row-wise unreordered, row-wise after RCM, cluster-wise after RCM +
+    hierarchical.  All timed in the same run with CUDA events on the engine's stream;
+    C checked identical across the variants (cluster-wise C == row-wise C bit for bit)."""
+    import torch
+    import numpy as np
+
+    cfg = 2 if args.workload == "cfg2" else 4
+    a0 = B.make_config(cfg, args.scale)
+    eng = B.Engine(0)
+    stream = torch.cuda.Stream()
+    eng.set_stream(stream.cuda_stream)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn().free()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            C = fn()
+            e1.record(stream)
+            C.free()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.mean(ts)), float(min(ts))
+
+    variants = {}
+    t0 = time.perf_counter()
+    a = a0
+    if cfg == 4:
+        A0 = eng.upload(a0)
+        products = eng.spgemm_products(A0, A0)
+        variants["rowwise_unreordered"] = timed(lambda: eng.spgemm_rowwise(A0, A0))
+        ref_c = eng.spgemm_rowwise(A0, A0).download()
+        A0.free()
+        t0 = time.perf_counter()
+        perm = B.reorder_rcm(a0)
+        a = B.permute_symmetric(a0, perm)
+    t_reorder = time.perf_counter() - t0 if cfg == 4 else 0.0
+    A = eng.upload(a)
+    products = eng.spgemm_products(A, A)
+    name = "rowwise" if cfg == 2 else "rowwise_rcm"
+    variants[name] = timed(lambda: eng.spgemm_rowwise(A, A))
+    t0 = time.perf_counter()
+    asg = eng.hierarchical_clusters(a)
+    Ac = eng.build_csr_cluster(A, asg)
+    eng.synchronize()
+    t_cluster = time.perf_counter() - t0
+    cname = "clusterwise" if cfg == 2 else "clusterwise_rcm_hier"
+    variants[cname] = timed(lambda: eng.spgemm_clusterwise(Ac, A))
+    c_row = eng.spgemm_rowwise(A, A).download()
+    c_cl = eng.spgemm_clusterwise(Ac, A).download()
+    same = (np.array_equal(c_row.row_ptr, c_cl.row_ptr) and
+            np.array_equal(c_row.col_idx, c_cl.col_idx) and
+            np.array_equal(c_row.values.view(np.uint64), c_cl.values.view(np.uint64)))
+    if cfg == 4:  # the reordered product is the original one, permuted
+        same = same and B.csr_equal_canonical(B.permute_symmetric(ref_c, perm), c_row, 0.0)
+    ms_row = variants[name][0]
+    peak, peak_kind = hbm_peak()
+    bal = bytes_alg(a.nnz(), a.nnz(), c_row.nnz(), a.nrows, a.nrows, a.nrows)
+    line = {
+        "metric": "A·B SpGEMM GFLOP/s (2×products/s)",
+        "value": 2.0 * products / (ms_row * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_row,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded BASELINE cfg{cfg})",
+        "config": {"workload": f"cfg{cfg}_AxA_rowwise_vs_clusterwise", "n": a.nrows,
+                   "nnz_a": a.nnz(), "products": products, "nnz_c": c_row.nnz(),
+                   "clusters": asg.nclusters, "parallelism": "x1"},
+        "variants_ms": {k: {"mean": round(v[0], 4), "best": round(v[1], 4),
+                            "gflops": round(2.0 * products / (v[0] * 1e-3) / 1e9, 2)}
+                        for k, v in variants.items()},
+        "clusterwise_speedup_vs_" + name: round(ms_row / variants[cname][0], 3),
+        "c_bit_identical_across_variants": bool(same),
+        "preprocessing_s": {"reorder": round(t_reorder, 3), "cluster": round(t_cluster, 3)},
+        "roofline": {"bound": "hbm", "achieved": bal / (ms_row * 1e-3) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": bal / (ms_row * 1e-3) / 1e9 / peak,
+                     "traffic": None, "bytes_alg_per_step": bal, "peak_source": peak_kind,
+                     "unit_of_work": "one full row-wise multiply"},
+    }
     print(json.dumps(line))
 
 

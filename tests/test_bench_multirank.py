@@ -46,3 +46,15 @@ def test_tall_skinny_workload_runs():
     line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert line["value"] > 0 and line["clusterwise"]["value"] > 0
     assert line["config"]["frontiers"] >= 1
+
+
+@pytest.mark.parametrize("wl,scale", [("cfg2", 512), ("cfg4", 16)])
+def test_clustered_workloads_run(wl, scale):
+    """bench.py --workload cfg2 / cfg4: row-wise and cluster-wise timed in one run, C identical."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--workload", wl, "--steps", "2",
+           "--warmup", "3", "--scale", str(scale)]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["c_bit_identical_across_variants"] is True
+    assert len(line["variants_ms"]) == (2 if wl == "cfg2" else 3)
