@@ -615,7 +615,10 @@ def run_clustered(B, args):
     name = "rowwise" if cfg == 2 else "rowwise_rcm"
     variants[name] = timed(lambda: eng.spgemm_rowwise(A, A))
     t0 = time.perf_counter()
-    asg = eng.hierarchical_clusters(a)
+    # cfg2: "hierarchical clustering (minhash, 64 hashes, max cluster size 8)" (BASELINE);
+    # cfg4: the reference's hierarchical top-k
+    asg = (eng.hierarchical_clusters(a, method="minhash", nhash=64) if cfg == 2
+           else eng.hierarchical_clusters(a))
     Ac = eng.build_csr_cluster(A, asg)
     eng.synchronize()
     t_cluster = time.perf_counter() - t0
@@ -639,7 +642,9 @@ def run_clustered(B, args):
         "data": f"synthetic (seeded BASELINE cfg{cfg})",
         "config": {"workload": f"cfg{cfg}_AxA_rowwise_vs_clusterwise", "n": a.nrows,
                    "nnz_a": a.nnz(), "products": products, "nnz_c": c_row.nnz(),
-                   "clusters": asg.nclusters, "parallelism": "x1"},
+                   "clusters": asg.nclusters,
+                   "clustering": "hierarchical, minhash-64 candidates" if cfg == 2
+                   else "RCM + hierarchical (top-k candidates)", "parallelism": "x1"},
         "variants_ms": {k: {"mean": round(v[0], 4), "best": round(v[1], 4),
                             "gflops": round(2.0 * products / (v[0] * 1e-3) / 1e9, 2)}
                         for k, v in variants.items()},

@@ -93,6 +93,8 @@ def main():
     row = timed(lambda: eng.spgemm_rowwise(A, A))
     out["rowwise"] = row
     want = eng.spgemm_rowwise(A, A).download()
+    rs = eng.rowwise_access_stats(A, A)
+    out["rowwise_b_row_loads"] = int(rs.b_row_loads)
     for method in ("topk", "minhash"):
         t0 = time.perf_counter()
         asg = eng.hierarchical_clusters(a, method=method, nhash=64)
@@ -104,16 +106,22 @@ def main():
                  np.array_equal(got.col_idx, want.col_idx) and
                  np.array_equal(got.values.view(np.uint64), want.values.view(np.uint64)))
         cl = timed(lambda: eng.spgemm_clusterwise(Ac, A))
+        acs = eng.cluster_access_stats(Ac, A)
         out[method] = dict(q, clustering_s=tc, clusterwise=cl, c_bit_identical=bool(exact),
-                           speedup_vs_rowwise=row["best_ms"] / cl["best_ms"])
+                           speedup_vs_rowwise=row["best_ms"] / cl["best_ms"],
+                           b_row_loads=int(acs.b_row_loads),
+                           b_row_load_reduction=rs.b_row_loads / max(1, acs.b_row_loads))
     if args.ref:
         import oracle as O
 
         t0 = time.perf_counter()
         cp, rows = O.ref_hierarchical_clusters(a)
-        out["reference_topk"] = dict(quality(B.ClusterAssignment(cp, rows), tmpl, cfg["children"]),
-                                     clustering_s=time.perf_counter() - t0,
-                                     threads=os.cpu_count())
+        tr = time.perf_counter() - t0
+        ra = B.ClusterAssignment(cp, rows)
+        acs = eng.cluster_access_stats(eng.build_csr_cluster(A, ra), A)
+        out["reference_topk"] = dict(quality(ra, tmpl, cfg["children"]), clustering_s=tr,
+                                     threads=os.cpu_count(), b_row_loads=int(acs.b_row_loads),
+                                     b_row_load_reduction=rs.b_row_loads / max(1, acs.b_row_loads))
     print(json.dumps(out))
 
 
