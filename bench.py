@@ -306,11 +306,23 @@ def main():
     eng.set_stream(stream.cuda_stream)
     bcast_ms = 0.0
     if engine_comm:
-        uid = torch.zeros(B.L.BSP_NCCL_ID_BYTES, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(B.Engine.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        eng.comm_init(world, rank, bytes(uid.cpu().numpy().tobytes()))
+        # the engine's own NCCL communicator; if it cannot be set up on every rank
+        # (checked with an all-reduce), fall back to torch.distributed + row ranges
+        ok = torch.ones(1, device="cuda")
+        try:
+            uid = torch.zeros(B.L.BSP_NCCL_ID_BYTES, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(B.Engine.nccl_unique_id()),
+                                           dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            eng.comm_init(world, rank, bytes(uid.cpu().numpy().tobytes()))
+        except Exception as ex:  # reported; the torch path below still measures
+            print(f"[bench] engine NCCL communicator unavailable ({ex}); "
+                  "falling back to torch.distributed", file=sys.stderr)
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        engine_comm = bool(ok.item() > 0)
+    if engine_comm:
         A_root = eng.upload(a) if rank == 0 else None
         eng.synchronize()
         A, bcast_ms = eng.broadcast(A_root, 0)
