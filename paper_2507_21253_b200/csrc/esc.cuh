@@ -33,6 +33,16 @@ struct Mats {
     // 32-bit (tables are only built when nnz(B) < 2^32)
     const uint32_t* __restrict__ starts = nullptr;
     int64_t bnnz = 0;  // nnz(B) (host-side decisions)
+    int64_t bnrows = 0;  // rows of B (host-side decisions)
+};
+
+// Per-B-row bin summary for the heavy-row planner: the row's columns as
+// (bin << 16 | count) entries, one per run of columns in the same planner bin
+// (4096 columns): cfg5's heavy rows reference 9.2e9 B entries but 5.4e9
+// summary entries.  sptr == nullptr: the planner streams the columns.
+struct BinSum {
+    const int64_t* __restrict__ sptr = nullptr;  // [B rows + 1]
+    const uint32_t* __restrict__ sent = nullptr;
 };
 
 struct Window {

@@ -199,6 +199,94 @@ __device__ __forceinline__ void stream_segments(const Mats& m, int32_t row, F&& 
     }
 }
 
+// The same walk over the segments' bin summaries (BinSum): f(p, q0, nent,
+// ent[U], carryw, eoff, b0, blen) per group of PLAN_U x 32 entries; ent[u] is
+// entry q0 + 32u + lane or ~0u past the end; carryw / eoff are per-segment
+// state (reset to -1 / 0); b0, blen: the B row's element range.
+template <class F>
+__device__ __forceinline__ void stream_summaries(const Mats& m, const BinSum& bs, int32_t row,
+                                                 F&& f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = PLAN_T / 32;
+    const int64_t rs = m.arp[row];
+    const int d = static_cast<int>(m.arp[row + 1] - rs);
+    for (int pb = warp; pb < d; pb += NW * 32) {
+        const int pl = pb + NW * lane;
+        int64_t mb0 = 0, mb1 = 0, ms0 = 0, ms1 = 0;
+        if (pl < d) {
+            const int32_t k = __ldg(m.acol + rs + pl);
+            mb0 = __ldg(m.brp + k);
+            mb1 = __ldg(m.brp + k + 1);
+            ms0 = __ldg(bs.sptr + k);
+            ms1 = __ldg(bs.sptr + k + 1);
+        }
+        const int nseg = ::min(32, (d - pb + NW - 1) / NW);
+        for (int j = 0; j < nseg; ++j) {
+            const int64_t b0 = __shfl_sync(0xffffffffu, mb0, j);
+            const int blen = static_cast<int>(__shfl_sync(0xffffffffu, mb1, j) - b0);
+            const int64_t s0 = __shfl_sync(0xffffffffu, ms0, j);
+            const int nent = static_cast<int>(__shfl_sync(0xffffffffu, ms1, j) - s0);
+            const int p = pb + NW * j;
+            int carryw = -1, eoff = 0;
+            for (int q0 = 0; q0 < ::max(nent, 1); q0 += 32 * PLAN_U) {
+                uint32_t ent[PLAN_U];
+#pragma unroll
+                for (int u = 0; u < PLAN_U; ++u) {
+                    const int q = q0 + 32 * u + lane;
+                    ent[u] = q < nent ? __ldg(bs.sent + s0 + q) : ~0u;
+                }
+                f(p, q0, nent, ent, carryw, eoff, b0, blen);
+            }
+        }
+    }
+}
+
+// Bin summary of B (see BinSum): a warp per B row; runs of columns in one bin
+// become one entry, a run continuing across 32-column chunks extends the
+// previous entry.  MODE 0 counts entries per row, MODE 1 writes them.
+template <int MODE>
+__global__ void bin_summary_kernel(const int64_t* __restrict__ brp, const int32_t* __restrict__ bcol,
+                                   int64_t nb, int log_binw, int64_t* __restrict__ cnt,
+                                   const int64_t* __restrict__ sptr, uint32_t* __restrict__ sent) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = int64_t{gridDim.x} * (blockDim.x >> 5);
+    const unsigned below = (1u << lane) - 1u;
+    for (int64_t k = blockIdx.x * int64_t{blockDim.x >> 5} + (threadIdx.x >> 5); k < nb; k += nw) {
+        const int64_t b0 = brp[k];
+        const int len = static_cast<int>(brp[k + 1] - b0);
+        int64_t pos = MODE ? sptr[k] : 0;
+        int32_t carry_bin = -1;
+        int64_t n = 0;
+        for (int q0 = 0; q0 < len; q0 += 32) {
+            const int q = q0 + lane;
+            const bool valid = q < len;
+            const int32_t bin = valid ? (__ldg(bcol + b0 + q) >> log_binw) : -2;
+            int32_t prev = __shfl_up_sync(0xffffffffu, bin, 1);
+            if (lane == 0) prev = carry_bin;
+            const bool head = valid && bin != prev;
+            const unsigned heads = __ballot_sync(0xffffffffu, head);
+            if (MODE) {
+                const int end = ::min(32, len - q0);
+                if (valid && (head || lane == 0)) {
+                    // run length up to the next head in this chunk (or its end)
+                    const unsigned above = heads & ~((2u << lane) - 1u);
+                    const int stop = above ? __ffs(above) - 1 : end;
+                    const uint32_t run = static_cast<uint32_t>(stop - lane);
+                    if (head)
+                        sent[pos + __popc(heads & below)] = (static_cast<uint32_t>(bin) << 16) | run;
+                    else  // lane 0 continues the previous chunk's last run
+                        sent[pos - 1] += run;
+                }
+            }
+            pos += __popc(heads);
+            n += __popc(heads);
+            carry_bin = __shfl_sync(0xffffffffu, bin, ::min(31, len - 1 - q0));
+            __syncwarp();
+        }
+        if (!MODE && lane == 0) cnt[k] = n;
+    }
+}
+
 // K2a: per heavy row, a product histogram over `nbins` column bins, then the
 // greedy window cut (below).  Writes the window count and the descriptors
 // {c0 | DENSE_BIT, product prefix} (+ sentinel {ncols, P}) at desc[doff[h]].
@@ -208,13 +296,24 @@ __global__ void __launch_bounds__(PLAN_T, 8) plan_count_kernel(Mats m,
                                                             int32_t* __restrict__ nwin,
                                                             const int64_t* __restrict__ doff,
                                                             uint2* __restrict__ desc,
-                                                            int32_t capg) {
+                                                            int32_t capg, BinSum bs) {
     __shared__ PlanCountShared s;
     const int32_t hrow = blockIdx.x;
     const int32_t row = heavy[hrow];
     const int lane = threadIdx.x & 31;
     for (int b = threadIdx.x; b < nbins; b += PLAN_T) s.hist[b] = 0;
     __syncthreads();
+    if (bs.sptr) {
+        // bin summaries: one atomic per (segment, bin) run instead of per column
+        stream_summaries(m, bs, row, [&](int, int q0, int nent, const uint32_t* ent, int&, int&,
+                                         int64_t, int) {
+#pragma unroll
+            for (int u = 0; u < PLAN_U; ++u) {
+                if (q0 + 32 * u >= nent) break;
+                if (ent[u] != ~0u) atomicAdd(&s.hist[ent[u] >> 16], static_cast<int>(ent[u] & 0xffffu));
+            }
+        });
+    } else
     stream_segments(m, row, [&](int, int q0, int len, const int32_t* cols, int&, int64_t) {
 #pragma unroll
         for (int u = 0; u < PLAN_U; ++u) {
@@ -295,7 +394,7 @@ __global__ void __launch_bounds__(PLAN_T, 5) plan_write_kernel(
     const int32_t* __restrict__ nwin, const int64_t* __restrict__ doff,
     const uint2* __restrict__ desc, const int64_t* __restrict__ win_off, Window* __restrict__ wins,
     uint8_t* __restrict__ win_cat, const int64_t* __restrict__ start_off, int64_t start_budget,
-    uint32_t* __restrict__ starts, int bs_x4) {
+    uint32_t* __restrict__ starts, int bs_x4, BinSum bs) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PlanWriteShared& s = *reinterpret_cast<PlanWriteShared*>(smem_raw);
     const int32_t hrow = blockIdx.x;
@@ -379,6 +478,39 @@ __global__ void __launch_bounds__(PLAN_T, 5) plan_write_kernel(
     const bool staged = tsz <= STAGE;
     uint32_t* tab = staged ? s.u.stage : starts + sofs;
     // entries are absolute B offsets (segment start b0 + element index)
+    if (bs.sptr) {
+        // bin summaries: an entry's first element offset is the exclusive prefix
+        // of the segment's run counts; windows starting in (previous entry's
+        // window, this entry's window] start at that offset
+        stream_summaries(m, bs, row, [&](int p, int q0, int nent, const uint32_t* ent,
+                                         int& carryw, int& eoff, int64_t b0, int blen) {
+#pragma unroll
+            for (int u = 0; u < PLAN_U; ++u) {
+                const int qb = q0 + 32 * u;
+                if (qb >= nent) break;
+                const bool valid = qb + lane < nent;
+                const int cntv = valid ? static_cast<int>(ent[u] & 0xffffu) : 0;
+                int incl = cntv;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const int excl = eoff + incl - cntv;
+                const int wq = valid ? s.binwin[ent[u] >> 16] : wtot;
+                int wp = __shfl_up_sync(0xffffffffu, wq, 1);
+                if (lane == 0) wp = carryw;
+                if (valid)
+                    for (int w2 = wp + 1; w2 <= wq; ++w2)
+                        tab[w2 * int64_t{d} + p] = static_cast<uint32_t>(b0 + excl);
+                carryw = __shfl_sync(0xffffffffu, wq, ::min(31, nent - 1 - qb));
+                eoff += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            if (q0 + 32 * PLAN_U >= nent)
+                for (int w2 = carryw + 1 + lane; w2 <= wtot; w2 += 32)
+                    tab[w2 * int64_t{d} + p] = static_cast<uint32_t>(b0 + blen);
+        });
+    } else
     stream_segments(m, row, [&](int p, int q0, int len, const int32_t* cols, int& carry,
                                 int64_t b0) {
         // carry: window of the element before this group (-1 at q0 == 0)
@@ -1096,6 +1228,7 @@ Mats make_mats(const bsp_csr* A, const bsp_csr* B) {
     Mats m{A->row_ptr, A->col_idx, A->values, B->row_ptr, B->col_idx, B->values,
            static_cast<int32_t>(B->ncols)};
     m.bnnz = B->nnz;
+    m.bnrows = B->nrows;
     return m;
 }
 
@@ -1225,8 +1358,32 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         d2h(h, &ndesc, doff.p + nh, 1);
         sync(h);
         DBuf<uint2> desc(h, ndesc);
+        // bin summaries of B for both planner passes (BSP_BIN_SUMMARY=0: stream columns)
+        static const bool use_sum = [] {
+            const char* e = std::getenv("BSP_BIN_SUMMARY");
+            return !(e && e[0] == '0');
+        }();
+        DBuf<int64_t> sptr;
+        DBuf<uint32_t> sent;
+        BinSum bs{};
+        if (use_sum) {
+            const int64_t nb = m.bnrows;
+            DBuf<int64_t> scnt(h, nb + 1);
+            BSP_CUDA(cudaMemsetAsync(scnt.p + nb, 0, sizeof(int64_t), h->stream));
+            const unsigned gs = static_cast<unsigned>(
+                std::max<int64_t>(1, std::min<int64_t>(div_up(nb, 8), int64_t{h->sm_count} * 16)));
+            BSP_LAUNCH(h, bin_summary_kernel<0>, gs, 256, 0, m.brp, m.bcol, nb, log_binw, scnt.p,
+                       nullptr, nullptr);
+            sptr = DBuf<int64_t>(h, nb + 1);
+            exclusive_scan_i64(h, scnt.p, sptr.p, nb + 1);
+            // bounded by nnz(B) (one entry per column at most): no readback
+            sent = DBuf<uint32_t>(h, std::max<int64_t>(m.bnnz, 1));
+            BSP_LAUNCH(h, bin_summary_kernel<1>, gs, 256, 0, m.brp, m.bcol, nb, log_binw, nullptr,
+                       sptr.p, sent.p);
+            bs = BinSum{sptr.p, sent.p};
+        }
         BSP_LAUNCH(h, plan_count_kernel, static_cast<unsigned>(nh), PLAN_T, 0, m, heavy, nbins,
-                   log_binw, nwin.p, doff.p, desc.p, capg);
+                   log_binw, nwin.p, doff.p, desc.p, capg, bs);
         DBuf<int64_t> woff(h, nh + 1);
         exclusive_scan_i32_to_i64(h, nwin.p, woff.p, nh + 1);
         // per-(window, segment) start tables, bounded per row and in total
@@ -1286,7 +1443,7 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
         BSP_LAUNCH(h, plan_write_kernel, static_cast<unsigned>(nh), PLAN_T,
                    sizeof(PlanWriteShared), m, heavy, nbins, log_binw, nwin.p, doff.p, desc.p,
                    woff.p, plan.wins.p, dense.p, use_starts ? soff.p : nullptr, budget,
-                   use_starts ? plan.starts.p : nullptr, bs_x4);
+                   use_starts ? plan.starts.p : nullptr, bs_x4, bs);
         plan.sparse_ids = DBuf<int32_t>(h, plan.nwin);
         plan.dense_ids = DBuf<int32_t>(h, plan.nwin);
         DBuf<unsigned long long> cnt(h, 2 * (NWCLS + 1));
