@@ -799,7 +799,7 @@ def merge_candidates(a: CsrMatrix, pairs: np.ndarray, params: ClusterParams = Cl
                                          C.byref(nc), C.byref(ptr), C.byref(rows), C.byref(nm),
                                          C.byref(mp)))
     asg = ClusterAssignment._adopt(int(nc.value), ptr, rows)
-    trace = default_engine()._adopt_pairs(mp, nm) if False else _adopt_pairs_plain(mp, nm)
+    trace = _adopt_pairs_plain(mp, nm)
     return asg, trace
 
 

@@ -4,9 +4,10 @@
 // (topk.cu / minhash.cu); the merge is sequential by design.
 #include "common.hpp"
 
+#include <parallel/algorithm>
+
 #include <algorithm>
 #include <queue>
-#include <unordered_set>
 
 namespace bsp {
 
@@ -32,6 +33,11 @@ double jaccard(const bsp_host_csr* a, int64_t i, int64_t j) {
     const int64_t uni = ni + nj - inter;
     return uni == 0 ? 0.0 : static_cast<double>(inter) / static_cast<double>(uni);
 }
+
+struct FlatClusters {
+    std::vector<int64_t> ptr;  // nclusters + 1
+    std::vector<int32_t> rows;
+};
 
 namespace {
 
@@ -81,29 +87,93 @@ inline uint64_t pair_key(int32_t lo, int32_t hi) {
     return (static_cast<uint64_t>(static_cast<uint32_t>(lo)) << 32) | static_cast<uint32_t>(hi);
 }
 
+// Set of (lo, hi) pair keys: open addressing, linear probing, rehash at half
+// load.  Replaces a node-based hash set (one allocation per candidate).
+class PairSet {
+    static constexpr uint64_t kEmpty = ~0ull;  // lo = hi = -1 never occurs
+    std::vector<uint64_t> slot_;
+    uint64_t mask_ = 0;
+    std::size_t count_ = 0;
+    static uint64_t mix(uint64_t k) {
+        k ^= k >> 33;
+        k *= 0xff51afd7ed558ccdull;
+        k ^= k >> 33;
+        return k;
+    }
+    void place(uint64_t key) {
+        uint64_t p = mix(key) & mask_;
+        while (slot_[p] != kEmpty) p = (p + 1) & mask_;
+        slot_[p] = key;
+    }
+
+public:
+    explicit PairSet(std::size_t expect) {
+        std::size_t cap = 64;
+        while (cap < 2 * expect) cap <<= 1;
+        slot_.assign(cap, kEmpty);
+        mask_ = cap - 1;
+    }
+    // true when the key was not present (std::unordered_set::insert().second)
+    bool insert(uint64_t key) {
+        uint64_t p = mix(key) & mask_;
+        for (;; p = (p + 1) & mask_) {
+            if (slot_[p] == key) return false;
+            if (slot_[p] == kEmpty) break;
+        }
+        if (2 * (count_ + 1) > slot_.size()) {
+            std::vector<uint64_t> old;
+            old.swap(slot_);
+            slot_.assign(old.size() * 2, kEmpty);
+            mask_ = slot_.size() - 1;
+            for (uint64_t k : old)
+                if (k != kEmpty) place(k);
+            place(key);
+        } else {
+            slot_[p] = key;
+        }
+        ++count_;
+        return true;
+    }
+};
+
 }  // namespace
 
-// reference clustering.hpp:122-183.
-std::vector<std::vector<int32_t>> merge_candidates(const bsp_host_csr* a,
-                                                   const bsp_candidate* pairs, int64_t npairs,
-                                                   double jacc_th, int32_t max_cluster,
-                                                   std::vector<bsp_candidate>* trace) {
-    std::vector<std::vector<int32_t>> clusters;
+// reference clustering.hpp:122-183.  Same pops in the same order as one max-heap
+// over (score, i, j): the candidate list is sorted best-first once (a total
+// order, so a sorted array pops exactly like the heap), and only re-scored root
+// pairs go through a (small) heap; each step takes the better of the two fronts.
+FlatClusters merge_candidates(const bsp_host_csr* a, const bsp_candidate* pairs, int64_t npairs,
+                              double jacc_th, int32_t max_cluster,
+                              std::vector<bsp_candidate>* trace) {
+    FlatClusters out;
     const int64_t n = a->nrows;
-    if (n == 0) return clusters;
-    std::priority_queue<Entry, std::vector<Entry>, Worse> heap;
-    std::unordered_set<uint64_t> known;
-    known.reserve(static_cast<std::size_t>(npairs) * 2 + 16);
+    out.ptr.push_back(0);
+    if (n == 0) return out;
+    std::vector<Entry> init(static_cast<std::size_t>(npairs));
+    PairSet known(static_cast<std::size_t>(npairs) + static_cast<std::size_t>(n) / 4);
     for (int64_t k = 0; k < npairs; ++k) {
         const int32_t lo = std::min(pairs[k].i, pairs[k].j);
         const int32_t hi = std::max(pairs[k].i, pairs[k].j);
-        heap.push({pairs[k].score, lo, hi});
+        init[k] = {pairs[k].score, lo, hi};
         known.insert(pair_key(lo, hi));
     }
+    const Worse worse;
+    const auto better = [&](const Entry& x, const Entry& y) { return worse(y, x); };
+    if (npairs > (1 << 16))
+        __gnu_parallel::sort(init.begin(), init.end(), better);
+    else
+        std::sort(init.begin(), init.end(), better);
+    std::priority_queue<Entry, std::vector<Entry>, Worse> heap;
     DisjointSet ds(n);
-    while (!heap.empty()) {
-        const Entry top = heap.top();
-        heap.pop();
+    std::size_t next = 0;
+    while (next < init.size() || !heap.empty()) {
+        Entry top;
+        if (heap.empty() || (next < init.size() && !worse(init[next], heap.top()))) {
+            top = init[next++];
+        } else {
+            top = heap.top();
+            heap.pop();
+        }
         const int32_t ri = ds.find(top.i), rj = ds.find(top.j);
         if (ri == rj) continue;
         if (ri == top.i && rj == top.j) {
@@ -114,21 +184,41 @@ std::vector<std::vector<int32_t>> merge_candidates(const bsp_host_csr* a,
             continue;
         }
         const int32_t lo = std::min(ri, rj), hi = std::max(ri, rj);
-        if (known.insert(pair_key(lo, hi)).second) {
+        if (known.insert(pair_key(lo, hi))) {
             const double s = jaccard(a, lo, hi);
             if (s >= jacc_th) heap.push({s, lo, hi});
         }
     }
-    std::vector<int32_t> cluster_of(n, -1);
+    // clusters numbered by their smallest row, rows ascending within a cluster
+    std::vector<int32_t> cluster_of(n, -1), root(n);
+    std::vector<int64_t> count;
     for (int64_t i = 0; i < n; ++i) {
         const int32_t r = ds.find(static_cast<int32_t>(i));
+        root[i] = r;
         if (cluster_of[r] == -1) {
-            cluster_of[r] = static_cast<int32_t>(clusters.size());
-            clusters.emplace_back();
+            cluster_of[r] = static_cast<int32_t>(count.size());
+            count.push_back(0);
         }
-        clusters[cluster_of[r]].push_back(static_cast<int32_t>(i));
+        ++count[cluster_of[r]];
     }
-    return clusters;
+    out.ptr.resize(count.size() + 1);
+    for (std::size_t c = 0; c < count.size(); ++c) out.ptr[c + 1] = out.ptr[c] + count[c];
+    out.rows.resize(n);
+    std::vector<int64_t> fill(out.ptr.begin(), out.ptr.end() - 1);
+    for (int64_t i = 0; i < n; ++i) out.rows[fill[cluster_of[root[i]]]++] = static_cast<int32_t>(i);
+    return out;
+}
+
+void export_flat(const FlatClusters& f, int64_t* nclusters_out, int64_t** cluster_ptr_out,
+                 int32_t** rows_out) {
+    const int64_t nc = static_cast<int64_t>(f.ptr.size()) - 1;
+    int64_t* ptr = host_malloc<int64_t>(nc + 1);
+    int32_t* rows = host_malloc<int32_t>(f.rows.size());
+    std::copy(f.ptr.begin(), f.ptr.end(), ptr);
+    std::copy(f.rows.begin(), f.rows.end(), rows);
+    *nclusters_out = nc;
+    *cluster_ptr_out = ptr;
+    *rows_out = rows;
 }
 
 }  // namespace bsp
@@ -194,9 +284,9 @@ int bsp_merge_candidates(const bsp_host_csr* A, const bsp_candidate* pairs, int6
     return guarded([&] {
         check_host_csr(A, "merge_candidates");
         std::vector<bsp_candidate> trace;
-        auto cl = merge_candidates(A, pairs, npairs, jacc_th, max_cluster,
-                                   merges_out ? &trace : nullptr);
-        export_assignment(cl, nclusters_out, cluster_ptr_out, rows_out);
+        const auto cl = merge_candidates(A, pairs, npairs, jacc_th, max_cluster,
+                                         merges_out ? &trace : nullptr);
+        export_flat(cl, nclusters_out, cluster_ptr_out, rows_out);
         if (merges_out) {
             *merges_out = host_malloc<bsp_candidate>(trace.size());
             std::copy(trace.begin(), trace.end(), *merges_out);
@@ -235,9 +325,9 @@ int bsp_hierarchical_clusters(bsp_handle h, const bsp_host_csr* A, double jacc_t
         }
         bsp_csr_free(h, &dA);
         check(rc);
-        cl = merge_candidates(A, pairs, npairs, jacc_th, max_cluster, nullptr);
+        const auto flat = merge_candidates(A, pairs, npairs, jacc_th, max_cluster, nullptr);
         std::free(pairs);
-        export_assignment(cl, nclusters_out, cluster_ptr_out, rows_out);
+        export_flat(flat, nclusters_out, cluster_ptr_out, rows_out);
     });
 }
 
