@@ -61,15 +61,23 @@ def bytes_alg(nnz_a, nnz_b, nnz_c, rows_a, rows_b, rows_c):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+    The sampler is started BEFORE the warm-up steps: nvidia-smi's start-up holds
+    driver locks for tens of ms, and a multiply whose allocation or launch waits
+    on them ran 40-90 ms long when the sampler started with the first timed step.
+    `mark()` is called at the start of the timed region; only the samples taken
+    after it (nvidia-smi's own timestamps) are summarised."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.t_mark = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -80,6 +88,10 @@ class ClockSampler:
         except Exception:
             self.proc = None
         return self
+
+    def mark(self):
+        import datetime
+        self.t_mark = datetime.datetime.now()
 
     def __exit__(self, *a):
         self.lines = []
@@ -92,16 +104,24 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        import datetime
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in self.lines:
             f = [x.strip() for x in l.split(",")]
+            if self.t_mark is not None:
+                try:
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f")
+                    if ts < self.t_mark:
+                        continue
+                except ValueError:
+                    pass
             try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
+                sm.append(float(f[1]))
+                mx = float(f[2])
             except (ValueError, IndexError):
                 continue
-            for nm, v in zip(names, f[3:7]):
+            for nm, v in zip(names, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
@@ -360,20 +380,21 @@ def main():
             return eng.spgemm_rowwise_sharded(A, A, gather=False)[0]
         return eng.spgemm_rowwise_range(A, A, r0, r1)
 
-    for _ in range(args.warmup):
-        C = step()
-        C.free()
-    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:  # started before the warm-up (see ClockSampler)
+        for _ in range(args.warmup):
+            C = step()
+            C.free()
+        torch.cuda.synchronize()
 
-    # ---- timed region: exactly K steps, events on the engine's stream ----
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    nnz_c_local = 0
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    l0 = eng.kernel_launches()
-    with ClockSampler(local) as clk:
+        # ---- timed region: exactly K steps, events on the engine's stream ----
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        nnz_c_local = 0
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = eng.kernel_launches()
+        clk.mark()
         t_wall0 = time.perf_counter()
         for s in range(args.steps):
             evs[s][0].record(stream)
@@ -607,9 +628,18 @@ def run_clustered(B, args):
             C.free()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
+        # per-kernel times of one more multiply (CUDA events around every launch)
+        eng.profile(True)
+        fn().free()
+        torch.cuda.synchronize()
+        kern = {k: round(v[1], 4) for k, v in
+                sorted(eng.profile_report().items(), key=lambda kv: -kv[1][1])[:12]}
+        eng.profile(False)
+        variant_kernels[len(variant_kernels)] = kern
         return float(np.mean(ts)), float(min(ts))
 
     variants = {}
+    variant_kernels = {}
     t0 = time.perf_counter()
     a = a0
     if cfg == 4:
@@ -660,6 +690,7 @@ def run_clustered(B, args):
         "variants_ms": {k: {"mean": round(v[0], 4), "best": round(v[1], 4),
                             "gflops": round(2.0 * products / (v[0] * 1e-3) / 1e9, 2)}
                         for k, v in variants.items()},
+        "variant_kernels_ms": {k: variant_kernels[i] for i, k in enumerate(variants)},
         "clusterwise_speedup_vs_" + name: round(ms_row / variants[cname][0], 3),
         "c_bit_identical_across_variants": bool(same),
         "preprocessing_s": {"reorder": round(t_reorder, 3), "cluster": round(t_cluster, 3)},

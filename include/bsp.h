@@ -120,7 +120,10 @@ typedef struct {
     int64_t units[16];    /* work units: [0..7] rows per class (0 empty; 1..6 light, at
                              most 128/512/1024/2048/3072/4096 products; 7 heavy), [8]
                              sparse windows, [9] dense windows, [10] cluster tiles, [11]
-                             of which union tiles (each B entry sorted once per cluster) */
+                             of which union tiles (each B entry sorted once per cluster),
+                             [12] two-row clusters on the cluster hash accumulator, [13]
+                             rows of duplicate-heavy clusters whose B-row reuse is too low
+                             to pay, run on the row-wise hash accumulator */
     int32_t kernels_launched;
     int32_t chunks;       /* row chunks: bsp_spgemm_rowwise_host splits A's rows when C
                              exceeds the device budget (half the free memory); 1 otherwise */

@@ -168,7 +168,11 @@ def load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise RuntimeError(f"libbsp.so not found at {LIB_PATH}; run python -m "
                            "paper_2507_21253_b200.build (no CPU fallback exists)")
-    lib = C.CDLL(str(LIB_PATH))
+    # BSP_LIB_VARIANT=name loads libbsp_name.so (an A/B build made by tools/build_variant.py
+    # with extra -D flags; experiments only)
+    variant = os.environ.get("BSP_LIB_VARIANT")
+    path = LIB_PATH.with_name(f"libbsp_{variant}.so") if variant else LIB_PATH
+    lib = C.CDLL(str(path))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -52,6 +52,7 @@ struct ClusterMats {
     const int32_t* __restrict__ bcol;
     const double* __restrict__ bval;
     int32_t ncols;
+    int64_t bnnz;  // nnz(B): bulk copies stay inside [0, bnnz)
 };
 
 // ---------------------------------------------------------------------------
@@ -250,21 +251,24 @@ constexpr int UMAXA = 1024;   // union tiles: A values staged (merged columns x 
 
 __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
                                         uint8_t* __restrict__ ccls, uint8_t* __restrict__ row_skip,
-                                        unsigned long long* __restrict__ counts, int union_ok) {
+                                        unsigned long long* __restrict__ counts, int union_ok,
+                                        int min_reuse10) {
     __shared__ unsigned s_cnt[NCC];
     if (threadIdx.x < NCC) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t c = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; c < ncl;
          c += int64_t{gridDim.x} * blockDim.x) {
         const int K = m.sizes[c];
-        int64_t P = 0, S = 0;
+        int64_t P = 0, S = 0, Sraw = 0;  // S: B entries staged (union_ok == 2: with the bulk copies' slack)
         const int64_t MC = m.ccp[c + 1] - m.ccp[c];
         for (int64_t u = m.ccp[c]; u < m.ccp[c + 1]; ++u) {
             const int32_t k = m.ccol[u];
             const int64_t len = m.brp[k + 1] - m.brp[k];
             const int live = __popc(m.mask[u]);
             P += static_cast<int64_t>(live) * len;
-            if (live) S += len;  // B entries the cluster loads (once each)
+            if (live) Sraw += len;
+            if (live && len > 0)  // B entries the cluster loads (once each)
+                S += union_ok == 2 ? (((m.brp[k] & 3) + len + 3) & ~int64_t{3}) : len;
         }
         // staged cluster tile: B rows of the cluster fit the stage, every
         // member fits one merge tile (otherwise the rows go to the row bins)
@@ -272,6 +276,14 @@ __global__ void cluster_products_kernel(ClusterMats m, int64_t ncl, int cbits,
         // tried — see DESIGN.md §4): classes by the cluster's total products
         int cl = 0;
         const bool keyfits = bit_length(static_cast<uint32_t>(K - 1)) + cbits <= 31;
+        // B-row reuse of the cluster = member products / B entries loaded once.
+        // Below min_reuse10 / 10 the shared loads do not pay for the cluster
+        // tile's member bookkeeping (measured, cfg4: pairs of stencil rows reuse
+        // 1.35x and run 26 ms on the cluster accumulator vs 16 ms row-wise; the
+        // paper finds the same on stencils): those rows take the row-wise classes.
+        if (10 * P < static_cast<int64_t>(min_reuse10) * Sraw) {
+            // cl = 0
+        } else
         if (union_ok && K >= 2 && K <= UMAXK && MC <= UMAXMC && MC * K <= UMAXA && S > 0 &&
             S <= 2048) {
             // union tile: each B entry expanded and sorted once for the cluster
@@ -479,15 +491,27 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
 template <int T, int CAPM>
 struct UnionShared {
     MergeShared<T, CAPM> m;
-    uint16_t pidx[CAPM];     // merged column (local) of each expanded entry
+    alignas(4) uint16_t pidx[CAPM];  // merged column (local) of each expanded entry
+                                     // (TMA: uint32 per 4 staged entries, shift << 16 | column)
     double sa[UMAXA];        // the cluster's A values, [p * K + l]
     uint32_t smask[UMAXMC];  // live members of merged column p
     int16_t runp[T];         // merged column of each compacted run of the chunk
     unsigned long long cnt[2][((CAPM + T - 1) / T) * (T / 32)];  // packed member counts
     int64_t mbase[UMAXK];
+    typename cub::BlockScan<unsigned long long, T>::TempStorage scan64;  // TMA staging offsets
 };
 
-template <int T, int CAPM>
+//
+// TMA = true (north star item 3): the cluster's B rows are STAGED in shared
+// memory by the TMA engine — one thread per merged column issues two bulk
+// copies (cp.async.bulk, columns and values) of the row's 16-byte-aligned
+// superset, all of them completing on one mbarrier — instead of one LDGSTS pair
+// per B entry.  Slack entries (<= 3 before and after a row) are overwritten
+// with a sentinel, and one pass compacts the staged columns into the sort
+// buffer; an entry's expansion index is its staged position (values and the
+// per-4-entries merged-column map stay where the copy put them).  Rows whose
+// superset would reach past nnz(B) are staged with plain loads.
+template <int T, int CAPM, bool TMA>
 __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
     cluster_union_kernel(ClusterMats m, const int32_t* __restrict__ ids, int csort,
                          const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
@@ -508,8 +532,80 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
     if (tid < K) us.mbase[tid] = crp[m.row_map[m.member_ptr[c] + tid]];
     for (int q = tid; q < MC * K; q += T) us.sa[q] = __ldg(m.aval + vbase + q);
     for (int q = tid; q < MC; q += T) us.smask[q] = __ldg(m.mask + u0 + q);
-    auto& x = s.ex();
     int total = 0, nruns = 0;
+    if constexpr (TMA) {
+        __shared__ __align__(8) uint64_t mbar;
+        uint32_t* stage = s.u.m.key1;  // staged columns, linear (idle sort buffer)
+        uint32_t* grp = reinterpret_cast<uint32_t*>(us.pidx);  // per 4 staged entries: shift << 16 | merged column
+        constexpr uint32_t SENT = 0xffffffffu;
+        if (tid == 0) mbar_init(&mbar, 1);
+        __syncthreads();
+        unsigned phase = 0;
+        int ptotal = 0;  // staged entries (with slack), a multiple of 4
+        const int64_t bulk_end = m.bnnz & ~int64_t{3};
+        for (int64_t uc = u0; uc < u1; uc += T) {
+            const int64_t u = uc + tid;
+            int len = 0, n4 = 0, lead = 0;
+            int64_t start = 0;
+            if (u < u1 && __ldg(m.mask + u) != 0u) {
+                const int32_t k = __ldg(m.ccol + u);
+                start = __ldg(m.brp + k);
+                len = static_cast<int>(__ldg(m.brp + k + 1) - start);
+                if (len > 0) {
+                    lead = static_cast<int>(start & 3);
+                    n4 = (lead + len + 3) & ~3;
+                }
+            }
+            // one scan: staged offset (bits 0-19), compact offset (20-39), run index (40+)
+            const unsigned long long packed = static_cast<unsigned long long>(n4) |
+                                              (static_cast<unsigned long long>(len) << 20) |
+                                              (static_cast<unsigned long long>(len > 0) << 40);
+            unsigned long long off, agg;
+            cub::BlockScan<unsigned long long, T>(us.scan64).ExclusiveSum(packed, off, agg);
+            const int po = ptotal + static_cast<int>(off & 0xfffffull);
+            const int co = total + static_cast<int>((off >> 20) & 0xfffffull);
+            const int r = nruns + static_cast<int>(off >> 40);
+            if (len > 0) {
+                if (r < S::MAXRUNS) s.ro(0)[r] = static_cast<uint16_t>(co);
+                const int64_t s4 = start - lead;
+                if (s4 + n4 <= bulk_end) {
+                    mbar_expect_tx(&mbar, static_cast<unsigned>(n4) * 12u);
+                    bulk_g2s(stage + po, m.bcol + s4, static_cast<unsigned>(n4) * 4u, &mbar);
+                    bulk_g2s(s.val + po, m.bval + s4, static_cast<unsigned>(n4) * 8u, &mbar);
+                } else {  // the last rows of B: no aligned superset inside the arrays
+                    for (int j = 0; j < len; ++j) {
+                        stage[po + lead + j] = static_cast<uint32_t>(__ldg(m.bcol + start + j));
+                        s.val[po + lead + j] = __ldg(m.bval + start + j);
+                    }
+                }
+                const uint32_t g = (static_cast<uint32_t>(po + lead - co) << 16) |
+                                   static_cast<uint32_t>(u - u0);
+                for (int j = 0; j < n4; j += 4) grp[(po + j) >> 2] = g;
+            }
+            __syncthreads();  // every expect_tx is registered before the arrival
+            if (tid == 0) mbar_arrive(&mbar);
+            mbar_wait(&mbar, phase);
+            phase ^= 1u;
+            if (len > 0) {  // mask the slack around the row
+                for (int j = 0; j < lead; ++j) stage[po + j] = SENT;
+                for (int j = lead + len; j < n4; ++j) stage[po + j] = SENT;
+            }
+            ptotal += static_cast<int>(agg & 0xfffffull);
+            total += static_cast<int>((agg >> 20) & 0xfffffull);
+            nruns += static_cast<int>(agg >> 40);
+        }
+        __syncthreads();
+        // compact the staged columns into the sort buffer (k order kept)
+        for (int e = tid; e < ptotal; e += T) {
+            const uint32_t k = stage[e];
+            if (k != SENT) {
+                const int g = e - static_cast<int>(grp[e >> 2] >> 16);
+                s.key0[PADI(g)] = k;
+                s.idx0[PADI(g)] = static_cast<uint16_t>(e);
+            }
+        }
+    } else {
+    auto& x = s.ex();
     for (int64_t uc = u0; uc < u1; uc += T) {
         const int64_t u = uc + tid;
         int len = 0;
@@ -553,15 +649,23 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
         nruns += nr;
         __syncthreads();
     }
+    }
     if (tid == 0) {
         if (nruns <= S::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
         s.nruns = nruns;
     }
     __syncthreads();
     // keys are absolute columns (kofs = 0: idx0 is set by the sort's prep)
-    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(m.ncols), csort, 0, false, 0);
+    // (TMA: idx0 already holds the staged positions)
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(m.ncols), csort, 0, false,
+                                     TMA ? -1 : 0);
     const uint32_t* KS = s.key(b);
     const uint16_t* X = s.idx(b);
+    // merged column (local) of expansion index xe
+    auto mcol = [&](int xe) -> int {
+        if constexpr (TMA) return static_cast<int>(reinterpret_cast<const uint32_t*>(us.pidx)[xe >> 2] & 0xffffu);
+        else return us.pidx[xe];
+    };
     uint32_t* umask = b ? s.key0 : s.u.m.key1;  // the buffer the sort left idle
     // pass A: each head's member mask (OR over its run) and the per-(row, warp)
     // head counts of every member (16-bit fields, members 0-3 and 4-7)
@@ -581,7 +685,7 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
             const uint32_t key = KS[PADI(o)];
             int e = o;
             do {
-                M |= us.smask[us.pidx[X[PADI(e)]]];
+                M |= us.smask[mcol(X[PADI(e)])];
                 ++e;
             } while (e < total && KS[PADI(e)] == key);
             umask[o] = M;
@@ -656,7 +760,7 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
         int e = o;
         do {
             const int xe = X[PADI(e)];
-            const int p = us.pidx[xe];
+            const int p = mcol(xe);
             const double bv = s.val[xe];
             const uint32_t mp = us.smask[p];
             const double* ap = us.sa + p * K;
@@ -737,21 +841,42 @@ __global__ void __launch_bounds__(T) cluster_union_count_kernel(ClusterMats m,
     if (tid < K) row_nnz[m.row_map[m.member_ptr[c] + tid]] = s_cnt[tid];
 }
 
+// BSP_CLUSTER_TMA=1: the union tiles stage their B rows with bulk copies instead
+// of gathering them with per-entry LDGSTS.  Bulk copies also need 16-byte
+// aligned B arrays (cudaMalloc'ed arrays are; a caller's offset view may not be).
+bool union_tma(const ClusterMats& m) {
+    static const bool on = [] {
+        const char* e = std::getenv("BSP_CLUSTER_TMA");
+        return e && e[0] == '1';  // measured slower on cfg2 (0.986 vs 0.919 ms): off by default
+    }();
+    return on && (reinterpret_cast<uintptr_t>(m.bcol) & 15u) == 0 &&
+           (reinterpret_cast<uintptr_t>(m.bval) & 15u) == 0;
+}
+
 template <int T, int CAPM>
 void launch_union(bsp_handle h, const ClusterMats& m, const int32_t* ids, int64_t n,
                   const int64_t* crp, int32_t* ocol, double* oval) {
     if (n <= 0) return;
     using U = UnionShared<T, CAPM>;
-    auto k = cluster_union_kernel<T, CAPM>;
     static const std::string nm =
         "cluster_union<" + std::to_string(T) + "," + std::to_string(CAPM) + ">";
+    static const std::string nm_tma =
+        "cluster_union_tma<" + std::to_string(T) + "," + std::to_string(CAPM) + ">";
     static const int csort = [] {
         const char* e = std::getenv("BSP_CSORT");
         return e ? std::atoi(e) : 1000;
     }();
-    set_smem(k, sizeof(U));
-    BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(U), m, ids, csort, crp,
-                  ocol, oval);
+    if (union_tma(m)) {
+        auto k = cluster_union_kernel<T, CAPM, true>;
+        set_smem(k, sizeof(U));
+        BSP_LAUNCH_AS(h, nm_tma.c_str(), k, static_cast<unsigned>(n), T, sizeof(U), m, ids, csort,
+                      crp, ocol, oval);
+    } else {
+        auto k = cluster_union_kernel<T, CAPM, false>;
+        set_smem(k, sizeof(U));
+        BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(U), m, ids, csort, crp,
+                      ocol, oval);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -873,13 +998,17 @@ __global__ void __launch_bounds__(CH_WARPS * 32)
             mk[u] = e < U ? keys[e] : 0x7fffffff;
             rk[u] = 0;
         }
-        const int nu = (U + 31) >> 5;
-        for (int jj = 0; jj < U; ++jj) {
-            const int32_t kj = keys[jj];
+        auto rank_cols = [&](auto nu_c) {
+            constexpr int NU = decltype(nu_c)::value;
+            for (int jj = 0; jj < U; ++jj) {
+                const int32_t kj = keys[jj];
 #pragma unroll
-            for (int u = 0; u < PER; ++u)
-                if (u < nu) rk[u] += kj < mk[u];
-        }
+                for (int u = 0; u < NU; ++u) rk[u] += kj < mk[u];
+            }
+        };
+        if (U <= 128) rank_cols(std::integral_constant<int, 4>{});
+        else if (U <= 256) rank_cols(std::integral_constant<int, 8>{});
+        else rank_cols(std::integral_constant<int, PER>{});
 #pragma unroll
         for (int u = 0; u < PER; ++u)
             if (u * 32 + lane < U) order[rk[u]] = static_cast<uint16_t>(u * 32 + lane);
@@ -911,33 +1040,50 @@ __global__ void __launch_bounds__(CH_WARPS * 32)
     }
 }
 
-// After the symbolic pass: clusters of two rows with products >= 2 x outputs and
-// <= CH_MAX outputs per member go to cluster_hashacc_kernel (hlist); the others
-// keep their class (tlists, per-class cursors).
+// After the symbolic pass: duplicate-heavy clusters (products >= 2 x outputs, <=
+// CH_MAX outputs per member) leave the sort tiles.  Two-row clusters whose B-row
+// reuse (products / B entries loaded once) reaches hacc_reuse10 / 10 go to
+// cluster_hashacc_kernel (hlist); the other duplicate-heavy clusters hand their
+// member rows to the row-wise hash accumulator (rlist) — measured on cfg4
+// (RCM + hierarchical: pairs of stencil rows, reuse 1.5x): 18.9 ms on the cluster
+// accumulator vs 13.0 ms row-wise, the shared loads saving less than the
+// per-member bookkeeping costs (the paper's own stencil finding).  The rest keep
+// their class (tlists, per-class cursors).  cursor[NCC] counts rlist's rows.
 __global__ void route_cluster_kernel(ClusterMats m, const int32_t* __restrict__ lists,
                                      const uint8_t* __restrict__ ccls, int64_t nlist,
                                      const int64_t* __restrict__ crp,
                                      unsigned long long* __restrict__ cursor,
-                                     int32_t* __restrict__ hlist, int32_t* __restrict__ tlists) {
+                                     int32_t* __restrict__ hlist, int32_t* __restrict__ tlists,
+                                     int32_t* __restrict__ rlist, int hacc_reuse10) {
     const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
     if (t >= nlist) return;
     const int32_t c = lists[t];
     const int64_t mb = m.member_ptr[c];
-    bool hash = false;
-    if (m.member_ptr[c + 1] - mb == 2) {
-        const int32_t r0 = m.row_map[mb], r1 = m.row_map[mb + 1];
-        const int64_t z0 = crp[r0 + 1] - crp[r0], z1 = crp[r1 + 1] - crp[r1];
-        int64_t P = 0;
-        for (int64_t u = m.ccp[c]; u < m.ccp[c + 1]; ++u) {
-            const int32_t k = m.ccol[u];
-            P += static_cast<int64_t>(__popc(m.mask[u])) * (m.brp[k + 1] - m.brp[k]);
-        }
-        hash = z0 <= CH_MAX && z1 <= CH_MAX && P >= 2 * (z0 + z1);
+    const int K = static_cast<int>(m.member_ptr[c + 1] - mb);
+    int64_t Z = 0, zmax = 0;
+    for (int l = 0; l < K; ++l) {
+        const int32_t r = m.row_map[mb + l];
+        const int64_t z = crp[r + 1] - crp[r];
+        Z += z;
+        zmax = max(zmax, z);
     }
-    if (hash)
+    int64_t P = 0, S = 0;
+    for (int64_t u = m.ccp[c]; u < m.ccp[c + 1]; ++u) {
+        const int32_t k = m.ccol[u];
+        const int64_t len = m.brp[k + 1] - m.brp[k];
+        const int live = __popc(m.mask[u]);
+        P += static_cast<int64_t>(live) * len;
+        if (live) S += len;
+    }
+    const bool dup = zmax <= CH_MAX && P >= 2 * Z;
+    if (dup && K == 2 && 10 * P >= static_cast<int64_t>(hacc_reuse10) * S) {
         hlist[atomicAdd(&cursor[0], 1ull)] = c;
-    else
+    } else if (dup) {
+        const unsigned long long o = atomicAdd(&cursor[NCC], static_cast<unsigned long long>(K));
+        for (int l = 0; l < K; ++l) rlist[o + l] = m.row_map[mb + l];
+    } else {
         tlists[atomicAdd(&cursor[ccls[c]], 1ull)] = c;
+    }
 }
 
 template <int T, int CAPM>
@@ -1131,7 +1277,8 @@ __global__ void __launch_bounds__(CN_WARPS * 32)
 ClusterMats make_cluster_mats(const bsp_csr_cluster* a, const bsp_csr* b) {
     return ClusterMats{a->cluster_sizes, a->member_ptr, a->cluster_col_ptr, a->col_idx,
                        a->value_ptr,     a->values,     a->member_mask,     a->row_map,
-                       b->row_ptr,       b->col_idx,    b->values,          static_cast<int32_t>(b->ncols)};
+                       b->row_ptr,       b->col_idx,    b->values,          static_cast<int32_t>(b->ncols),
+                       b->nnz};
 }
 
 }  // namespace
@@ -1507,9 +1654,14 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         BSP_CUDA(cudaMemsetAsync(counts.p, 0, NCC * sizeof(unsigned long long), h->stream));
         // BSP_CLUSTER_UNION=0: member-keyed tiles only
         const char* ue = std::getenv("BSP_CLUSTER_UNION");
-        const int union_ok = (ue && ue[0] == '0') ? 0 : 1;
+        const int union_ok = (ue && ue[0] == '0') ? 0 : (union_tma(cm) ? 2 : 1);
+        // BSP_CLUSTER_MIN_REUSE (x10, default 15 = 1.5x): clusters sharing less go row-wise
+        static const int min_reuse10 = [] {
+            const char* e = std::getenv("BSP_CLUSTER_MIN_REUSE");
+            return e ? std::atoi(e) : 15;
+        }();
         BSP_LAUNCH(h, cluster_products_kernel, grid_for(h, ncl, 256), 256, 0, cm, ncl, cbits, ccls.p,
-                   skip.p, counts.p, union_ok);
+                   skip.p, counts.p, union_ok, min_reuse10);
         unsigned long long hc[NCC];
         d2h(h, hc, counts.p, NCC);
         sync(h);
@@ -1566,17 +1718,24 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
         const char* he = std::getenv("BSP_HACC");
         const bool repeats = 4 * h->stats.products >= 5 * std::max<int64_t>(1, nnz);
         if (acc > 0 && repeats && !(he && he[0] == '0')) {
-            DBuf<int32_t> hl(h, acc), tl(h, acc);
-            DBuf<unsigned long long> cur(h, NCC);
-            std::vector<unsigned long long> cu(NCC, 0);
+            DBuf<int32_t> hl(h, acc), tl(h, acc), rl(h, std::max<int64_t>(n, 1));
+            DBuf<unsigned long long> cur(h, NCC + 1);
+            std::vector<unsigned long long> cu(NCC + 1, 0);
             for (int c = 1; c < NCC; ++c) cu[c] = static_cast<unsigned long long>(off[c] - off[1]);
-            h2d(h, cur.p, cu.data(), NCC);
+            h2d(h, cur.p, cu.data(), NCC + 1);
+            // BSP_CLUSTER_HACC_REUSE (x10, default 20 = 2.0x): B-row reuse a two-row
+            // cluster needs for the cluster accumulator (below: row-wise accumulator)
+            static const int hacc_reuse10 = [] {
+                const char* e = std::getenv("BSP_CLUSTER_HACC_REUSE");
+                return e ? std::atoi(e) : 20;
+            }();
             BSP_LAUNCH(h, route_cluster_kernel, static_cast<unsigned>(div_up(acc, 256)), 256, 0, cm,
-                       lists.p + off[1], ccls.p, acc, rp.p, cur.p, hl.p, tl.p);
-            unsigned long long hc2[NCC];
-            d2h(h, hc2, cur.p, NCC);
+                       lists.p + off[1], ccls.p, acc, rp.p, cur.p, hl.p, tl.p, rl.p, hacc_reuse10);
+            unsigned long long hc2[NCC + 1];
+            d2h(h, hc2, cur.p, NCC + 1);
             sync(h);
             const int64_t nh = static_cast<int64_t>(hc2[0]);
+            const int64_t nr = static_cast<int64_t>(hc2[NCC]);
             int64_t off2[NCC], cnt2[NCC];
             for (int c = 0; c < NCC; ++c) {
                 off2[c] = c == 0 ? 0 : off[c] - off[1];
@@ -1589,6 +1748,11 @@ int bsp_spgemm_clusterwise(bsp_handle h, const bsp_csr_cluster* A, const bsp_csr
                 BSP_LAUNCH(h, cluster_hashacc_kernel, grid, CH_WARPS * 32, sizeof(ClusterHaccShared),
                            cm, hl.p, nh, rp.p, pay.col_idx(), pay.values());
             }
+            if (nr > 0) {
+                sort_ids(h, rl.p, nr);  // row order: neighbouring rows share B rows in L2
+                run_hashacc_rows(h, m, rl.p, nr, 0, rp.p, pay.col_idx(), pay.values());
+            }
+            h->stats.units[13] = nr;  // cluster rows on the row-wise accumulator
             h->stats.units[12] = nh;
             run_cluster_classes(h, cm, tl.p, off2, cnt2, cbits, rp.p, pay.col_idx(), pay.values());
         } else {

@@ -191,20 +191,48 @@ void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes) {
     if (gap_log_enabled()) gap_mark_sync();
 }
 
-size_t available_bytes(bsp_handle h) {
-    size_t free_b = 0, total_b = 0;
-    const auto t0 = std::chrono::steady_clock::now();
-    BSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (gap_log_enabled())
-        gap_slow_call("cudaMemGetInfo", std::chrono::duration<double, std::milli>(
-                                            std::chrono::steady_clock::now() - t0).count());
+// Device bytes a new allocation of this handle can get: free HBM outside the
+// handle's pools plus the pools' reserved-but-unused bytes.
+// cudaMemGetInfo takes a device-wide driver lock: on a box where anything polls
+// the GPU (nvidia-smi, DCGM) it blocked for 5-180 ms every few calls, idling
+// the GPU at the start of a multiply (measured on cfg5: one step in four
+// +5..+180 ms, tools/step_gaps.py).  So the driver is asked only when the
+// handle has no figure yet, every BSP_MEMINFO_PERIOD_S seconds (default 60),
+// or on request (refresh: a failed allocation); in between, the figure follows
+// the growth of this handle's own pools (cudaMemPoolGetAttribute, no device
+// lock), which is where a multiply's memory goes.  Memory taken by other users
+// of the device is seen at the next refresh.
+size_t available_bytes(bsp_handle h, bool refresh) {
+    uint64_t reserved_all = 0, unused = 0;
     for (cudaMemPool_t pool : {h->scratch_pool, h->out_pool}) {
         uint64_t reserved = 0, used = 0;
         BSP_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
         BSP_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
-        free_b += static_cast<size_t>(reserved - used);
+        reserved_all += reserved;
+        unused += reserved - used;
     }
-    return free_b;
+    static const double period_s = [] {
+        const char* e = std::getenv("BSP_MEMINFO_PERIOD_S");
+        return e ? std::atof(e) : 60.0;
+    }();
+    const auto now = std::chrono::steady_clock::now();
+    if (refresh || h->free_outside < 0 ||
+        std::chrono::duration<double>(now - h->free_time).count() > period_s) {
+        size_t free_b = 0, total_b = 0;
+        BSP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (gap_log_enabled())
+            gap_slow_call("cudaMemGetInfo", std::chrono::duration<double, std::milli>(
+                                                std::chrono::steady_clock::now() - now).count());
+        h->free_outside = static_cast<int64_t>(free_b);
+        h->free_reserved = reserved_all;
+        h->free_time = now;
+    }
+    // pools grown since the query took their memory from the free part
+    int64_t outside = h->free_outside - (static_cast<int64_t>(reserved_all) -
+                                         static_cast<int64_t>(h->free_reserved));
+    if (outside < 0) outside = 0;
+    // blocks in the handle's cache go back to the pools on the first miss
+    return static_cast<size_t>(outside) + static_cast<size_t>(unused) + h->cached_bytes;
 }
 
 }  // namespace bsp
@@ -256,6 +284,7 @@ int bsp_destroy(bsp_handle h) {
         if (!h) return;
         cudaStreamSynchronize(h->stream);
         if (h->comm) bsp_comm_destroy(h);
+        flush_block_cache(h);
         if (h->keep_starts) {
             cudaFreeAsync(h->keep_starts, h->stream);
             cudaStreamSynchronize(h->stream);
@@ -280,6 +309,7 @@ int bsp_set_stream(bsp_handle h, void* s) {
     return guarded([&] {
         require(h != nullptr, "bsp_set_stream: null handle");
         BSP_CUDA(cudaSetDevice(h->device));
+        flush_block_cache(h);  // cached blocks are ordered on the old stream
         if (h->own_stream) {
             BSP_CUDA(cudaStreamSynchronize(h->stream));
             BSP_CUDA(cudaStreamDestroy(h->stream));

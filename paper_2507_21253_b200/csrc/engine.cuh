@@ -7,7 +7,10 @@
 
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -54,6 +57,27 @@ struct bsp_handle_s {
     // between two kernels of a multiply).
     void* keep_starts = nullptr;
     size_t keep_starts_bytes = 0;
+    // Free device memory outside this handle's pools, as of the last
+    // cudaMemGetInfo (free_outside), with the pools' reserved bytes at that
+    // moment: available_bytes() then follows the pools' own growth without
+    // asking the driver again (see available_bytes).
+    int64_t free_outside = -1;
+    uint64_t free_reserved = 0;
+    std::chrono::steady_clock::time_point free_time{};
+    // Block cache above the pools (see dalloc): freed blocks by (pool, bytes),
+    // live blocks by address.
+    struct BlockInfo {
+        size_t bytes;
+        int pool;
+    };
+    std::unordered_map<void*, BlockInfo> live_blocks;
+    struct FreeBlock {
+        void* p;
+        uint64_t stamp;  // alloc_seq when it was freed
+    };
+    std::unordered_multimap<uint64_t, FreeBlock> free_blocks;  // key = bytes << 1 | pool
+    size_t cached_bytes = 0;
+    uint64_t alloc_seq = 0;
     const void* part_key[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t part_nnz[2] = {0, 0};
     std::vector<int64_t> part_bounds;
@@ -127,29 +151,103 @@ void gap_check_launch(const char* name);
 enum class Pool { scratch, out };
 
 void gap_slow_call(const char* what, double ms);
-template <typename T>
-T* dalloc(bsp_handle h, int64_t n, Pool pool = Pool::scratch) {
+
+// Stream-ordered allocation with a per-handle block cache.  A repeated multiply
+// asks for the same block sizes again, and every driver allocation call — even
+// cudaMallocFromPoolAsync served from the pool's cached memory — takes driver
+// locks that a GPU monitor (nvidia-smi, DCGM) holds for milliseconds at a time
+// (measured on cfg5 under `nvidia-smi -lms 250`: pool allocations of 20-50 ms
+// inside a multiply, one step in five 5-15 % long).  Freed blocks are therefore
+// kept by exact size and handed back without a driver call.  A request the
+// cache cannot serve allocates from the pool; blocks that no request has
+// matched for kBlockMaxAge allocations go back to the pool then, and when the
+// pool is out of memory every cached block goes back before one retry (so a
+// different workload gets the memory it would have had without the cache;
+// available_bytes counts cached blocks as available).  All blocks of a handle
+// are used in its stream's order, like the stream-ordered frees they replace;
+// changing the stream or destroying the handle flushes the cache.
+constexpr uint64_t kBlockMaxAge = 4096;
+
+inline void flush_block_cache(bsp_handle h) {
+    for (auto& kv : h->free_blocks) cudaFreeAsync(kv.second.p, h->stream);
+    h->free_blocks.clear();
+    h->cached_bytes = 0;
+}
+
+inline void* dalloc_bytes(bsp_handle h, size_t bytes, Pool pool) {
+    const int pi = pool == Pool::out ? 1 : 0;
+    const uint64_t key = (static_cast<uint64_t>(bytes) << 1) | static_cast<uint64_t>(pi);
+    ++h->alloc_seq;
+    auto it = h->free_blocks.find(key);
+    if (it != h->free_blocks.end()) {
+        void* p = it->second.p;
+        h->free_blocks.erase(it);
+        h->cached_bytes -= bytes;
+        h->live_blocks[p] = {bytes, pi};
+        return p;
+    }
+    // miss: stale blocks go back to the pool first
+    for (auto jt = h->free_blocks.begin(); jt != h->free_blocks.end();) {
+        if (h->alloc_seq - jt->second.stamp > kBlockMaxAge) {
+            cudaFreeAsync(jt->second.p, h->stream);
+            h->cached_bytes -= static_cast<size_t>(jt->first >> 1);
+            jt = h->free_blocks.erase(jt);
+        } else {
+            ++jt;
+        }
+    }
     void* p = nullptr;
-    const size_t bytes = static_cast<size_t>(n > 0 ? n : 1) * sizeof(T);
     const bool lg = gap_log_enabled();
     const auto t0 = lg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
-    cuda_check(cudaMallocFromPoolAsync(&p, bytes, pool == Pool::out ? h->out_pool : h->scratch_pool,
-                                       h->stream),
-               "cudaMallocFromPoolAsync");
+    cudaMemPool_t mp = pool == Pool::out ? h->out_pool : h->scratch_pool;
+    cudaError_t me = cudaMallocFromPoolAsync(&p, bytes, mp, h->stream);
+    if (me == cudaErrorMemoryAllocation && !h->free_blocks.empty()) {
+        cudaGetLastError();
+        flush_block_cache(h);
+        me = cudaMallocFromPoolAsync(&p, bytes, mp, h->stream);
+    }
+    if (me == cudaErrorMemoryAllocation) h->free_outside = -1;  // the cached figure was wrong
+    cuda_check(me, "cudaMallocFromPoolAsync");
     if (lg)
         gap_slow_call("cudaMallocFromPoolAsync",
                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
                           .count());
-    return static_cast<T*>(p);
+    h->live_blocks[p] = {bytes, pi};
+    return p;
+}
+
+template <typename T>
+T* dalloc(bsp_handle h, int64_t n, Pool pool = Pool::scratch) {
+    return static_cast<T*>(
+        dalloc_bytes(h, static_cast<size_t>(n > 0 ? n : 1) * sizeof(T), pool));
 }
 
 inline void dfree(bsp_handle h, void* p) {
-    if (p) cudaFreeAsync(p, h->stream);
+    if (!p) return;
+    auto it = h->live_blocks.find(p);
+    if (it == h->live_blocks.end()) {  // not this handle's block: plain stream-ordered free
+        cudaFreeAsync(p, h->stream);
+        return;
+    }
+    const auto info = it->second;
+    h->live_blocks.erase(it);
+    static const bool cache_on = [] {
+        const char* e = std::getenv("BSP_BLOCK_CACHE");
+        return !(e && e[0] == '0');
+    }();
+    if (!cache_on) {
+        cudaFreeAsync(p, h->stream);
+        return;
+    }
+    h->free_blocks.emplace((static_cast<uint64_t>(info.bytes) << 1) | static_cast<uint64_t>(info.pool),
+                           bsp_handle_s::FreeBlock{p, h->alloc_seq});
+    h->cached_bytes += info.bytes;
 }
 
 // Device bytes available to a new allocation: free HBM plus what the
 // handle's pools hold cached but unused.
-size_t available_bytes(bsp_handle h);
+// refresh = true: ask the driver now (allocation failures, explicit requests).
+size_t available_bytes(bsp_handle h, bool refresh = false);
 
 // RAII device buffer bound to a handle's stream.
 template <typename T>

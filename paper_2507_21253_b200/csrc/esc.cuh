@@ -7,6 +7,9 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
+#include <mutex>
+#include <unordered_map>
+
 namespace bsp {
 
 constexpr int CAP = 4096;     // max products of one sparse tile (smem ESC)
@@ -236,6 +239,10 @@ void plan_symbolic(bsp_handle h, const Mats& m, const RowwisePlan& plan, int64_t
 void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
                   const int64_t* win_scan, int32_t* ccol, double* cval, int skip_wcls = -1);
 void sort_ids(bsp_handle h, int32_t* ids, int64_t n);
+// Duplicate-heavy rows (absolute ids, each with at most 256 outputs) on the row-wise hash
+// accumulator (rowwise.cu hashacc_kernel); C placed at crp[row - rb].
+void run_hashacc_rows(bsp_handle h, const Mats& m, const int32_t* rows, int64_t n, int64_t rb,
+                      const int64_t* crp, int32_t* ccol, double* cval);
 
 // B with <= 64 columns: per-row 64-bit column masks of B, then the row-wise
 // narrow kernel over rows [0, n) of A (skip[r] != 0 rows left out): symbolic
@@ -246,8 +253,24 @@ void narrow64_rows(bsp_handle h, const Mats& m, const unsigned long long* mask, 
                    const uint8_t* skip, int64_t* row_nnz, const int64_t* crp, int32_t* ccol,
                    double* cval, unsigned long long* products);
 
+// Opt a kernel into `bytes` of dynamic shared memory.  The attribute is set once
+// per (kernel, device): cudaFuncSetAttribute is a driver call that can wait on
+// the driver's locks (measured: up to 13 ms under a GPU monitor), and every
+// multiply would otherwise make ~40 of them.
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
+    // (kernels of one signature share this instantiation: keyed by address and device)
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t key = reinterpret_cast<uint64_t>(reinterpret_cast<const void*>(kernel)) ^
+                         (static_cast<uint64_t>(dev) << 56);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = done.find(key);
+        if (it != done.end() && it->second == bytes) return;
+    }
     const bool lg = gap_log_enabled();
     const auto t0 = lg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
     BSP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -255,6 +278,8 @@ void set_smem(K kernel, size_t bytes) {
     if (lg)
         gap_slow_call("cudaFuncSetAttribute", std::chrono::duration<double, std::milli>(
                                                   std::chrono::steady_clock::now() - t0).count());
+    std::lock_guard<std::mutex> lk(mu);
+    done[key] = bytes;
 }
 
 }  // namespace bsp

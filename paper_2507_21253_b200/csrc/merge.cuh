@@ -55,7 +55,7 @@ struct MergeShared {
     uint32_t key0[NP];
     uint16_t idx0[NP];
     uint16_t ro0[MAXRUNS + 2];
-    double val[CAPM];
+    alignas(16) double val[CAPM];  // 16-byte aligned: a bulk-copy destination (cluster.cu)
     // buffer 1 of the merge, aliased with the radix sort's temp storage, the
     // counting sort's arrays and the expansion state
     union U {
@@ -113,6 +113,56 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// Bulk (TMA engine) global -> shared copies completing on an mbarrier
+// (sm_90+ cp.async.bulk, SASS UBLKCP; the wait is SYNCS).  Source, destination
+// and size must be multiples of 16 bytes: callers copy the 16-byte-aligned
+// superset of a B-row segment and mask the slack.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int arrivals) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(arrivals)
+                 : "memory");
+    // make the initialised barrier visible to the async proxy
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+// Generic-proxy accesses to shared memory ordered before later async-proxy
+// (bulk copy) accesses to the same locations.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+// Adds `bytes` to the barrier's pending transaction count (no arrival).
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    unsigned done;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 // Warp-contiguous split of `ct` flattened run elements over `nwarps` warps
@@ -544,10 +594,30 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
             int c = lo;
             if (hi - lo > 1) {
                 c = lo & ~3;
+#if defined(BSP_X_RANKPIPE)
+                // next group loaded before the current one is counted
+                int j = c;
+                uint4 w = *reinterpret_cast<const uint4*>(pk + j);
+                for (j += 4; j < hi; j += 4) {
+                    const uint4 wn = *reinterpret_cast<const uint4*>(pk + j);
+                    c += (w.x < v) + (w.y < v) + (w.z < v) + (w.w < v);
+                    w = wn;
+                }
+                c += (w.x < v) + (w.y < v) + (w.z < v) + (w.w < v);
+#elif defined(BSP_X_RANK8)
+                for (int j = c; j < hi; j += 8) {
+                    const uint4 w = *reinterpret_cast<const uint4*>(pk + j);
+                    uint4 w2 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                    if (j + 4 < hi) w2 = *reinterpret_cast<const uint4*>(pk + j + 4);
+                    c += (w.x < v) + (w.y < v) + (w.z < v) + (w.w < v);
+                    c += (w2.x < v) + (w2.y < v) + (w2.z < v) + (w2.w < v);
+                }
+#else
                 for (int j = c; j < hi; j += 4) {
                     const uint4 w = *reinterpret_cast<const uint4*>(pk + j);
                     c += (w.x < v) + (w.y < v) + (w.z < v) + (w.w < v);
                 }
+#endif
             }
             const uint32_t col = rel + cmin - static_cast<uint32_t>(kofs > 0 ? kofs : 0);
             s.key0[PADI(c)] = cbits > 0 ? (mem << cbits) | col : col;

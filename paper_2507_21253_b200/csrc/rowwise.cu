@@ -1649,11 +1649,19 @@ __global__ void __launch_bounds__(HACC_WARPS * 32)
             mv[u] = i < nnz ? vals[i] : 0.0;
             rk[u] = 0;
         }
-        for (int jj = 0; jj < nnz; ++jj) {
-            const int32_t kj = keys[jj];
+        // (only the lane slots that hold columns are ranked: cfg4's rows hold
+        // 125 columns = 4 of the 8 slots, and the ranking is most of the row's work)
+        auto rank_cols = [&](auto nu_c) {
+            constexpr int NU = decltype(nu_c)::value;
+            for (int jj = 0; jj < nnz; ++jj) {
+                const int32_t kj = keys[jj];
 #pragma unroll
-            for (int u = 0; u < PER; ++u) rk[u] += kj < mk[u];
-        }
+                for (int u = 0; u < NU; ++u) rk[u] += kj < mk[u];
+            }
+        };
+        if (nnz <= 64) rank_cols(std::integral_constant<int, 2>{});
+        else if (nnz <= 128) rank_cols(std::integral_constant<int, 4>{});
+        else rank_cols(std::integral_constant<int, PER>{});
         const int64_t base = crp[row - rb];
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
@@ -1684,6 +1692,17 @@ __global__ void route_light_kernel(const int32_t* __restrict__ lists, int64_t nl
         while (c < NCLS - 1 && P > kClassCap[c]) ++c;
         tlists[atomicAdd(&cursor[c], 1ull)] = row;
     }
+}
+
+// Rows (absolute ids; at most HACC_MAX outputs each) on the hash accumulator.
+void run_hashacc_rows(bsp_handle h, const Mats& m, const int32_t* rows, int64_t n, int64_t rb,
+                      const int64_t* crp, int32_t* ccol, double* cval) {
+    if (n <= 0) return;
+    set_smem(hashacc_kernel, sizeof(HaccShared));
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>(div_up(n, HACC_WARPS), int64_t{h->sm_count} * 16)));
+    BSP_LAUNCH(h, hashacc_kernel, grid, HACC_WARPS * 32, sizeof(HaccShared), m, rows, n, rb, crp,
+               ccol, cval);
 }
 
 void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const int64_t* crp,
@@ -1724,13 +1743,7 @@ void plan_numeric(bsp_handle h, const Mats& m, const RowwisePlan& plan, const in
     unsigned long long hc[NCLS];
     d2h(h, hc, cursor.p, NCLS);
     const int64_t nh = static_cast<int64_t>(hc[0]);
-    if (nh > 0) {
-        set_smem(hashacc_kernel, sizeof(HaccShared));
-        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-            1, std::min<int64_t>(div_up(nh, HACC_WARPS), int64_t{h->sm_count} * 16)));
-        BSP_LAUNCH(h, hashacc_kernel, grid, HACC_WARPS * 32, sizeof(HaccShared), m, hlist.p, nh,
-                   plan.rb, crp, ccol, cval);
-    }
+    run_hashacc_rows(h, m, hlist.p, nh, plan.rb, crp, ccol, cval);
     for (int c = NCLS - 2; c >= 1; --c) {
         const int64_t b0 = plan.class_off[c] - plan.class_off[1];
         const int64_t cnt = static_cast<int64_t>(hc[c]) - b0;
@@ -1995,10 +2008,13 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     int64_t cap = nnz;
     // the planner's allocations since the sample are small next to C; C's own
     // allocation still fails cleanly (BSP_ERR_OOM) if memory was taken meanwhile
-    const int64_t avail = plan.avail_hint;
+    int64_t avail = plan.avail_hint;
     if (lb) {
         cap = nnz + plan.wcls_prod[LBC];
-        // C (12 B per entry) + the look-back state, with a 1 GB margin
+        // C (12 B per entry) + the look-back state, with a 1 GB margin (a figure
+        // that says no is checked against the driver before it is believed)
+        if (12 * cap + 16 * nlb + (int64_t{1} << 30) > avail)
+            avail = static_cast<int64_t>(available_bytes(h, true));
         if (12 * cap + 16 * nlb + (int64_t{1} << 30) > avail) {
             // no room for the bound: count the class symbolically after all
             lb = false;
@@ -2015,6 +2031,7 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
         }
     }
     {
+        if (12 * cap > avail) avail = static_cast<int64_t>(available_bytes(h, true));
         if (12 * cap > avail)
             throw oom_error("spgemm_rowwise: C needs " + std::to_string(12 * cap >> 20) +
                             " MiB, more than the " + std::to_string(avail >> 20) +

@@ -223,3 +223,37 @@ def test_clusters_beyond_32_members(engine, k):
     big = random_csr(1100, 50, 0.05, 7)
     with pytest.raises(B.ContractError):  # the format's limit: 1024 rows per cluster
         engine.build_csr_cluster(engine.upload(big), B.fixed_length_clusters(big.nrows, 1025))
+
+
+_KNOB_SCRIPT = r"""
+import sys, numpy as np
+import oracle as O
+import paper_2507_21253_b200 as B
+e = B.default_engine()
+for cfg, scale in ((2, 512), (2, 2048), (4, 16), (5, 13)):
+    a = B.make_config(cfg, scale)
+    asg = e.hierarchical_clusters(a)
+    A = e.upload(a)
+    c = e.spgemm_clusterwise(e.build_csr_cluster(A, asg), A).download()
+    o = O.spgemm_rowwise(a, a)
+    assert np.array_equal(c.row_ptr, o.row_ptr) and np.array_equal(c.col_idx, o.col_idx), cfg
+    assert np.array_equal(c.values.view(np.uint64), o.values.view(np.uint64)), cfg
+names = set(e.profile_names()) if hasattr(e, "profile_names") else set()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"BSP_CLUSTER_TMA": "1"},
+                                 {"BSP_CLUSTER_TMA": "1", "BSP_CLUSTER_MIN_REUSE": "0"},
+                                 {"BSP_CLUSTER_MIN_REUSE": "0"},
+                                 {"BSP_CLUSTER_MIN_REUSE": "40"}])
+def test_cluster_knobs_bit_identical(env):
+    """The bulk-copy (TMA) staged union tile and the reuse routing threshold are read once
+    per process: each setting runs in its own process and must reproduce the oracle's C."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **env)
+    e["PYTHONPATH"] = root + os.pathsep + os.path.join(root, "tests") + os.pathsep + e.get("PYTHONPATH", "")
+    r = subprocess.run([sys.executable, "-c", _KNOB_SCRIPT], env=e, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
