@@ -255,7 +255,7 @@ def run_reference(args, world: int):
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------
@@ -508,7 +508,7 @@ def main():
             line["cpu_baseline"] = cb
         else:
             line["cpu_baseline"] = None
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -597,7 +597,7 @@ def run_tall_skinny(B, args, num_frontiers=10, batch=64, seed=0):
                                               f"only spgemm_rowwise timed"}
     for f in fs:
         f.free()
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 def run_clustered(B, args):
@@ -699,7 +699,7 @@ def run_clustered(B, args):
                      "traffic": None, "bytes_alg_per_step": bal, "peak_source": peak_kind,
                      "unit_of_work": "one full row-wise multiply"},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 def run_e2e(B, eng, host, n, ncols, args, total_products, rank=0, world=1, dist=None):
@@ -772,11 +772,35 @@ def run_e2e(B, eng, host, n, ncols, args, total_products, rank=0, world=1, dist=
         if s > 0:
             times.append(dt)
         del dev, A
+    # The copy floor of this box: the same bytes (every chunk's three arrays, same sizes)
+    # device -> pinned host on the copy stream with nothing else running — what the PCIe
+    # link allows for this step's output, measured beside the pipeline it bounds.
+    floor_ms = None
+    try:
+        src_i = torch.empty(max(max_nnz, 1), dtype=torch.int32, device="cuda")
+        src_v = torch.empty(max(max_nnz, 1), dtype=torch.float64, device="cuda")
+        src_r = torch.empty(max_rows + 1, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fstream = torch.cuda.Stream()  # torch's own stream (it outlives the copy handle)
+        with torch.cuda.stream(fstream):
+            f0.record(fstream)
+            for g, (r_, z_) in enumerate(sizes):
+                rp, ci, v = ring[g % 2]
+                rp[:r_ + 1].copy_(src_r[:r_ + 1], non_blocking=True)
+                ci[:z_].copy_(src_i[:z_], non_blocking=True)
+                v[:z_].copy_(src_v[:z_], non_blocking=True)
+            f1.record(fstream)
+        torch.cuda.synchronize()
+        floor_ms = f0.elapsed_time(f1)
+        del src_i, src_v, src_r
+    except Exception:
+        floor_ms = None
     ce.close()
     t = statistics.median(times)
     return {"value": 2.0 * total_products / t / 1e9, "unit": "GFLOP/s",
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * t,
-            "chunks": nchunks * world,
+            "chunks": nchunks * world, "d2h_copy_floor_ms": floor_ms,
             "path": "pinned H2D of A + bsp_spgemm_rowwise_range per row chunk + "
                     "bsp_csr_download_async of every chunk of C into a pinned host ring"
                     + (f" (per rank, {world} ranks, max over ranks)" if world > 1 else "")}
