@@ -23,6 +23,29 @@
 
 namespace bsp {
 
+// BSP_X_PHASE (tools/build_variant.py, experiments only): thread 0 of every
+// look-back window tile adds the cycles between consecutive phase marks to
+// g_phase[] (tools/phase_times.py prints the share of each phase).
+#ifdef BSP_X_PHASE
+static __device__ unsigned long long g_phase[32];
+static __device__ long long g_phase_last[1 << 22];
+static __device__ long long g_phase_t0[1 << 22];   // tile start
+static __device__ int g_phase_cls[1 << 22];        // tile's segment-count class
+__device__ __forceinline__ void phase_mark(int i) {
+    if (threadIdx.x == 0) {
+        long long& last = g_phase_last[blockIdx.x & ((1 << 22) - 1)];
+        if (last != 0) {
+            const long long t = clock64();
+            atomicAdd(&g_phase[i], static_cast<unsigned long long>(t - last));
+            last = t;
+        }
+    }
+}
+#define PH(i) phase_mark(i)
+#else
+#define PH(i)
+#endif
+
 // Padded shared-memory index: one pad word per 32 keeps the per-thread
 // contiguous chunks of the merge (thread t owns [t*E, t*E+E)) on distinct
 // banks (ncu: 42% of shared wavefronts were bank conflicts without it).
@@ -233,6 +256,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         const int nr = agg >> 16, ct = agg & 0xffff;
         if (tid == 0) x.poff[nr] = ct;
         __syncthreads();
+        PH(1);
         // Gather: warp w takes a contiguous slice of the chunk's products, its
         // lanes consecutive ones (coalesced), and copies each product's B
         // column and value straight into the tile with cp.async — no register
@@ -259,6 +283,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
             cp_async_wait_all();
         }
         __syncthreads();
+        PH(2);
         // fix-up: product a_ik * b_kj; window-relative key and position
         // (deferred: sort_tile applies them only on the paths that read them)
         for (int e = tid; e < ct; e += T) {
@@ -272,12 +297,87 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         total += ct;
         nruns += nr;
         __syncthreads();
+        PH(3);
     }
     if (tid == 0) {
         if (nruns <= MergeShared<T, CAPM>::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
         s.nruns = nruns;
     }
     __syncthreads();
+    PH(4);
+    return total;
+}
+
+// Keys-only expansion for the look-back window tile (esc_window_lb2_kernel):
+// the tile's output count depends only on the columns, so only they are
+// gathered before the sort; product g's B offset goes to src[g] and its A entry
+// (segment index within the row) to seg[g], both in the (still idle) value
+// buffer, and the values are fetched after the tile has published its count
+// (reduce_lb2).  The column copies (cp.async) are waited for once, after the
+// last chunk.  Requires nnz(B) < 2^32.
+template <int T, int CAPM>
+__device__ __forceinline__ int expand_keys(const Mats& m, int32_t c0, int32_t c1,
+                                           MergeShared<T, CAPM>& s, int64_t wsofs, int wwi,
+                                           int64_t wrs, int64_t wd) {
+    const int tid = threadIdx.x;
+    const int64_t rs = wrs, re = wrs + wd;
+    uint32_t* src = reinterpret_cast<uint32_t*>(s.val);
+    uint32_t* seg = src + CAPM;
+    int total = 0, nruns = 0;
+    auto& x = s.ex();
+    uint32_t* pseg = reinterpret_cast<uint32_t*>(x.pav);  // segment index of each compacted run
+    for (int64_t pc = rs; pc < re; pc += T) {
+        const int64_t p = pc + tid;
+        int len = 0;
+        int64_t start = 0;
+        if (p < re) {
+            int64_t b0, b1;
+            segment_range(m, false, wsofs, wwi, p, rs, re - rs, c0, c1, b0, b1);
+            start = b0;
+            len = static_cast<int>(b1 - b0);
+        }
+        const int packed = len | ((len > 0) << 16);
+        int off, agg;
+        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        const int r = off >> 16;
+        if (len > 0) {
+            if (nruns + r < MergeShared<T, CAPM>::MAXRUNS)
+                s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
+            x.pstart[r] = start;
+            x.poff[r] = off & 0xffff;
+            pseg[r] = static_cast<uint32_t>(p - rs);
+        }
+        const int nr = agg >> 16, ct = agg & 0xffff;
+        if (tid == 0) x.poff[nr] = ct;
+        __syncthreads();
+        PH(1);
+        {
+            int e0, we, qa;
+            warp_slice(x.poff, nr, ct, T / 32, e0, we, qa);
+            for (; e0 < we; e0 += 32) {
+                const int q = warp_runs(x.poff, nr, e0, qa);
+                const int e = e0 + (threadIdx.x & 31);
+                if (e < we) {
+                    const int64_t sa = x.pstart[q] + (e - x.poff[q]);
+                    const int g = total + e;
+                    cp_async4(&s.key(0)[PADI(g)], m.bcol + sa);
+                    src[g] = static_cast<uint32_t>(sa);
+                    seg[g] = pseg[q];
+                }
+            }
+        }
+        total += ct;
+        nruns += nr;
+        __syncthreads();  // the next chunk rewrites the compacted runs
+        PH(2);
+    }
+    cp_async_wait_all();
+    if (tid == 0) {
+        if (nruns <= MergeShared<T, CAPM>::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
+        s.nruns = nruns;
+    }
+    __syncthreads();
+    PH(4);
     return total;
 }
 
@@ -519,6 +619,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
         atomicMax(&s_max, mx);
     }
     __syncthreads();
+    PH(5);
     const uint32_t cmin = s_min;
     const int cb = LNB - lk;  // column bucket bits per member slot
     const int cw = bit_length(s_max - cmin);
@@ -542,6 +643,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
     for (int o = 16; o > 0; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
     if ((tid & 31) == 0) atomicAdd(&s_cost, cost);
     __syncthreads();
+    PH(6);
     if (s_over || s_cost > max_cost * total) return false;
     uint32_t loc[PER];
     int run = 0;
@@ -560,6 +662,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
     }
     if (tid == 0) cnt[NB] = static_cast<uint16_t>(total);
     __syncthreads();
+    PH(7);
     const uint32_t lm = (1u << sh) - 1u;
     // Narrow row tiles: the whole (column - min, index) fits one 32-bit word,
     // globally ordered and unique, so a slot's rank is the count of smaller
@@ -583,6 +686,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
         }
         if (tid < 4) pk[total + tid] = 0xffffffffu;
         __syncthreads();
+        PH(8);
         const uint32_t im = (1u << IB) - 1u;
         const uint32_t rm = (1u << cw) - 1u;  // cw <= 32 - IB
         for (int q = tid; q < total; q += T) {
@@ -624,6 +728,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
             s.idx0[PADI(c)] = static_cast<uint16_t>(v & im);
         }
         __syncthreads();
+        PH(9);
         return true;
     }
 #pragma unroll
@@ -652,6 +757,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
         s.idx0[PADI(c)] = static_cast<uint16_t>(v & 0xffffu);
     }
     __syncthreads();
+    PH(10);
     return true;
 }
 
@@ -698,9 +804,12 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     prep();
     if (radix) {
         radix_sort_tile<T, CAPM>(s, total, bits);
+        PH(11);
         return 0;
     }
-    return merge_runs<T, CAPM>(s, total);
+    const int mb = merge_runs<T, CAPM>(s, total);
+    PH(12);
+    return mb;
 }
 
 // Single-pass output placement (decoupled look-back, the CUB single-pass scan
@@ -826,6 +935,14 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
     if constexpr (LB) {
         if (threadIdx.x == 0) publish(tile_cnt);
         __syncthreads();
+        PH(13);
+#ifdef BSP_X_PHASE
+        if (threadIdx.x == 0 && g_phase_last[blockIdx.x & ((1 << 22) - 1)] != 0) {
+            const int b = blockIdx.x & ((1 << 22) - 1);
+            atomicAdd(&g_phase[20 + g_phase_cls[b]], static_cast<unsigned long long>(clock64() - g_phase_t0[b]));
+            atomicAdd(&g_phase[26 + g_phase_cls[b]], 1ull);
+        }
+#endif
         // rank -> head position, in the buffer the sort left idle
         uint16_t* hpos = b ? s.idx0 : reinterpret_cast<uint16_t*>(s.u.c.packed);
         const unsigned below = (1u << lane) - 1u;
@@ -846,6 +963,7 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
             hpos[rank] = static_cast<uint16_t>(o);
         }
         __syncthreads();
+        PH(14);
         long long off = 0;
         if constexpr (!std::is_same_v<std::decay_t<Place>, int>) {
             // placement now: warp 0 walks, the tile stores at the offset
@@ -855,6 +973,7 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
                 if (lane == 0) s_off = v;
             }
             __syncthreads();
+            PH(15);
             off = s_off;
         }
         ccol += off;
@@ -865,6 +984,7 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
             cval[q] = s.val[X[PADI(o)]];
         }
         __syncthreads();
+        PH(16);
         return tile_cnt;
     }
     __syncthreads();
@@ -885,6 +1005,110 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
         cval[rank] = acc;
     }
     __syncthreads();
+    return tile_cnt;
+}
+
+// Reduction and single-pass placement of the look-back tile whose values were
+// not gathered yet (expand_keys).  The sorted tile is in buffer 0.  The count is
+// published right after the head scan; then the values are fetched — product g
+// takes b from bval[src[g]] (cp.async into the sort's idle buffer) and a from
+// the A row — the heads sum their runs left to right from 0.0 in ascending k
+// (spgemm.hpp:92-97), warp 0 takes the offset from the look-back and the tile
+// stores its output coalesced.  Everything after `publish` overlaps the
+// predecessors' sorts.
+template <int T, int CAPM, class Publish, class Place>
+__device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM>& s, int total, uint32_t kofs,
+                                          int32_t* __restrict__ ccol, double* __restrict__ cval,
+                                          const double* __restrict__ arow,
+                                          const double* __restrict__ bval, Publish&& publish,
+                                          Place&& place) {
+    constexpr int NW = T / 32;
+    constexpr int R = (CAPM + T - 1) / T;
+    static_assert(sizeof(typename MergeShared<T, CAPM>::U) >= sizeof(double) * CAPM, "value buffer");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t* K = s.key0;
+    const uint16_t* X = s.idx0;
+    int* cnt = reinterpret_cast<int*>(s.hist);
+    const int nrows = (total + T - 1) / T;
+    unsigned hm[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int o = r * T + threadIdx.x;
+        const bool h = o < total && (o == 0 || K[PADI(o)] != K[PADI(o - 1)]);
+        hm[r] = __ballot_sync(0xffffffffu, h);
+        if (lane == 0 && r < nrows) cnt[r * NW + warp] = __popc(hm[r]);
+    }
+    __syncthreads();
+    const int v = threadIdx.x < nrows * NW ? cnt[threadIdx.x] : 0;
+    int pre, tile_cnt;
+    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(v, pre, tile_cnt);
+    __syncthreads();
+    if (threadIdx.x < nrows * NW) cnt[threadIdx.x] = pre;
+    if (threadIdx.x == 0) publish(tile_cnt);
+    PH(13);
+    // values into the sort's idle buffer, in expansion order (a run's entries
+    // are consecutive in B: neighbouring lanes share sectors, as in the
+    // combined gather; fetching them in sorted order instead — contiguous
+    // runs for the sums — read 4x the sectors: 182 vs 170 ms on cfg5)
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(s.val);
+    const uint32_t* seg = src + CAPM;
+    double* pv = reinterpret_cast<double*>(&s.u);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int g = r * T + threadIdx.x;
+        if (g < total) cp_async8(&pv[g], bval + src[g]);
+    }
+    double av[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int g = r * T + threadIdx.x;
+        av[r] = g < total ? __ldg(arow + seg[g]) : 0.0;
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int g = r * T + threadIdx.x;
+        if (g < total) pv[g] = __dmul_rn(av[r], pv[g]);  // this thread's own copies
+    }
+    __syncthreads();
+    PH(3);
+    // run sums (each head overwrites its own first slot); rank -> head position
+    uint16_t* hpos = reinterpret_cast<uint16_t*>(s.val);  // src/seg are consumed
+    const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (!((hm[r] >> lane) & 1u)) continue;
+        const int o = r * T + threadIdx.x;
+        const int rank = cnt[r * NW + warp] + __popc(hm[r] & below);
+        const uint32_t key = K[PADI(o)];
+        double acc = 0.0;
+        int e = o;
+        const int x0 = X[PADI(o)];
+        do {
+            acc = __dadd_rn(acc, pv[X[PADI(e)]]);
+            ++e;
+        } while (e < total && K[PADI(e)] == key);
+        pv[x0] = acc;  // only this head reads its run's slots
+        hpos[rank] = static_cast<uint16_t>(o);
+    }
+    __syncthreads();
+    PH(14);
+    __shared__ long long s_off2;
+    if (warp == 0) {
+        const long long vv = place(tile_cnt);
+        if (lane == 0) s_off2 = vv;
+    }
+    __syncthreads();
+    PH(15);
+    ccol += s_off2;
+    cval += s_off2;
+    for (int q = threadIdx.x; q < tile_cnt; q += T) {
+        const int o = hpos[q];
+        ccol[q] = static_cast<int32_t>(K[PADI(o)] + kofs);
+        cval[q] = pv[X[PADI(o)]];
+    }
+    __syncthreads();
+    PH(16);
     return tile_cnt;
 }
 

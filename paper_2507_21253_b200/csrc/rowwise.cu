@@ -36,6 +36,7 @@
 
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_partition.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -697,8 +698,19 @@ __global__ void __launch_bounds__(T, CAPM <= 2048 ? 4 : 2) esc_window_lb_kernel(
     if (threadIdx.x == 0) s_tile = atomicAdd(lb.counter, 1);
     __syncthreads();
     const int t = s_tile;
+#ifdef BSP_X_PHASE
     const int32_t w = ids[t];
     const Window wd = wins[w];
+    if (threadIdx.x == 0) {
+        const int b = blockIdx.x & ((1 << 22) - 1);
+        g_phase_last[b] = g_phase_t0[b] = clock64();
+        g_phase_cls[b] = wd.d <= 256 ? 0 : (wd.d <= 512 ? 1 : (wd.d <= 1024 ? 2 : (wd.d <= 2048 ? 3 : (wd.d <= 4096 ? 4 : 5))));
+        atomicAdd(&g_phase[0], 1ull);
+    }
+#else
+    const int32_t w = ids[t];
+    const Window wd = wins[w];
+#endif
     const int total = expand_runs<T, CAPM, true>(m, wd.row, wd.c0, wd.c1, false, s, wd.sofs, wd.wi,
                                                  wd.rs, wd.d, /*defer=*/true);
     const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(wd.c1 - wd.c0), csort, 0, false,
@@ -713,6 +725,63 @@ __global__ void __launch_bounds__(T, CAPM <= 2048 ? 4 : 2) esc_window_lb_kernel(
         out.win_nnz[w] = cnt;
         atomicAdd(reinterpret_cast<unsigned long long*>(&out.row_nnz[r]),
                   static_cast<unsigned long long>(cnt));
+#ifdef BSP_X_PHASE
+        g_phase_last[blockIdx.x & ((1 << 22) - 1)] = 0;
+#endif
+    }
+}
+
+// Look-back window tile, second form: only the columns are gathered before the
+// sort; the values are fetched — in sorted order — after the tile has published
+// its count (expand_keys / reduce_lb2).  A tile's count does not depend on the
+// values, so the value gather, the a*b products and the run sums all overlap
+// the wait for the predecessors' counts (measured on cfg5 with the first form:
+// 20 % of every tile's residency was that wait, and 21 % the combined gather).
+// Bit-identical output: each run's products are summed in ascending k as before.
+template <int T, int CAPM>
+__global__ void __launch_bounds__(T, CAPM <= 2048 ? 4 : 2) esc_window_lb2_kernel(
+    Mats m, const int32_t* __restrict__ ids, const Window* __restrict__ wins, OutCtx out,
+    int csort, LbCtx lb) {
+    using S = MergeShared<T, CAPM>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S& s = *reinterpret_cast<S*>(smem_raw);
+    __shared__ int s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(lb.counter, 1);
+    __syncthreads();
+    const int t = s_tile;
+    const int32_t w = ids[t];
+    const Window wd = wins[w];
+#ifdef BSP_X_PHASE
+    if (threadIdx.x == 0) {
+        const int b = blockIdx.x & ((1 << 22) - 1);
+        g_phase_last[b] = g_phase_t0[b] = clock64();
+        g_phase_cls[b] = wd.d <= 256 ? 0 : (wd.d <= 512 ? 1 : (wd.d <= 1024 ? 2 : (wd.d <= 2048 ? 3 : (wd.d <= 4096 ? 4 : 5))));
+        atomicAdd(&g_phase[0], 1ull);
+    }
+#endif
+    const int total = expand_keys<T, CAPM>(m, wd.c0, wd.c1, s, wd.sofs, wd.wi, wd.rs, wd.d);
+    const int b = sort_tile<T, CAPM>(s, total, static_cast<uint32_t>(wd.c1 - wd.c0), csort, 0, false,
+                                     wd.c0);
+    if (b == 1) {  // merged runs end in buffer 1 (rare): the reduction reads buffer 0
+        for (int e = threadIdx.x; e < total; e += T) {
+            s.key0[PADI(e)] = s.u.m.key1[PADI(e)];
+            s.idx0[PADI(e)] = s.u.m.idx1[PADI(e)];
+        }
+        __syncthreads();
+    }
+    const int64_t r = wd.row - out.row_begin;
+    const int64_t known = out.crp[r] + out.win_scan[w] - out.win_scan[wd.first];
+    const int cnt = reduce_lb2<T, CAPM>(
+        s, total, static_cast<uint32_t>(wd.c0), out.ccol + known, out.cval + known,
+        m.aval + wd.rs, m.bval, [&](int agg) { lookback_publish(lb.status, t, agg); },
+        [&](int agg) { return lookback_warp(lb.status, t, agg); });
+    if (threadIdx.x == 0) {
+        out.win_nnz[w] = cnt;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&out.row_nnz[r]),
+                  static_cast<unsigned long long>(cnt));
+#ifdef BSP_X_PHASE
+        g_phase_last[blockIdx.x & ((1 << 22) - 1)] = 0;
+#endif
     }
 }
 
@@ -1963,6 +2032,25 @@ void narrow64_rows(bsp_handle h, const Mats& m, const unsigned long long* mask, 
                       mask, int64_t{0}, n, nullptr, crp, ccol, cval, nullptr, skip, nx.p);
 }
 
+// Look-back list split (rowwise_multiply): windows whose A row has at most dmax
+// segments stay on the look-back tile.
+struct WindowShortRow {
+    const Window* wins;
+    int dmax;
+    __device__ bool operator()(int32_t w) const { return wins[w].d <= dmax; }
+};
+__global__ void sum_window_products_kernel(const int32_t* __restrict__ ids, int64_t n,
+                                           const Window* __restrict__ wins,
+                                           unsigned long long* __restrict__ out) {
+    unsigned long long v = 0;
+    for (int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; i < n;
+         i += int64_t{gridDim.x} * blockDim.x)
+        v += static_cast<unsigned long long>(wins[ids[i]].nprod);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
 void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t rb, int64_t re,
                       bsp_csr* C, const uint8_t* row_skip, int64_t* row_nnz_out) {
     check_csr(A, "spgemm_rowwise");
@@ -1995,10 +2083,64 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
         const char* e = std::getenv("BSP_LOOKBACK");
         return !(e && e[0] == '0');
     }();
-    const int64_t nlb = plan.wcls_off[LBC + 1] - plan.wcls_off[LBC];
+    int64_t nlb = plan.wcls_off[LBC + 1] - plan.wcls_off[LBC];
     bool lb = lb_on && nlb > 0;
+    // Windows of rows with many segments leave the look-back list (BSP_LB_DMAX,
+    // 0 = keep all): a tile's time to publish its count grows with the A row's
+    // length d (measured on cfg5, cycles from tile start to publish: 29K at
+    // d <= 256, 46K at d <= 1024, 97K at d <= 4096, 167K above), and every tile
+    // behind a slow one waits for it (the wait was 20 % of all tile residency).
+    // The few long-row windows can take the two-pass path (symbolic + numeric
+    // with known offsets) so that the look-back stream keeps tiles of similar
+    // duration — measured on cfg5: no gain (the look-back kernel gets shorter
+    // only by the work that leaves it: 170.5 / 165.6 / 154.5 / 135.7 / 108.2 ms
+    // at dmax off / 2048 / 1024 / 512 / 256, step 287.4 / 288.1 / 288.5 / 291.6 /
+    // 295.9 ms), so the wait is not caused by these tiles alone; off by default.
+    static const int lb_dmax = [] {
+        const char* e = std::getenv("BSP_LB_DMAX");
+        return e ? std::atoi(e) : 0;  // measured: no gain (see below), off by default
+    }();
+    int32_t* const lb_list = plan.sparse_ids.p + plan.wcls_off[LBC];
+    int64_t ntp = 0;           // two-pass windows: lb_list[nlb, nlb + ntp)
+    int64_t lb_products = plan.wcls_prod[LBC];
+    if (lb) {
+        sort_ids(h, lb_list, nlb);  // C's layout order (window ids follow the row-sorted heavy list)
+        if (lb_dmax > 0) {
+            DBuf<int32_t> part(h, nlb);
+            DBuf<int64_t> nsel(h, 1);
+            size_t bytes = 0;
+            const WindowShortRow pred{plan.wins.p, lb_dmax};
+            BSP_CUDA(cub::DevicePartition::If(nullptr, bytes, lb_list, part.p, nsel.p, nlb, pred,
+                                              h->stream));
+            DBuf<uint8_t> tmp(h, static_cast<int64_t>(bytes));
+            BSP_CUDA(cub::DevicePartition::If(tmp.p, bytes, lb_list, part.p, nsel.p, nlb, pred,
+                                              h->stream));
+            ++h->launches;
+            BSP_CUDA(cudaMemcpyAsync(lb_list, part.p, nlb * sizeof(int32_t),
+                                     cudaMemcpyDeviceToDevice, h->stream));
+            const int64_t keep = read_scalar(h, nsel.p);
+            ntp = nlb - keep;
+            nlb = keep;
+            if (ntp > 0) {
+                DBuf<unsigned long long> tp_prod(h, 1);
+                BSP_CUDA(cudaMemsetAsync(tp_prod.p, 0, sizeof(unsigned long long), h->stream));
+                BSP_LAUNCH(h, sum_window_products_kernel,
+                           static_cast<unsigned>(std::min<int64_t>(div_up(ntp, 256), 1024)), 256, 0,
+                           lb_list + nlb, ntp, plan.wins.p, tp_prod.p);
+                lb_products -= static_cast<int64_t>(read_scalar(h, tp_prod.p));
+            }
+            if (nlb == 0) lb = false;  // (all of them two-pass: counted below)
+        }
+    }
     DBuf<int64_t> win_nnz;
-    plan_symbolic(h, m, plan, crp.p, win_nnz, lb ? LBC : -1);
+    plan_symbolic(h, m, plan, crp.p, win_nnz, (lb || ntp > 0) ? LBC : -1);
+    if (ntp > 0) {  // the long-row windows' symbolic count
+        OutCtx so{};
+        so.row_begin = plan.rb;
+        so.row_nnz = crp.p;
+        so.win_nnz = win_nnz.p;
+        launch_tile<256, 2048, false>(h, plan.with_starts(m), lb_list + nlb, ntp, plan.wins.p, so);
+    }
     BSP_CUDA(cudaMemsetAsync(crp.p + n, 0, sizeof(int64_t), h->stream));
     DBuf<int64_t> rp(h, n + 1, Pool::out);
     exclusive_scan_i64(h, crp.p, rp.p, n + 1);
@@ -2010,7 +2152,7 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     // allocation still fails cleanly (BSP_ERR_OOM) if memory was taken meanwhile
     int64_t avail = plan.avail_hint;
     if (lb) {
-        cap = nnz + plan.wcls_prod[LBC];
+        cap = nnz + lb_products;
         // C (12 B per entry) + the look-back state, with a 1 GB margin (a figure
         // that says no is checked against the driver before it is believed)
         if (12 * cap + 16 * nlb + (int64_t{1} << 30) > avail)
@@ -2023,8 +2165,8 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
             so.row_nnz = crp.p;
             so.win_nnz = win_nnz.p;
             Mats ms = plan.with_starts(m);
-            launch_tile<256, 2048, false>(h, ms, plan.sparse_ids.p + plan.wcls_off[LBC], nlb,
-                                          plan.wins.p, so);
+            launch_tile<256, 2048, false>(h, ms, lb_list, nlb, plan.wins.p, so);
+            ntp += nlb;  // all of the class on the two-pass path now
             exclusive_scan_i64(h, crp.p, rp.p, n + 1);
             exclusive_scan_i64(h, win_nnz.p, win_scan.p, plan.nwin + 1);
             nnz = cap = read_scalar(h, rp.p + n);
@@ -2042,8 +2184,7 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     if (lb) {
         // windows of the class in C's layout order (window ids follow the
         // row-sorted heavy list), claimed in that order
-        int32_t* ids = plan.sparse_ids.p + plan.wcls_off[LBC];
-        sort_ids(h, ids, nlb);
+        int32_t* ids = lb_list;  // sorted (and split) above
         DBuf<unsigned long long> status(h, nlb);
         DBuf<int> counter(h, 1);
         BSP_CUDA(cudaMemsetAsync(status.p, 0, nlb * sizeof(unsigned long long), h->stream));
@@ -2061,10 +2202,30 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
             return e ? std::atoi(e) : 1000;
         }();
         using S = MergeShared<256, 2048>;
-        auto k = esc_window_lb_kernel<256, 2048>;
-        set_smem(k, sizeof(S));
-        BSP_LAUNCH_AS(h, "esc_window_lb<256,2048>", k, static_cast<unsigned>(nlb), 256, sizeof(S),
-                      plan.with_starts(m), ids, plan.wins.p, out, csort, LbCtx{counter.p, status.p});
+        // BSP_LB_V2=1: the second form (only the columns gathered before the sort,
+        // the values after the count is published).  Measured on cfg5: the wait for
+        // the predecessors' counts falls from 10.7K to 6.2K cycles per tile and the
+        // tile's residency from 54.1K to 49.7K cycles, but the kernel takes the same
+        // time (171.1 vs 170.4 ms): with more warps runnable at once the L1/shared
+        // memory pipe (61 % busy) and the issue slots (59 %) are what is left, so
+        // the first form stays the default.
+        static const bool lb_v2 = [] {
+            const char* e = std::getenv("BSP_LB_V2");
+            return e && e[0] == '1';
+        }();
+        if (lb_v2 && m.bnnz < (int64_t{1} << 32)) {
+            auto k = esc_window_lb2_kernel<256, 2048>;
+            set_smem(k, sizeof(S));
+            BSP_LAUNCH_AS(h, "esc_window_lb2<256,2048>", k, static_cast<unsigned>(nlb), 256,
+                          sizeof(S), plan.with_starts(m), ids, plan.wins.p, out, csort,
+                          LbCtx{counter.p, status.p});
+        } else {
+            auto k = esc_window_lb_kernel<256, 2048>;
+            set_smem(k, sizeof(S));
+            BSP_LAUNCH_AS(h, "esc_window_lb<256,2048>", k, static_cast<unsigned>(nlb), 256,
+                          sizeof(S), plan.with_starts(m), ids, plan.wins.p, out, csort,
+                          LbCtx{counter.p, status.p});
+        }
         // final row_ptr and window offsets for the remaining numeric tiles
         BSP_CUDA(cudaMemsetAsync(crp.p + n, 0, sizeof(int64_t), h->stream));
         exclusive_scan_i64(h, crp.p, rp.p, n + 1);
@@ -2075,7 +2236,18 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
         BSP_CUDA(cudaMemcpyAsync(row_nnz_out, crp.p, n * sizeof(int64_t),
                                  cudaMemcpyDeviceToDevice, h->stream));
     h->stats.nnz_out = nnz;
-    plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values(), lb ? LBC : -1);
+    plan_numeric(h, m, plan, rp.p, win_scan.p, pay.col_idx(), pay.values(),
+                 (lb || ntp > 0) ? LBC : -1);
+    if (ntp > 0) {  // the class's two-pass windows (the tail of its list)
+        OutCtx o2{};
+        o2.row_begin = plan.rb;
+        o2.crp = rp.p;
+        o2.win_scan = win_scan.p;
+        o2.ccol = pay.col_idx();
+        o2.cval = pay.values();
+        const int64_t t0 = lb ? nlb : 0;
+        launch_tile<256, 2048, true>(h, plan.with_starts(m), lb_list + t0, ntp, plan.wins.p, o2);
+    }
     C->nrows = n;
     C->ncols = B->ncols;
     C->nnz = nnz;
@@ -2293,5 +2465,18 @@ int bsp_partition_rows(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int32_t
         bounds_out[nparts] = n;
     });
 }
+
+#ifdef BSP_X_PHASE
+// experiments only (tools/phase_times.py): the look-back tile's phase cycle counters
+int bsp_debug_phases(unsigned long long* out32, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out32, bsp::g_phase, sizeof(unsigned long long) * 32);
+    if (reset) {
+        unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(bsp::g_phase, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 }  // extern "C"

@@ -323,3 +323,36 @@ def test_device_transpose_matches_host(engine, cfg, scale):
     want = B.transpose(a)
     got = engine.transpose(engine.upload(a)).download()
     assert_csr_identical(got, want, f"transpose cfg{cfg}")
+
+
+_LB_KNOB_SCRIPT = r"""
+import numpy as np
+import oracle as O
+import paper_2507_21253_b200 as B
+e = B.default_engine()
+for cfg, scale in ((5, 15), (3, 15), (5, 16)):
+    a = B.make_config(cfg, scale)
+    A = e.upload(a)
+    c = e.spgemm_rowwise(A, A).download()
+    assert e.exec_stats()["units"][8] > 0, "no sparse windows"
+    o = O.spgemm_rowwise(a, a)
+    assert np.array_equal(c.row_ptr, o.row_ptr) and np.array_equal(c.col_idx, o.col_idx), cfg
+    assert np.array_equal(c.values.view(np.uint64), o.values.view(np.uint64)), cfg
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"BSP_LB_V2": "1"}, {"BSP_LB_DMAX": "64"},
+                                 {"BSP_LB_V2": "1", "BSP_LB_DMAX": "128"},
+                                 {"BSP_LOOKBACK": "0"}, {"BSP_BLOCK_CACHE": "0"}])
+def test_lookback_knobs_bit_identical(env):
+    """The look-back tile's second form (values gathered after the count is published), the
+    split of long-row windows onto the two-pass path, the two-pass path alone and the block
+    cache switch are read once per process: each runs in its own process against the oracle."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **env)
+    e["PYTHONPATH"] = root + os.pathsep + os.path.join(root, "tests") + os.pathsep + e.get("PYTHONPATH", "")
+    r = subprocess.run([sys.executable, "-c", _LB_KNOB_SCRIPT], env=e, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
