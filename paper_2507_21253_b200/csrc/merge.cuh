@@ -51,13 +51,16 @@ __device__ __forceinline__ void phase_mark(int i) {
 // banks (ncu: 42% of shared wavefronts were bank conflicts without it).
 __device__ __forceinline__ int PADI(int i) { return i + (i >> 5); }
 
-template <int T, int CAPM>
+// VALB: bytes of the value buffer (the look-back tile's second form keeps only a
+// B offset and a segment index per product there: 6 bytes instead of 8);
+// RBO: radix digit bits override (smaller digits = smaller sort storage).
+template <int T, int CAPM, int VALB = 8 * CAPM, int RBO = 0>
 struct MergeShared {
     static constexpr int NP = CAPM + CAPM / 32 + 1;
     // radix digit bits: CUB's rank storage is T x 2^RB / 2 words whatever the
     // tile size, so 256-thread tiles of <= 3072 products (sized for 3-4
     // CTAs/SM) use 5-bit digits (16 KB), the others 6-bit digits
-    static constexpr int RB = (T >= 128 && CAPM <= 3072) ? 5 : 6;
+    static constexpr int RB = RBO ? RBO : ((T >= 128 && CAPM <= 3072) ? 5 : 6);
     using RSort = cub::BlockRadixSort<uint32_t, T, CAPM / T, uint16_t, RB>;
     // run offsets: tiles with more runs than this use the radix sort
     static constexpr int MAXRUNS = CAPM < 1024 ? CAPM : 1024;
@@ -78,7 +81,7 @@ struct MergeShared {
     uint32_t key0[NP];
     uint16_t idx0[NP];
     uint16_t ro0[MAXRUNS + 2];
-    alignas(16) double val[CAPM];  // 16-byte aligned: a bulk-copy destination (cluster.cu)
+    alignas(16) double val[VALB / 8];  // 16-byte aligned: a bulk-copy destination (cluster.cu)
     // buffer 1 of the merge, aliased with the radix sort's temp storage, the
     // counting sort's arrays and the expansion state
     union U {
@@ -217,9 +220,9 @@ __device__ __forceinline__ int warp_runs(const int32_t* poff, int nr, int e0, in
     return my;
 }
 
-template <int T, int CAPM, bool VALUES>
+template <int T, int CAPM, bool VALUES, int VB, int RBO>
 __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c0, int32_t c1,
-                                           bool full, MergeShared<T, CAPM>& s,
+                                           bool full, MergeShared<T, CAPM, VB, RBO>& s,
                                            int64_t wsofs = -1, int wwi = 0, int64_t wrs = -1,
                                            int64_t wd = 0, bool defer = false) {
     const int tid = threadIdx.x;
@@ -247,7 +250,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         // compact the non-empty segments of this chunk (run order = k order)
         const int r = off >> 16;
         if (len > 0) {
-            if (nruns + r < MergeShared<T, CAPM>::MAXRUNS)
+            if (nruns + r < MergeShared<T, CAPM, VB, RBO>::MAXRUNS)
                 s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
             x.pstart[r] = start;
             x.poff[r] = off & 0xffff;
@@ -300,7 +303,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         PH(3);
     }
     if (tid == 0) {
-        if (nruns <= MergeShared<T, CAPM>::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
+        if (nruns <= MergeShared<T, CAPM, VB, RBO>::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
         s.nruns = nruns;
     }
     __syncthreads();
@@ -315,14 +318,18 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
 // buffer, and the values are fetched after the tile has published its count
 // (reduce_lb2).  The column copies (cp.async) are waited for once, after the
 // last chunk.  Requires nnz(B) < 2^32.
-template <int T, int CAPM>
+template <int T, int CAPM, int VB, int RBO>
 __device__ __forceinline__ int expand_keys(const Mats& m, int32_t c0, int32_t c1,
-                                           MergeShared<T, CAPM>& s, int64_t wsofs, int wwi,
+                                           MergeShared<T, CAPM, VB, RBO>& s, int64_t wsofs, int wwi,
                                            int64_t wrs, int64_t wd) {
     const int tid = threadIdx.x;
     const int64_t rs = wrs, re = wrs + wd;
+    // compact value buffer (VB < 8 bytes per product): 16-bit segment indices
+    // (rows of at most 65535 entries; the caller routes longer rows elsewhere)
+    constexpr bool SEG16 = VB < 8 * CAPM;
     uint32_t* src = reinterpret_cast<uint32_t*>(s.val);
     uint32_t* seg = src + CAPM;
+    uint16_t* seg16 = reinterpret_cast<uint16_t*>(src + CAPM);
     int total = 0, nruns = 0;
     auto& x = s.ex();
     uint32_t* pseg = reinterpret_cast<uint32_t*>(x.pav);  // segment index of each compacted run
@@ -341,7 +348,7 @@ __device__ __forceinline__ int expand_keys(const Mats& m, int32_t c0, int32_t c1
         cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
         const int r = off >> 16;
         if (len > 0) {
-            if (nruns + r < MergeShared<T, CAPM>::MAXRUNS)
+            if (nruns + r < MergeShared<T, CAPM, VB, RBO>::MAXRUNS)
                 s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
             x.pstart[r] = start;
             x.poff[r] = off & 0xffff;
@@ -362,7 +369,8 @@ __device__ __forceinline__ int expand_keys(const Mats& m, int32_t c0, int32_t c1
                     const int g = total + e;
                     cp_async4(&s.key(0)[PADI(g)], m.bcol + sa);
                     src[g] = static_cast<uint32_t>(sa);
-                    seg[g] = pseg[q];
+                    if constexpr (SEG16) seg16[g] = static_cast<uint16_t>(pseg[q]);
+                    else seg[g] = pseg[q];
                 }
             }
         }
@@ -373,7 +381,7 @@ __device__ __forceinline__ int expand_keys(const Mats& m, int32_t c0, int32_t c1
     }
     cp_async_wait_all();
     if (tid == 0) {
-        if (nruns <= MergeShared<T, CAPM>::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
+        if (nruns <= MergeShared<T, CAPM, VB, RBO>::MAXRUNS) s.ro(0)[nruns] = static_cast<uint16_t>(total);
         s.nruns = nruns;
     }
     __syncthreads();
@@ -383,8 +391,8 @@ __device__ __forceinline__ int expand_keys(const Mats& m, int32_t c0, int32_t c1
 
 // Bottom-up stable merge of the runs in key[0]/idx[0]; returns the buffer
 // holding the sorted result.
-template <int T, int CAPM>
-__device__ __forceinline__ int merge_runs(MergeShared<T, CAPM>& s, int total,
+template <int T, int CAPM, int VB, int RBO>
+__device__ __forceinline__ int merge_runs(MergeShared<T, CAPM, VB, RBO>& s, int total,
                                           int max_levels = 64) {
     const int tid = threadIdx.x;
     int R = s.nruns;
@@ -450,8 +458,8 @@ __device__ __forceinline__ int merge_runs(MergeShared<T, CAPM>& s, int total,
 // chosen instead of merge_runs when the merge tree would need more levels
 // than the radix sort needs passes (windows of heavy rows carry hundreds of
 // short runs).  Result left in buffer 0.
-template <int T, int CAPM>
-__device__ __forceinline__ void radix_sort_tile(MergeShared<T, CAPM>& s, int total, int bits) {
+template <int T, int CAPM, int VB, int RBO>
+__device__ __forceinline__ void radix_sort_tile(MergeShared<T, CAPM, VB, RBO>& s, int total, int bits) {
     constexpr int I = CAPM / T;
     const int tid = threadIdx.x;
     uint32_t k[I];
@@ -464,7 +472,7 @@ __device__ __forceinline__ void radix_sort_tile(MergeShared<T, CAPM>& s, int tot
         v[i] = e < total ? s.idx0[PADI(e)] : static_cast<uint16_t>(0);
     }
     __syncthreads();
-    typename MergeShared<T, CAPM>::RSort(s.u.sort).Sort(k, v, 0, bits);
+    typename MergeShared<T, CAPM, VB, RBO>::RSort(s.u.sort).Sort(k, v, 0, bits);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < I; ++i) {
@@ -483,8 +491,8 @@ __device__ __forceinline__ void radix_sort_tile(MergeShared<T, CAPM>& s, int tot
 // entries (skewed columns or many duplicates): the caller then merges/radixes.
 constexpr int MSD_MAXB = 24;
 
-template <int T, int CAPM>
-__device__ __forceinline__ bool msd_sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width) {
+template <int T, int CAPM, int VB, int RBO>
+__device__ __forceinline__ bool msd_sort_tile(MergeShared<T, CAPM, VB, RBO>& s, int total, uint32_t width) {
     constexpr int NB = CAPM / 2;
     constexpr int LNB = 31 - __builtin_clz(static_cast<unsigned>(NB));
     constexpr int PER = NB / T;
@@ -574,10 +582,10 @@ __device__ __forceinline__ bool msd_sort_tile(MergeShared<T, CAPM>& s, int total
 // Result in buffer 0.
 constexpr int CS_MAXB = 128;
 
-template <int T, int CAPM>
-__device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width,
+template <int T, int CAPM, int VB, int RBO>
+__device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM, VB, RBO>& s, int total, uint32_t width,
                                                 int cbits, int max_cost, int kofs = -1) {
-    using S = MergeShared<T, CAPM>;
+    using S = MergeShared<T, CAPM, VB, RBO>;
     constexpr int NB = S::NB, LNB = S::LNB, PER = NB / T, I = (CAPM + T - 1) / T;
     static_assert(PER % 2 == 0 || PER == 1, "bucket split");
     const int tid = threadIdx.x;
@@ -765,8 +773,8 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM>& s, int tot
 // (csort > 0: try the counting sort first when the merge tree is >= 3 levels
 // deep — or only in place of the radix sort (radix_only) — with csort as its
 // cost cap).
-template <int T, int CAPM>
-__device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uint32_t width,
+template <int T, int CAPM, int VB, int RBO>
+__device__ __forceinline__ int sort_tile(MergeShared<T, CAPM, VB, RBO>& s, int total, uint32_t width,
                                          int csort = 0, int cbits = 0,
                                          bool radix_only = false, int kofs = -1) {
     const int R = s.nruns;
@@ -794,10 +802,10 @@ __device__ __forceinline__ int sort_tile(MergeShared<T, CAPM>& s, int total, uin
     // pad key = 2^bits - 1 >= every key (<= width-1); pads sit after `total`
     // and the sort is stable, so real entries keep the first `total` slots.
     const int bits = bit_length(width > 1 ? width - 1 : 1);
-    constexpr int RB = MergeShared<T, CAPM>::RB;
+    constexpr int RB = MergeShared<T, CAPM, VB, RBO>::RB;
     const int passes = (bits + RB - 1) / RB;
     // measured: cfg4 (5 levels vs 4 passes) prefers merge
-    const bool radix = levels > passes + 1 || R > MergeShared<T, CAPM>::MAXRUNS;
+    const bool radix = levels > passes + 1 || R > MergeShared<T, CAPM, VB, RBO>::MAXRUNS;
     if (csort > 0 && levels >= 3 && (radix || !radix_only) &&
         count_sort_tile<T, CAPM>(s, total, width, cbits, csort, kofs))
         return 0;
@@ -905,14 +913,14 @@ __device__ __forceinline__ long long lookback_warp(unsigned long long* st, int t
 // for the predecessors' counts overlaps this work; then warp 0 obtains the
 // offset (`place(count)`, the look-back) and the tile stores its output
 // coalesced at ccol/cval + offset.
-template <int T, int CAPM, bool LB = false, class Publish = int, class Place = int>
-__device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, int total,
+template <int T, int CAPM, bool LB = false, class Publish = int, class Place = int, int VB = 0, int RBO = 0>
+__device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM, VB, RBO>& s, int b, int total,
                                                 uint32_t kofs, int32_t* __restrict__ ccol,
                                                 double* __restrict__ cval, Publish&& publish = 0,
                                                 Place&& place = 0) {
     constexpr int NW = T / 32;
     constexpr int R = (CAPM + T - 1) / T;
-    static_assert(R * NW <= T && R * NW <= MergeShared<T, CAPM>::NHIST, "row/warp counters");
+    static_assert(R * NW <= T && R * NW <= MergeShared<T, CAPM, VB, RBO>::NHIST, "row/warp counters");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t* K = s.key(b);
     const uint16_t* X = s.idx(b);
@@ -952,14 +960,20 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
             const int o = r * T + threadIdx.x;
             const int rank = cnt[r * NW + warp] + __popc(hm[r] & below);
             const uint32_t key = K[PADI(o)];
-            const int x0 = X[PADI(o)];
-            double acc = 0.0;
-            int e = o;
-            do {
-                acc = __dadd_rn(acc, s.val[X[PADI(e)]]);
-                ++e;
-            } while (e < total && K[PADI(e)] == key);
-            s.val[x0] = acc;  // only this head reads its run's slots
+            // A run of one product (nearly all of them at cf ~ 1) keeps its
+            // slot as it is: the final store forms 0.0 + p itself.  Longer
+            // runs leave their sum (never -0.0: it starts from +0.0) in the
+            // head's slot, for which 0.0 + sum changes nothing.
+            if (o + 1 < total && K[PADI(o + 1)] == key) {
+                const int x0 = X[PADI(o)];
+                double acc = 0.0;
+                int e = o;
+                do {
+                    acc = __dadd_rn(acc, s.val[X[PADI(e)]]);
+                    ++e;
+                } while (e < total && K[PADI(e)] == key);
+                s.val[x0] = acc;  // only this head reads its run's slots
+            }
             hpos[rank] = static_cast<uint16_t>(o);
         }
         __syncthreads();
@@ -981,7 +995,7 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
         for (int q = threadIdx.x; q < tile_cnt; q += T) {
             const int o = hpos[q];
             ccol[q] = static_cast<int32_t>(K[PADI(o)] + kofs);
-            cval[q] = s.val[X[PADI(o)]];
+            cval[q] = __dadd_rn(0.0, s.val[X[PADI(o)]]);
         }
         __syncthreads();
         PH(16);
@@ -1016,15 +1030,15 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM>& s, int b, 
 // (spgemm.hpp:92-97), warp 0 takes the offset from the look-back and the tile
 // stores its output coalesced.  Everything after `publish` overlaps the
 // predecessors' sorts.
-template <int T, int CAPM, class Publish, class Place>
-__device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM>& s, int total, uint32_t kofs,
+template <int T, int CAPM, int VB, int RBO, class Publish, class Place>
+__device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM, VB, RBO>& s, int total, uint32_t kofs,
                                           int32_t* __restrict__ ccol, double* __restrict__ cval,
                                           const double* __restrict__ arow,
                                           const double* __restrict__ bval, Publish&& publish,
                                           Place&& place) {
     constexpr int NW = T / 32;
     constexpr int R = (CAPM + T - 1) / T;
-    static_assert(sizeof(typename MergeShared<T, CAPM>::U) >= sizeof(double) * CAPM, "value buffer");
+    static_assert(sizeof(typename MergeShared<T, CAPM, VB, RBO>::U) >= sizeof(double) * CAPM, "value buffer");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t* K = s.key0;
     const uint16_t* X = s.idx0;
@@ -1050,8 +1064,10 @@ __device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM>& s, int total, ui
     // are consecutive in B: neighbouring lanes share sectors, as in the
     // combined gather; fetching them in sorted order instead — contiguous
     // runs for the sums — read 4x the sectors: 182 vs 170 ms on cfg5)
+    constexpr bool SEG16 = VB < 8 * CAPM;
     const uint32_t* src = reinterpret_cast<const uint32_t*>(s.val);
     const uint32_t* seg = src + CAPM;
+    const uint16_t* seg16 = reinterpret_cast<const uint16_t*>(src + CAPM);
     double* pv = reinterpret_cast<double*>(&s.u);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1062,7 +1078,7 @@ __device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM>& s, int total, ui
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int g = r * T + threadIdx.x;
-        av[r] = g < total ? __ldg(arow + seg[g]) : 0.0;
+        av[r] = g < total ? __ldg(arow + (SEG16 ? static_cast<uint32_t>(seg16[g]) : seg[g])) : 0.0;
     }
     cp_async_wait_all();
 #pragma unroll
@@ -1081,14 +1097,16 @@ __device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM>& s, int total, ui
         const int o = r * T + threadIdx.x;
         const int rank = cnt[r * NW + warp] + __popc(hm[r] & below);
         const uint32_t key = K[PADI(o)];
-        double acc = 0.0;
-        int e = o;
-        const int x0 = X[PADI(o)];
-        do {
-            acc = __dadd_rn(acc, pv[X[PADI(e)]]);
-            ++e;
-        } while (e < total && K[PADI(e)] == key);
-        pv[x0] = acc;  // only this head reads its run's slots
+        if (o + 1 < total && K[PADI(o + 1)] == key) {  // (single products: see reduce_and_write)
+            double acc = 0.0;
+            int e = o;
+            const int x0 = X[PADI(o)];
+            do {
+                acc = __dadd_rn(acc, pv[X[PADI(e)]]);
+                ++e;
+            } while (e < total && K[PADI(e)] == key);
+            pv[x0] = acc;  // only this head reads its run's slots
+        }
         hpos[rank] = static_cast<uint16_t>(o);
     }
     __syncthreads();
@@ -1105,7 +1123,7 @@ __device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM>& s, int total, ui
     for (int q = threadIdx.x; q < tile_cnt; q += T) {
         const int o = hpos[q];
         ccol[q] = static_cast<int32_t>(K[PADI(o)] + kofs);
-        cval[q] = pv[X[PADI(o)]];
+        cval[q] = __dadd_rn(0.0, pv[X[PADI(o)]]);
     }
     __syncthreads();
     PH(16);

@@ -738,11 +738,19 @@ __global__ void __launch_bounds__(T, CAPM <= 2048 ? 4 : 2) esc_window_lb_kernel(
 // the wait for the predecessors' counts (measured on cfg5 with the first form:
 // 20 % of every tile's residency was that wait, and 21 % the combined gather).
 // Bit-identical output: each run's products are summed in ascending k as before.
-template <int T, int CAPM>
-__global__ void __launch_bounds__(T, CAPM <= 2048 ? 4 : 2) esc_window_lb2_kernel(
+// COMPACT: 6 bytes per product in the value buffer (32-bit B offset, 16-bit
+// segment index: rows of at most 65535 entries) and 4-bit radix digits in the
+// fallback sort: 44.9 KB per tile, 5 CTAs per SM at 48 registers (the tile is
+// latency bound: 2 / 3 / 4 CTAs per SM measured 265.8 / 198.5 / 169.2 ms).
+template <int T, int CAPM, bool COMPACT>
+struct LbTileShared {
+    using type = std::conditional_t<COMPACT, MergeShared<T, CAPM, 6 * CAPM, 4>, MergeShared<T, CAPM>>;
+};
+template <int T, int CAPM, bool COMPACT>
+__global__ void __launch_bounds__(T, COMPACT ? 5 : 4) esc_window_lb2_kernel(
     Mats m, const int32_t* __restrict__ ids, const Window* __restrict__ wins, OutCtx out,
     int csort, LbCtx lb) {
-    using S = MergeShared<T, CAPM>;
+    using S = typename LbTileShared<T, CAPM, COMPACT>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S& s = *reinterpret_cast<S*>(smem_raw);
     __shared__ int s_tile;
@@ -2096,10 +2104,20 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
     // only by the work that leaves it: 170.5 / 165.6 / 154.5 / 135.7 / 108.2 ms
     // at dmax off / 2048 / 1024 / 512 / 256, step 287.4 / 288.1 / 288.5 / 291.6 /
     // 295.9 ms), so the wait is not caused by these tiles alone; off by default.
-    static const int lb_dmax = [] {
+    // BSP_LB_V2: form of the look-back tile (0: values gathered with the columns;
+    // 1: values after the count is published; 2: as 1 in the compact layout at 5
+    // CTAs per SM, rows of more than 65535 entries on the two-pass path)
+    static const int lb_v2 = [] {
+        const char* e = std::getenv("BSP_LB_V2");
+        return e ? std::atoi(e) : 2;  // measured on cfg5: 169.2 / 169.4 / 156.8 ms at 0 / 1 / 2
+    }();
+    static const int lb_dmax_env = [] {
         const char* e = std::getenv("BSP_LB_DMAX");
         return e ? std::atoi(e) : 0;  // measured: no gain (see below), off by default
     }();
+    const int lb_dmax = (lb_v2 == 2 && m.bnnz < (int64_t{1} << 32))
+                            ? (lb_dmax_env > 0 ? std::min(lb_dmax_env, 65535) : 65535)
+                            : lb_dmax_env;
     int32_t* const lb_list = plan.sparse_ids.p + plan.wcls_off[LBC];
     int64_t ntp = 0;           // two-pass windows: lb_list[nlb, nlb + ntp)
     int64_t lb_products = plan.wcls_prod[LBC];
@@ -2202,28 +2220,37 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
             return e ? std::atoi(e) : 1000;
         }();
         using S = MergeShared<256, 2048>;
-        // BSP_LB_V2=1: the second form (only the columns gathered before the sort,
-        // the values after the count is published).  Measured on cfg5: the wait for
-        // the predecessors' counts falls from 10.7K to 6.2K cycles per tile and the
-        // tile's residency from 54.1K to 49.7K cycles, but the kernel takes the same
-        // time (171.1 vs 170.4 ms): with more warps runnable at once the L1/shared
-        // memory pipe (61 % busy) and the issue slots (59 %) are what is left, so
-        // the first form stays the default.
-        static const bool lb_v2 = [] {
-            const char* e = std::getenv("BSP_LB_V2");
-            return e && e[0] == '1';
-        }();
-        if (lb_v2 && m.bnnz < (int64_t{1} << 32)) {
-            auto k = esc_window_lb2_kernel<256, 2048>;
+        // The second form (only the columns gathered before the sort, the values
+        // after the count is published) by itself — BSP_LB_V2=1 — cuts the wait for
+        // the predecessors' counts from 10.7K to 6.2K cycles per tile and the tile's
+        // residency from 54.1K to 49.7K cycles at the same kernel time (169.4 vs
+        // 169.2 ms); what it buys is the compact layout (6 bytes per product where
+        // the first form keeps an 8-byte value through the sort): 44.9 KB per tile,
+        // 5 CTAs per SM instead of 4 — the default, 156.8 ms.
+        if (lb_v2 == 2 && m.bnnz < (int64_t{1} << 32)) {
+            using S5 = LbTileShared<256, 2048, true>::type;
+            auto k = esc_window_lb2_kernel<256, 2048, true>;
+            set_smem(k, sizeof(S5));
+            BSP_LAUNCH_AS(h, "esc_window_lb2c<256,2048>", k, static_cast<unsigned>(nlb), 256,
+                          sizeof(S5), plan.with_starts(m), ids, plan.wins.p, out, csort,
+                          LbCtx{counter.p, status.p});
+        } else if (lb_v2 == 1 && m.bnnz < (int64_t{1} << 32)) {
+            auto k = esc_window_lb2_kernel<256, 2048, false>;
             set_smem(k, sizeof(S));
             BSP_LAUNCH_AS(h, "esc_window_lb2<256,2048>", k, static_cast<unsigned>(nlb), 256,
                           sizeof(S), plan.with_starts(m), ids, plan.wins.p, out, csort,
                           LbCtx{counter.p, status.p});
         } else {
+            // BSP_LB_PAD_SMEM=bytes: extra (unused) dynamic shared memory, to measure the
+            // tile's sensitivity to CTAs per SM (experiments only)
+            static const size_t pad = [] {
+                const char* e = std::getenv("BSP_LB_PAD_SMEM");
+                return e ? static_cast<size_t>(std::atoll(e)) : size_t{0};
+            }();
             auto k = esc_window_lb_kernel<256, 2048>;
-            set_smem(k, sizeof(S));
+            set_smem(k, sizeof(S) + pad);
             BSP_LAUNCH_AS(h, "esc_window_lb<256,2048>", k, static_cast<unsigned>(nlb), 256,
-                          sizeof(S), plan.with_starts(m), ids, plan.wins.p, out, csort,
+                          sizeof(S) + pad, plan.with_starts(m), ids, plan.wins.p, out, csort,
                           LbCtx{counter.p, status.p});
         }
         // final row_ptr and window offsets for the remaining numeric tiles

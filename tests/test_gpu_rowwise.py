@@ -344,7 +344,7 @@ print("ok")
 
 @pytest.mark.parametrize("env", [{"BSP_LB_V2": "1"}, {"BSP_LB_DMAX": "64"},
                                  {"BSP_LB_V2": "1", "BSP_LB_DMAX": "128"},
-                                 {"BSP_LOOKBACK": "0"}, {"BSP_BLOCK_CACHE": "0"}])
+                                 {"BSP_LOOKBACK": "0"}, {"BSP_BLOCK_CACHE": "0"}, {"BSP_LB_V2": "0"}])
 def test_lookback_knobs_bit_identical(env):
     """The look-back tile's second form (values gathered after the count is published), the
     split of long-row windows onto the two-pass path, the two-pass path alone and the block
