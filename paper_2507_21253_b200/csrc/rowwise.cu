@@ -59,7 +59,7 @@ __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restri
                                 uint8_t* __restrict__ cls, const uint8_t* __restrict__ skip,
                                 int64_t* __restrict__ class_count,
                                 int64_t* __restrict__ class_products, int shadow,
-                                unsigned long long* __restrict__ max_prod) {
+                                unsigned long long* __restrict__ max_prod, int heavy_above = 4096) {
     // shadow: skipped rows get their own classes NCLS + c (a second plan)
     __shared__ unsigned long long s_cnt[2 * NCLS], s_prod[2 * NCLS], s_max;
     if (threadIdx.x < 2 * NCLS) {
@@ -86,6 +86,7 @@ __global__ void products_kernel(Mats m, int64_t rb, int64_t n, int64_t* __restri
             if (P > 0) {
                 c = 1;
                 while (c < NCLS - 1 && P > kClassCap[c]) ++c;
+                if (P > heavy_above) c = NCLS - 1;  // planned into column windows
             }
             // skip 1: planned apart in the shadow plan; 2: counted elsewhere
             // (cluster union tiles count their own rows)
@@ -1340,9 +1341,20 @@ void build_plan(bsp_handle h, const Mats& m, int64_t rb, int64_t re,
     BSP_CUDA(cudaMemsetAsync(counters.p, 0, (2 * ncl + 1) * sizeof(int64_t), h->stream));
     const int grid = static_cast<int>(std::min<int64_t>(div_up(std::max<int64_t>(n, 1), 8),
                                                         int64_t{h->sm_count} * 8));
+    // BSP_HEAVY_ABOVE: rows with more products are planned into column windows
+    // (the shadow plan's rows stay light up to the largest row tile, 4096).
+    // Measured on cfg5 with the 5-CTA look-back tile: 273.8 / 270.2 / 271.0 /
+    // 274.4 ms at 4096 / 3072 / 2048 / 1024 — the 4096-product row tile (2 CTAs
+    // per SM, plus its symbolic pass) loses to windows on the look-back tile.
+    static const int heavy_above = [] {
+        const char* e = std::getenv("BSP_HEAVY_ABOVE");
+        const int v = e ? std::atoi(e) : 3072;
+        return v >= 128 && v <= 4096 ? v : 4096;
+    }();
     BSP_LAUNCH(h, products_kernel, grid, 256, 0, m, rb, n, prod_out, cls.p, skip, counters.p,
                counters.p + ncl, shadow ? 1 : 0,
-               reinterpret_cast<unsigned long long*>(counters.p + 2 * ncl));
+               reinterpret_cast<unsigned long long*>(counters.p + 2 * ncl),
+               shadow ? 4096 : heavy_above);
     int64_t hc[4 * NCLS + 1];
     d2h(h, hc, counters.p, 2 * ncl + 1);
     sync(h);
