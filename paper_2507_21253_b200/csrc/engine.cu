@@ -1,6 +1,9 @@
 // Handle, memory and transfer entry points of the C ABI, plus device-wide
 // scan helpers and the device transpose (reference csr.hpp:115-135).
 #include "engine.cuh"
+
+#include <mutex>
+#include <unordered_map>
 #include "esc.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -202,6 +205,30 @@ void small_readback(bsp_handle h, void* dst, const void* src, size_t bytes) {
 // the growth of this handle's own pools (cudaMemPoolGetAttribute, no device
 // lock), which is where a multiply's memory goes.  Memory taken by other users
 // of the device is seen at the next refresh.
+namespace {
+struct RegEntry {
+    bsp_handle owner;
+    size_t bytes;
+    int pool;
+};
+std::mutex g_reg_mu;
+std::unordered_map<void*, RegEntry> g_reg;
+}  // namespace
+void block_registry_put(void* p, bsp_handle owner, size_t bytes, int pool) {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_reg[p] = RegEntry{owner, bytes, pool};
+}
+bool block_registry_take(void* p, bsp_handle* owner, size_t* bytes, int* pool) {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    auto it = g_reg.find(p);
+    if (it == g_reg.end()) return false;
+    *owner = it->second.owner;
+    *bytes = it->second.bytes;
+    *pool = it->second.pool;
+    g_reg.erase(it);
+    return true;
+}
+
 size_t available_bytes(bsp_handle h, bool refresh) {
     uint64_t reserved_all = 0, unused = 0;
     for (cudaMemPool_t pool : {h->scratch_pool, h->out_pool}) {
@@ -286,6 +313,10 @@ int bsp_destroy(bsp_handle h) {
         if (h->comm) bsp_comm_destroy(h);
         flush_block_cache(h);
         if (h->keep_starts) {
+            bsp_handle o = nullptr;
+            size_t b = 0;
+            int pl = 0;
+            block_registry_take(h->keep_starts, &o, &b, &pl);
             cudaFreeAsync(h->keep_starts, h->stream);
             cudaStreamSynchronize(h->stream);
         }

@@ -64,13 +64,9 @@ struct bsp_handle_s {
     int64_t free_outside = -1;
     uint64_t free_reserved = 0;
     std::chrono::steady_clock::time_point free_time{};
-    // Block cache above the pools (see dalloc): freed blocks by (pool, bytes),
-    // live blocks by address.
-    struct BlockInfo {
-        size_t bytes;
-        int pool;
-    };
-    std::unordered_map<void*, BlockInfo> live_blocks;
+    // Block cache above the pools (see dalloc): freed blocks by (pool, bytes); live
+    // blocks are in a process-wide registry by address (a block may be freed
+    // through another handle, e.g. a copy-stream handle after its download).
     struct FreeBlock {
         void* p;
         uint64_t stamp;  // alloc_seq when it was freed
@@ -152,6 +148,11 @@ enum class Pool { scratch, out };
 
 void gap_slow_call(const char* what, double ms);
 
+// Live blocks of every handle, by address (engine.cu; mutex-guarded).
+void block_registry_put(void* p, bsp_handle owner, size_t bytes, int pool);
+// Removes p's entry; false when p is not a registered block.
+bool block_registry_take(void* p, bsp_handle* owner, size_t* bytes, int* pool);
+
 // Stream-ordered allocation with a per-handle block cache.  A repeated multiply
 // asks for the same block sizes again, and every driver allocation call — even
 // cudaMallocFromPoolAsync served from the pool's cached memory — takes driver
@@ -183,7 +184,7 @@ inline void* dalloc_bytes(bsp_handle h, size_t bytes, Pool pool) {
         void* p = it->second.p;
         h->free_blocks.erase(it);
         h->cached_bytes -= bytes;
-        h->live_blocks[p] = {bytes, pi};
+        block_registry_put(p, h, bytes, pi);
         return p;
     }
     // miss: stale blocks go back to the pool first
@@ -212,7 +213,7 @@ inline void* dalloc_bytes(bsp_handle h, size_t bytes, Pool pool) {
         gap_slow_call("cudaMallocFromPoolAsync",
                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
                           .count());
-    h->live_blocks[p] = {bytes, pi};
+    block_registry_put(p, h, bytes, pi);
     return p;
 }
 
@@ -224,24 +225,21 @@ T* dalloc(bsp_handle h, int64_t n, Pool pool = Pool::scratch) {
 
 inline void dfree(bsp_handle h, void* p) {
     if (!p) return;
-    auto it = h->live_blocks.find(p);
-    if (it == h->live_blocks.end()) {  // not this handle's block: plain stream-ordered free
-        cudaFreeAsync(p, h->stream);
-        return;
-    }
-    const auto info = it->second;
-    h->live_blocks.erase(it);
+    bsp_handle owner = nullptr;
+    size_t bytes = 0;
+    int pool = 0;
     static const bool cache_on = [] {
         const char* e = std::getenv("BSP_BLOCK_CACHE");
         return !(e && e[0] == '0');
     }();
-    if (!cache_on) {
+    // another handle's block (or not a registered one): plain stream-ordered free
+    if (!block_registry_take(p, &owner, &bytes, &pool) || owner != h || !cache_on) {
         cudaFreeAsync(p, h->stream);
         return;
     }
-    h->free_blocks.emplace((static_cast<uint64_t>(info.bytes) << 1) | static_cast<uint64_t>(info.pool),
+    h->free_blocks.emplace((static_cast<uint64_t>(bytes) << 1) | static_cast<uint64_t>(pool),
                            bsp_handle_s::FreeBlock{p, h->alloc_seq});
-    h->cached_bytes += info.bytes;
+    h->cached_bytes += bytes;
 }
 
 // Device bytes available to a new allocation: free HBM plus what the
