@@ -161,13 +161,15 @@ bool block_registry_take(void* p, bsp_handle* owner, size_t* bytes, int* pool);
 // inside a multiply, one step in five 5-15 % long).  Freed blocks are therefore
 // kept by exact size and handed back without a driver call.  A request the
 // cache cannot serve allocates from the pool; blocks that no request has
-// matched for kBlockMaxAge allocations go back to the pool then, and when the
+// matched for kBlockMaxAge allocations go back to the pool then (large cached
+// blocks at once when the missed request is itself large), and when the
 // pool is out of memory every cached block goes back before one retry (so a
 // different workload gets the memory it would have had without the cache;
 // available_bytes counts cached blocks as available).  All blocks of a handle
 // are used in its stream's order, like the stream-ordered frees they replace;
 // changing the stream or destroying the handle flushes the cache.
 constexpr uint64_t kBlockMaxAge = 4096;
+constexpr size_t kBigBlock = size_t{64} << 20;
 
 inline void flush_block_cache(bsp_handle h) {
     for (auto& kv : h->free_blocks) cudaFreeAsync(kv.second.p, h->stream);
@@ -187,9 +189,15 @@ inline void* dalloc_bytes(bsp_handle h, size_t bytes, Pool pool) {
         block_registry_put(p, h, bytes, pi);
         return p;
     }
-    // miss: stale blocks go back to the pool first
+    // miss: stale blocks go back to the pool first — and, for a large request,
+    // every large cached block of that pool: the pool then serves the request
+    // from their (still mapped) memory instead of growing by as much again
+    // (row-chunked multiplies: each chunk's C is tens of GB of a different size)
+    const bool big = bytes >= kBigBlock;
     for (auto jt = h->free_blocks.begin(); jt != h->free_blocks.end();) {
-        if (h->alloc_seq - jt->second.stamp > kBlockMaxAge) {
+        const size_t jb = static_cast<size_t>(jt->first >> 1);
+        const int jp = static_cast<int>(jt->first & 1u);
+        if (h->alloc_seq - jt->second.stamp > kBlockMaxAge || (big && jp == pi && jb >= kBigBlock)) {
             cudaFreeAsync(jt->second.p, h->stream);
             h->cached_bytes -= static_cast<size_t>(jt->first >> 1);
             jt = h->free_blocks.erase(jt);
