@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
         // packed scan: low 16 bits product offset, high 16 bits run index
         const int packed = seg * nl | (nl << 16);
         int off, agg;
-        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(packed, off, agg);
         x.pstart[tid] = start;
         x.poff[tid] = total + (off & 0xffff);
         slot_sm[tid] = make_uint2(static_cast<uint32_t>(seg), nl ? msk : 0u);
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
     __syncthreads();
     const int v = tid < nrows * NW ? cnt[tid] : 0;
     int pre, tile_cnt;
-    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(v, pre, tile_cnt);
+    cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(v, pre, tile_cnt);
     __syncthreads();
     if (tid < nrows * NW) cnt[tid] = pre;
     __syncthreads();
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
         }
         const int packed = len | ((len > 0) << 16);
         int off, agg;
-        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(packed, off, agg);
         const int r = off >> 16;
         if (len > 0) {
             if (nruns + r < S::MAXRUNS)

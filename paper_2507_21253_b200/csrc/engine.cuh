@@ -169,7 +169,10 @@ bool block_registry_take(void* p, bsp_handle* owner, size_t* bytes, int* pool);
 // are used in its stream's order, like the stream-ordered frees they replace;
 // changing the stream or destroying the handle flushes the cache.
 constexpr uint64_t kBlockMaxAge = 4096;
-constexpr size_t kBigBlock = size_t{64} << 20;
+// Only blocks this large are returned on a large miss: returning smaller ones made
+// a repeated multiply cycle (block X released for a miss on Y, Y released for the
+// next step's miss on X, ...: two driver allocations per step came back).
+constexpr size_t kBigBlock = size_t{1} << 30;
 
 inline void flush_block_cache(bsp_handle h) {
     for (auto& kv : h->free_blocks) cudaFreeAsync(kv.second.p, h->stream);
@@ -207,6 +210,7 @@ inline void* dalloc_bytes(bsp_handle h, size_t bytes, Pool pool) {
     }
     void* p = nullptr;
     const bool lg = gap_log_enabled();
+    if (lg) std::fprintf(stderr, "[miss] %zu bytes pool %d (%zu blocks cached)\n", bytes, pi, h->free_blocks.size());
     const auto t0 = lg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
     cudaMemPool_t mp = pool == Pool::out ? h->out_pool : h->scratch_pool;
     cudaError_t me = cudaMallocFromPoolAsync(&p, bytes, mp, h->stream);

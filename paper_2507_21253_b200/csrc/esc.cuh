@@ -10,6 +10,11 @@
 #include <mutex>
 #include <unordered_map>
 
+// Block scan algorithm of the tiles (A/B: -DBSP_SCAN_ALGO=cub::BLOCK_SCAN_WARP_SCANS)
+#ifndef BSP_SCAN_ALGO
+#define BSP_SCAN_ALGO cub::BLOCK_SCAN_RAKING
+#endif
+
 namespace bsp {
 
 constexpr int CAP = 4096;     // max products of one sparse tile (smem ESC)

@@ -111,7 +111,7 @@ struct MergeShared {
     __device__ __forceinline__ Ex& ex() {
         if constexpr (EX_IN_U) return u.x; else return xo;
     }
-    typename cub::BlockScan<int32_t, T>::TempStorage scan;
+    typename cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>::TempStorage scan;
     int nruns;
 };
 
@@ -249,7 +249,7 @@ __device__ __forceinline__ int expand_runs(const Mats& m, int32_t row, int32_t c
         // packed scan: low 16 bits offset, high 16 bits run index
         const int packed = len | ((len > 0) << 16);
         int off, agg;
-        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(packed, off, agg);
         // compact the non-empty segments of this chunk (run order = k order)
         const int r = off >> 16;
         if (len > 0) {
@@ -348,7 +348,7 @@ __device__ __forceinline__ int expand_keys(const Mats& m, int32_t c0, int32_t c1
         }
         const int packed = len | ((len > 0) << 16);
         int off, agg;
-        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(packed, off, agg);
         const int r = off >> 16;
         if (len > 0) {
             if (nruns + r < MergeShared<T, CAPM, VB, RBO>::MAXRUNS)
@@ -522,7 +522,7 @@ __device__ __forceinline__ bool msd_sort_tile(MergeShared<T, CAPM, VB, RBO>& s, 
         run += static_cast<int>(loc[i]);
     }
     int base, agg;
-    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(run, base, agg);
+    cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(run, base, agg);
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         s.hist[tid * PER + i] = static_cast<uint32_t>(base);
@@ -664,7 +664,7 @@ __device__ __forceinline__ bool count_sort_tile(MergeShared<T, CAPM, VB, RBO>& s
         run += static_cast<int>(loc[j]);
     }
     int base, agg;
-    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(run, base, agg);
+    cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(run, base, agg);
     __syncthreads();  // all counters read before they become offsets
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
@@ -940,7 +940,7 @@ __device__ __forceinline__ int reduce_and_write(MergeShared<T, CAPM, VB, RBO>& s
     __syncthreads();
     const int v = threadIdx.x < nrows * NW ? cnt[threadIdx.x] : 0;
     int pre, tile_cnt;
-    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(v, pre, tile_cnt);
+    cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(v, pre, tile_cnt);
     __syncthreads();
     if (threadIdx.x < nrows * NW) cnt[threadIdx.x] = pre;
     if constexpr (LB) {
@@ -1058,7 +1058,7 @@ __device__ __forceinline__ int reduce_lb2(MergeShared<T, CAPM, VB, RBO>& s, int 
     __syncthreads();
     const int v = threadIdx.x < nrows * NW ? cnt[threadIdx.x] : 0;
     int pre, tile_cnt;
-    cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(v, pre, tile_cnt);
+    cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(v, pre, tile_cnt);
     __syncthreads();
     if (threadIdx.x < nrows * NW) cnt[threadIdx.x] = pre;
     if (threadIdx.x == 0) publish(tile_cnt);

@@ -758,8 +758,10 @@ __global__ void __launch_bounds__(T, COMPACT ? 5 : 4) esc_window_lb2_kernel(
     if (threadIdx.x == 0) s_tile = atomicAdd(lb.counter, 1);
     __syncthreads();
     const int t = s_tile;
-    const int32_t w = ids[t];
-    const Window wd = wins[w];
+    // ids == nullptr: `wins` is the list's windows gathered in list order (one
+    // dependent load less at the start of every tile), the window id in pad_
+    const Window wd = ids ? wins[ids[t]] : wins[t];
+    const int32_t w = ids ? ids[t] : wd.pad_;
 #ifdef BSP_X_PHASE
     if (threadIdx.x == 0) {
         const int b = blockIdx.x & ((1 << 22) - 1);
@@ -802,7 +804,7 @@ struct HashShared {
     alignas(16) int32_t table[TS];
     int32_t stage[STAGED ? CAPM : 1];  // gathered columns of the current chunk
     typename cub::BlockReduce<int32_t, T>::TempStorage red;
-    typename cub::BlockScan<int32_t, T>::TempStorage scan;
+    typename cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>::TempStorage scan;
     int64_t pstart[T];
     int32_t poff[T + 1];
 };
@@ -862,7 +864,7 @@ __global__ void __launch_bounds__(T) hash_count_kernel(Mats m, const int32_t* __
         const int packed = len | ((len > 0) << 16);
         int off, agg;
         __syncthreads();
-        cub::BlockScan<int32_t, T>(s.scan).ExclusiveSum(packed, off, agg);
+        cub::BlockScan<int32_t, T, BSP_SCAN_ALGO>(s.scan).ExclusiveSum(packed, off, agg);
         if (len > 0) {
             s.pstart[off >> 16] = start;
             s.poff[off >> 16] = off & 0xffff;
@@ -2052,6 +2054,16 @@ void narrow64_rows(bsp_handle h, const Mats& m, const unsigned long long* mask, 
                       mask, int64_t{0}, n, nullptr, crp, ccol, cval, nullptr, skip, nx.p);
 }
 
+// The look-back list's windows in list order (id kept in pad_).
+__global__ void gather_windows_kernel(const int32_t* __restrict__ ids, int64_t n,
+                                      const Window* __restrict__ wins, Window* __restrict__ out) {
+    const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+    if (i >= n) return;
+    Window w = wins[ids[i]];
+    w.pad_ = ids[i];
+    out[i] = w;
+}
+
 // Look-back list split (rowwise_multiply): windows whose A row has at most dmax
 // segments stay on the look-back tile.
 struct WindowShortRow {
@@ -2243,9 +2255,20 @@ void rowwise_multiply(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int64_t 
             using S5 = LbTileShared<256, 2048, true>::type;
             auto k = esc_window_lb2_kernel<256, 2048, true>;
             set_smem(k, sizeof(S5));
+            // BSP_LB_GATHER=0: tiles read their window through the id list
+            static const bool gather = [] {
+                const char* e = std::getenv("BSP_LB_GATHER");
+                return !(e && e[0] == '0');
+            }();
+            DBuf<Window> lbw;
+            if (gather) {
+                lbw = DBuf<Window>(h, nlb);
+                BSP_LAUNCH(h, gather_windows_kernel, static_cast<unsigned>(div_up(nlb, 256)), 256, 0,
+                           ids, nlb, plan.wins.p, lbw.p);
+            }
             BSP_LAUNCH_AS(h, "esc_window_lb2c<256,2048>", k, static_cast<unsigned>(nlb), 256,
-                          sizeof(S5), plan.with_starts(m), ids, plan.wins.p, out, csort,
-                          LbCtx{counter.p, status.p});
+                          sizeof(S5), plan.with_starts(m), gather ? nullptr : ids,
+                          gather ? lbw.p : plan.wins.p, out, csort, LbCtx{counter.p, status.p});
         } else if (lb_v2 == 1 && m.bnnz < (int64_t{1} << 32)) {
             auto k = esc_window_lb2_kernel<256, 2048, false>;
             set_smem(k, sizeof(S));
