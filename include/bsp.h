@@ -123,7 +123,9 @@ typedef struct {
                              of which union tiles (each B entry sorted once per cluster),
                              [12] two-row clusters on the cluster hash accumulator, [13]
                              rows of duplicate-heavy clusters whose B-row reuse is too low
-                             to pay, run on the row-wise hash accumulator */
+                             to pay, run on the row-wise hash accumulator, [14] device
+                             allocations the call had to ask the driver for (0 once a
+                             repeated multiply is served from the handle's block cache) */
     int32_t kernels_launched;
     int32_t chunks;       /* row chunks: bsp_spgemm_rowwise_host splits A's rows when C
                              exceeds the device budget (half the free memory); 1 otherwise */

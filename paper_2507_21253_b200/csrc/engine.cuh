@@ -209,6 +209,7 @@ inline void* dalloc_bytes(bsp_handle h, size_t bytes, Pool pool) {
         }
     }
     void* p = nullptr;
+    ++h->stats.units[14];  // a driver allocation inside this call
     const bool lg = gap_log_enabled();
     if (lg) std::fprintf(stderr, "[miss] %zu bytes pool %d (%zu blocks cached)\n", bytes, pi, h->free_blocks.size());
     const auto t0 = lg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};

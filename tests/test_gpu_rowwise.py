@@ -356,3 +356,25 @@ def test_lookback_knobs_bit_identical(env):
     r = subprocess.run([sys.executable, "-c", _LB_KNOB_SCRIPT], env=e, capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_repeated_multiply_makes_no_driver_allocation(engine):
+    """A repeated multiply is served from the handle's block cache: after the first calls no
+    allocation reaches the driver (exec_stats units[14]); such calls wait on the driver's
+    locks whenever a GPU monitor polls, which showed as 5-300 % long steps in the bench."""
+    a = B.make_config(5, 15)
+    A = engine.upload(a)
+    misses = []
+    for _ in range(4):
+        c = engine.spgemm_rowwise(A, A)
+        misses.append(engine.exec_stats()["units"][14])
+        c.free()
+    assert misses[0] > 0 and misses[2] == 0 and misses[3] == 0, misses
+    asg = engine.hierarchical_clusters(a)
+    Ac = engine.build_csr_cluster(A, asg)
+    misses = []
+    for _ in range(4):
+        c = engine.spgemm_clusterwise(Ac, A)
+        misses.append(engine.exec_stats()["units"][14])
+        c.free()
+    assert misses[2] == 0 and misses[3] == 0, misses
