@@ -489,20 +489,29 @@ __global__ void __launch_bounds__(T, CAPM == 3072 ? 3 : (T >= 256 ? (CAPM <= 204
 // Sort work drops from P (member products) to S (B entries loaded): cfg2's
 // clusters load each template column's B row once for 8 members.
 // ---------------------------------------------------------------------------
-template <int T, int CAPM>
+// The small tile (<= 1024 entries, <= 256 merged columns, <= 8 members) keeps its
+// per-entry and per-column maps in bytes, stages half as many A values and sorts
+// with 4-bit radix digits: 31.9 KB = 7 CTAs per SM (38.6 KB = 5 before; the tile
+// is latency bound like the row tiles).
+template <int T, int CAPM, bool TMA>
 struct UnionShared {
-    MergeShared<T, CAPM> m;
-    alignas(4) uint16_t pidx[CAPM];  // merged column (local) of each expanded entry
-                                     // (TMA: uint32 per 4 staged entries, shift << 16 | column)
-    // the small tile stages half as many (38.6 -> 33.5 KB: 6 CTAs per SM instead of 5)
-    static constexpr int MAXA = CAPM <= 1024 ? UMAXA / 2 : UMAXA;
-    static constexpr int MAXMC = CAPM <= 1024 ? UMAXMC / 2 : UMAXMC;
+    static constexpr bool SMALL = CAPM <= 1024;
+    using MS = MergeShared<T, CAPM, 8 * CAPM, SMALL ? 4 : 0>;
+    using pidx_t = std::conditional_t<SMALL, uint8_t, uint16_t>;
+    using mask_t = std::conditional_t<SMALL, uint8_t, uint32_t>;
+    MS m;
+    alignas(4) pidx_t pidx[CAPM];  // merged column (local) of each expanded entry
+                                   // (TMA: uint32 per 4 staged entries, shift << 16 | column)
+    static constexpr int MAXA = SMALL ? UMAXA / 2 : UMAXA;
+    static constexpr int MAXMC = SMALL ? UMAXMC / 2 : UMAXMC;
     double sa[MAXA];         // the cluster's A values, [p * K + l]
-    uint32_t smask[MAXMC];   // live members of merged column p
-    int16_t runp[T];         // merged column of each compacted run of the chunk
+    mask_t smask[MAXMC];     // live members of merged column p (K <= 8)
+    pidx_t runp[T];          // merged column of each compacted run of the chunk
     unsigned long long cnt[2][((CAPM + T - 1) / T) * (T / 32)];  // packed member counts
     int64_t mbase[UMAXK];
-    typename cub::BlockScan<unsigned long long, T>::TempStorage scan64;  // TMA staging offsets
+    struct NoScan {};
+    std::conditional_t<TMA, typename cub::BlockScan<unsigned long long, T>::TempStorage, NoScan>
+        scan64;  // TMA staging offsets
 };
 
 //
@@ -516,12 +525,12 @@ struct UnionShared {
 // per-4-entries merged-column map stay where the copy put them).  Rows whose
 // superset would reach past nnz(B) are staged with plain loads.
 template <int T, int CAPM, bool TMA>
-__global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
+__global__ void __launch_bounds__(T, T >= 256 ? 3 : (TMA ? 6 : 7))
     cluster_union_kernel(ClusterMats m, const int32_t* __restrict__ ids, int csort,
                          const int64_t* __restrict__ crp, int32_t* __restrict__ ocol,
                          double* __restrict__ oval) {
-    using U = UnionShared<T, CAPM>;
-    using S = MergeShared<T, CAPM>;
+    using U = UnionShared<T, CAPM, TMA>;
+    using S = typename U::MS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     U& us = *reinterpret_cast<U*>(smem_raw);
     S& s = us.m;
@@ -535,7 +544,8 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
     const int64_t vbase = m.vptr[c];
     if (tid < K) us.mbase[tid] = crp[m.row_map[m.member_ptr[c] + tid]];
     for (int q = tid; q < MC * K; q += T) us.sa[q] = __ldg(m.aval + vbase + q);
-    for (int q = tid; q < MC; q += T) us.smask[q] = __ldg(m.mask + u0 + q);
+    for (int q = tid; q < MC; q += T)
+        us.smask[q] = static_cast<typename U::mask_t>(__ldg(m.mask + u0 + q));
     int total = 0, nruns = 0;
     if constexpr (TMA) {
         __shared__ __align__(8) uint64_t mbar;
@@ -628,7 +638,7 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
                 s.ro(0)[nruns + r] = static_cast<uint16_t>(total + (off & 0xffff));
             x.pstart[r] = start;
             x.poff[r] = off & 0xffff;
-            us.runp[r] = static_cast<int16_t>(uc + tid - u0);
+            us.runp[r] = static_cast<typename U::pidx_t>(uc + tid - u0);
         }
         const int nr = agg >> 16, ct = agg & 0xffff;
         if (tid == 0) x.poff[nr] = ct;
@@ -644,7 +654,7 @@ __global__ void __launch_bounds__(T, T >= 256 ? 3 : 6)
                     const int g = total + e;
                     cp_async4(&s.key0[PADI(g)], m.bcol + src);
                     cp_async8(&s.val[g], m.bval + src);
-                    us.pidx[g] = static_cast<uint16_t>(us.runp[q]);
+                    us.pidx[g] = us.runp[q];
                 }
             }
             cp_async_wait_all();
@@ -861,7 +871,6 @@ template <int T, int CAPM>
 void launch_union(bsp_handle h, const ClusterMats& m, const int32_t* ids, int64_t n,
                   const int64_t* crp, int32_t* ocol, double* oval) {
     if (n <= 0) return;
-    using U = UnionShared<T, CAPM>;
     static const std::string nm =
         "cluster_union<" + std::to_string(T) + "," + std::to_string(CAPM) + ">";
     static const std::string nm_tma =
@@ -871,11 +880,13 @@ void launch_union(bsp_handle h, const ClusterMats& m, const int32_t* ids, int64_
         return e ? std::atoi(e) : 1000;
     }();
     if (union_tma(m)) {
+        using U = UnionShared<T, CAPM, true>;
         auto k = cluster_union_kernel<T, CAPM, true>;
         set_smem(k, sizeof(U));
         BSP_LAUNCH_AS(h, nm_tma.c_str(), k, static_cast<unsigned>(n), T, sizeof(U), m, ids, csort,
                       crp, ocol, oval);
     } else {
+        using U = UnionShared<T, CAPM, false>;
         auto k = cluster_union_kernel<T, CAPM, false>;
         set_smem(k, sizeof(U));
         BSP_LAUNCH_AS(h, nm.c_str(), k, static_cast<unsigned>(n), T, sizeof(U), m, ids, csort, crp,
