@@ -363,6 +363,7 @@ def test_repeated_multiply_makes_no_driver_allocation(engine):
     allocation reaches the driver (exec_stats units[14]); such calls wait on the driver's
     locks whenever a GPU monitor polls, which showed as 5-300 % long steps in the bench."""
     a = B.make_config(5, 15)
+    engine = B.Engine(0)  # a fresh handle: its first multiply has to allocate
     A = engine.upload(a)
     misses = []
     for _ in range(4):
