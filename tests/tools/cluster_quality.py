@@ -11,7 +11,7 @@ reference) has no oracle, so it is judged by
 The planted group of each (permuted) row is recovered by permuting an identity
 matrix with the generator's own row permutation (reorder_random(n, perm_seed)).
 
-usage: python tools/cluster_quality.py [--scale NT] [--steps K] [--ref]  (one JSON line)
+usage: python tests/tools/cluster_quality.py [--scale NT] [--steps K] [--ref]  (one JSON line)
 """
 import argparse
 import json
@@ -19,7 +19,7 @@ import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 

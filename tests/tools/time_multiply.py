@@ -1,12 +1,13 @@
-"""Time row-wise / cluster-wise / row-chunked multiplies of a BASELINE config on cuda:0
+"""(Lives under tests/: --check uses the oracle as the checker.)
+Time row-wise / cluster-wise / row-chunked multiplies of a BASELINE config on cuda:0
 (CUDA events on the engine stream, per step), with an optional per-kernel event profile and
 an oracle check.  Used for the A/B runs and ncu captures recorded in profiles/.
 
-usage: python tools/time_multiply.py [--cfg 5] [--scale S] [--steps K] [--warmup W] [--prof]
+usage: python tests/tools/time_multiply.py [--cfg 5] [--scale S] [--steps K] [--warmup W] [--prof]
        [--cluster] [--rcm] [--chunks N] [--check] [--tag T]
 """
 import argparse, json, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_2507_21253_b200 as B
 ap = argparse.ArgumentParser()
