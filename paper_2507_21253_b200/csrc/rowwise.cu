@@ -2493,7 +2493,7 @@ int bsp_spgemm_rowwise_host(bsp_handle h, const bsp_host_csr* A, const bsp_host_
 // Partition cost of a row with P intermediate products (the rule
 // distributed.product_split mirrors).
 constexpr int64_t row_cost(int64_t P) {
-    return P > 65536 ? 3 * P : (P > 4096 ? 2 * P : P);
+    return P > 65536 ? 2 * P : P;
 }
 
 int bsp_partition_rows(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int32_t nparts,
@@ -2506,10 +2506,12 @@ int bsp_partition_rows(bsp_handle h, const bsp_csr* A, const bsp_csr* B, int32_t
         const int rc = bsp_spgemm_products(h, A, B, prod.p, &total);
         if (rc != BSP_OK) throw std::runtime_error(bsp_last_error());
         BSP_CUDA(cudaMemsetAsync(prod.p + n, 0, sizeof(int64_t), h->stream));
-        // Split on a per-row cost, not the raw product count: a heavy row's
-        // products (> 4096, planned into windows, counted by the window
-        // symbolic) cost about twice a light row's, the hub rows' (> 65536)
-        // three times (measured per-shard times, tools/shard_projection.py).
+        // Split on a per-row cost, not the raw product count: a hub row's
+        // products (> 65536 per row: dense windows, long A rows) cost about
+        // twice the others'.  Fitted to the per-shard times of the 2/4/8-way
+        // splits (tools/shard_projection.py, round 2): 21.2 / 19.7 / 40.7 ms per
+        // 1e9 products of light / windowed / hub rows + 6 ms per shard (round
+        // 1's tiles: windowed rows 2x, hub rows 3x).
         std::vector<int64_t> hp(n);
         d2h(h, hp.data(), prod.p, n);
         sync(h);

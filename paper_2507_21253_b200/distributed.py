@@ -21,11 +21,12 @@ import numpy as np
 
 
 def row_cost(row_products: np.ndarray) -> np.ndarray:
-    """Partition cost of each row (bsp_partition_rows' rule): a heavy row's
-    products (> 4096: planned windows + window symbolic) cost ~2 light ones,
-    a hub row's (> 65536) ~3 (per-shard timings, tools/shard_projection.py)."""
+    """Partition cost of each row (bsp_partition_rows' rule): a hub row's products
+    (> 65536 per row) cost ~2x the others' (fitted to per-shard timings,
+    tools/shard_projection.py: 21.2 / 19.7 / 40.7 ms per 1e9 products of light /
+    windowed / hub rows)."""
     rp = np.asarray(row_products, dtype=np.int64)
-    return np.where(rp > 65536, 3 * rp, np.where(rp > 4096, 2 * rp, rp))
+    return np.where(rp > 65536, 2 * rp, rp)
 
 
 def product_split(row_products: np.ndarray, nparts: int) -> np.ndarray:

@@ -85,7 +85,7 @@ def test_product_split_rule():
     for parts in (2, 3, 5):
         b = D.product_split(prods, parts)
         assert b[0] == 0 and b[-1] == prods.size and np.all(np.diff(b) >= 0)
-        cost = np.array([3 * p if p > 65536 else (2 * p if p > 4096 else p) for p in prods])
+        cost = np.array([2 * p if p > 65536 else p for p in prods])
         pre = np.concatenate([[0], np.cumsum(cost)])
         for g in range(1, parts):  # first row whose exclusive cost prefix reaches total*g/parts
             t = cost.sum() * g // parts
